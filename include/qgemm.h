@@ -1,0 +1,113 @@
+/*
+ * qgemm.h -- C ABI of the B200-native quaternion GEMM library (libqgemm.so).
+ *
+ * Operation (arXiv 1903.05575 = PAPER.md; "P:n" = PAPER.md line n):
+ *
+ *     C <- alpha * op(A) * op(B) + beta * C                Eq. general_gemm
+ *
+ * over the Hamilton quaternions H (Eq. quaternion_def, product
+ * Eq. quaternion_prod), op(X) in {X, X^T, X^H}, where
+ * (X^H)_{mu nu} = conj(X_{nu mu}) and conj is Eq. quaternion_conj
+ * (P:330-334).  op(A) is M x K, op(B) is K x N, C is M x N.
+ *
+ * Scalars: alpha and beta are quaternions applied FROM THE LEFT,
+ *     (q P Q)_{mu nu} = q * sum_k P_{mu k} Q_{k nu}
+ * (reading R2).  A real scalar r is passed as {r, 0, 0, 0}.
+ *
+ * Storage: column-major; element (i, j) of a stored
+ * matrix X with leading dimension ldx occupies the 4 consecutive scalars
+ *     X[4*(i + j*ldx) + c],  c = 0..3  (components q^0, q^1, q^2, q^3).
+ * Leading dimensions are counted in QUATERNIONS:
+ *     lda >= max(1, M) for transA = 'N', else lda >= max(1, K)
+ *     ldb >= max(1, K) for transB = 'N', else ldb >= max(1, N)
+ *     ldc >= max(1, M)
+ * Rows beyond the logical extent (the ld padding) are never read or written.
+ *
+ * op characters: 'N' (no-op), 'T' (transpose, no conjugation), 'H' or 'C'
+ * (conjugate transpose), case-insensitive (reading R6).
+ *
+ * Ownership: A, B, C and workspace are caller-owned DEVICE pointers on the
+ * device current for the calling thread; alpha and beta are HOST pointers to 4
+ * scalars, read before the call returns.  The library allocates nothing, and
+ * keeps no reference to any argument once the enqueued work has completed.
+ * `stream` is a cudaStream_t (NULL = legacy default stream).
+ *
+ * Asynchrony: the call validates, enqueues the pack / mainloop / epilogue
+ * kernels on `stream` and returns.  Faults that happen while the kernels run
+ * surface at the caller's next synchronisation on that stream.
+ *
+ * Quick returns (BLAS convention; reading R4):
+ *     M == 0 or N == 0      -> returns 0, enqueues nothing;
+ *     alpha == 0 or K == 0  -> C <- beta * C (one elementwise kernel);
+ *     beta == 0             -> C is overwritten and never read (NaN in C does
+ *                              not propagate; reading R3).
+ *
+ * Error convention (LAPACK "info" style; reading R7):
+ *     0   success (work enqueued)
+ *    -i   the i-th argument is invalid, numbering
+ *           transA=1 transB=2 M=3 N=4 K=5 alpha=6 A=7 lda=8 B=9 ldb=10
+ *           beta=11 C=12 ldc=13 workspace=14 workspace_bytes=15 stream=16;
+ *         a C extent overlapping the A or B extent returns -12;
+ *         NULL A/B are accepted only when they are not read (K == 0 or alpha == 0);
+ *         pointers not aligned to their scalar type return -7/-9/-12/-14.
+ *    >0   a cudaError_t raised while enqueueing.
+ * Nothing is enqueued when the return value is non-zero.
+ *
+ * Workspace: qgemm_workspace_bytes() returns the size that lets the call pack
+ * all of op(A) and op(B) at once.  A smaller workspace is accepted down to the
+ * size of a single K-panel (qgemm_workspace_min_bytes); the call then loops over
+ * K-panels (Alg. 2 kappa loop), applying beta on the first panel and
+ * accumulating onto C afterwards.  Smaller -> -15.
+ * The workspace must be 256-byte aligned (-14 otherwise).
+ */
+#ifndef QGEMM_B200_H
+#define QGEMM_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* FP64: computes in double on the FP64 tensor pipe (DMMA). */
+int qgemm(char transA, char transB, int64_t M, int64_t N, int64_t K,
+          const double alpha[4], const double *A, int64_t lda,
+          const double *B, int64_t ldb, const double beta[4],
+          double *C, int64_t ldc,
+          void *workspace, size_t workspace_bytes, void *stream);
+
+/* FP32: same contract with float storage and float arithmetic (FP32 FMA). */
+int qgemm_f32(char transA, char transB, int64_t M, int64_t N, int64_t K,
+              const float alpha[4], const float *A, int64_t lda,
+              const float *B, int64_t ldb, const float beta[4],
+              float *C, int64_t ldc,
+              void *workspace, size_t workspace_bytes, void *stream);
+
+/* Workspace bytes for a single-panel call (dtype 0 = FP64, 1 = FP32).
+ * Returns 0 for quick-return shapes and for invalid arguments. */
+size_t qgemm_workspace_bytes(char transA, char transB, int64_t M, int64_t N, int64_t K, int dtype);
+
+/* Smallest accepted workspace (one K-panel), same arguments. */
+size_t qgemm_workspace_min_bytes(char transA, char transB, int64_t M, int64_t N, int64_t K, int dtype);
+
+/* Debug/cross-check path: one thread per output quaternion, reads op(A) and
+ * op(B) in place (no pack, no workspace).  Same arguments, errors and
+ * semantics as qgemm() minus the workspace.  Not used by qgemm(). */
+int qgemm_naive(char transA, char transB, int64_t M, int64_t N, int64_t K,
+                const double alpha[4], const double *A, int64_t lda,
+                const double *B, int64_t ldb, const double beta[4],
+                double *C, int64_t ldc, void *stream);
+
+/* Number of kernels the last successful call on this host thread enqueued
+ * (for the bench's gpu_launches count). */
+int qgemm_last_launch_count(void);
+
+/* Library version string. */
+const char *qgemm_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* QGEMM_B200_H */
