@@ -103,6 +103,15 @@ int qgemm_naive(char transA, char transB, int64_t M, int64_t N, int64_t K,
  * (for the bench's gpu_launches count). */
 int qgemm_last_launch_count(void);
 
+/* Instrumentation (off by default).  While enabled, every kernel this host
+ * thread enqueues is bracketed by two CUDA events recorded on the same stream.
+ * qgemm_timing_collect() synchronises on those events, writes the summed
+ * milliseconds and launch counts per kernel kind into ms[4] / counts[4]
+ * (0 = pack, 1 = mainloop (DMMA or FP32), 2 = beta-scale, 3 = naive), clears
+ * the record and returns 0 (or a cudaError_t).  Host arrays, caller-owned. */
+void qgemm_timing_enable(int on);
+int qgemm_timing_collect(double ms[4], int counts[4]);
+
 /* Library version string. */
 const char *qgemm_version(void);
 

@@ -30,7 +30,8 @@
  *     by exactly one thread in the same order, so the result is independent of
  *     the thread count.
  *
- * Everything is FP64, compiled with -O2 -fno-fast-math -ffp-contract=off.
+ * Everything is FP64, compiled with -O3 -fno-fast-math -ffp-contract=off (IEEE
+ * semantics, no reassociation, no FMA contraction).
  *
  * Parity pins: see tests/test_oracle_pins.py (basis table, worked product, norm,
  * associativity, (AB)^H = B^H A^H, chi-embedding vs numpy complex GEMM, complex and
@@ -46,7 +47,7 @@
 #endif
 
 /* Levi-Civita symbol eps_{ij}^k for i,j,k in {1,2,3} (Eq. quaternion_alg). */
-static int levi_civita(int i, int j, int k) {
+static inline int levi_civita(int i, int j, int k) {
   if (i == j || j == k || i == k) return 0;
   /* even permutations of (1,2,3): (1,2,3), (2,3,1), (3,1,2) */
   if ((i == 1 && j == 2 && k == 3) || (i == 2 && j == 3 && k == 1) ||

@@ -1,0 +1,20 @@
+"""B200-native quaternion GEMM (arXiv 1903.05575 hot path).
+
+C <- alpha op(A) op(B) + beta C over Hamilton quaternions, op in {N, T, H},
+column-major interleaved storage; FP64 on the FP64 tensor pipe (DMMA), FP32 on
+FFMA.  The computation lives in libqgemm.so (include/qgemm.h); this package is
+the thin Python binding plus the multi-GPU row-block driver.
+"""
+from ._lib import EXPORTS, QgemmError, SO_PATH, load  # noqa: F401
+from .qgemm import (  # noqa: F401
+    get_workspace,
+    last_launch_count,
+    qgemm,
+    qgemm_f32,
+    qgemm_naive,
+    timing_collect,
+    timing_enable,
+    version,
+    workspace_bytes,
+    workspace_min_bytes,
+)

@@ -1,0 +1,170 @@
+// qg_dmma.cuh -- FP64 mainloop on the FP64 tensor pipe (DMMA.8x8x4) with the
+// alpha/beta epilogue fused (SURVEY.md §8(a) rows a4 "Mainloop" and a5 "Epilogue").
+//
+// PAPER.md: the micro-kernel of Alg. 3 accumulates a register
+// block C_r as a sum of rank-1 updates over k (Eq. micro_kernel);
+// the quaternion product of each update is the 16-FMA Hamilton rule
+// (Eq. quaternion_prod; batch form Eqs. simd_batch_mul*).
+//
+// B200 form.  Component planes make the quaternion product a sum of 16 real
+// matrix products per output tile (derived from P:274-309):
+//     D^{p XOR s} += eps(p,s) * A^p * B^s,     p, s in {0,1,2,3},
+// evaluated with mma.sync.m8n8k4.f64 (SASS DMMA.8x8x4), which measured
+// 37.0 TFLOP/s on B200 vs 33.8 for DFMA (tools/microbench/fp64_pipes.cu).
+// The sign is applied by feeding -B^s (one sign flip per fragment, reused by
+// every m8 tile of the warp), so each A^p/B^s fragment loaded from shared
+// memory is reused across all four output components (north star).
+//
+// CTA: 64x64 output quaternions, 8 consumer warps (2 in m x 4 in n, each a
+// 32x16 warp tile = 4x2 m8n8 tiles x 4 components = 64 f64 accumulators per
+// lane) + 1 producer warp that streams packed chunks (qg_pack.cuh FragLayout)
+// through a 3-stage shared-memory ring with 1-D bulk copies (cp.async.bulk,
+// SASS UBLKCP) completing on mbarriers.  Epilogue: alpha (x) acc + beta (x) C,
+// left products, masked at the M/N edges, C re-interleaved in
+// registers (each lane owns whole quaternions).
+#pragma once
+#include "qg_pack.cuh"
+
+namespace qg {
+
+constexpr int kStages = 3;
+constexpr int kConsumerWarps = 8;
+constexpr int kDmmaThreads = (kConsumerWarps + 1) * 32;
+constexpr int kGroupM = 8;  // rasterisation: 8 M-tiles share each B panel in flight
+constexpr size_t kDmmaSmemBytes = size_t(kStages) * 2 * kChunkElems * sizeof(double) + 2 * kStages * 8;
+
+struct DmmaArgs {
+  const double *Ap;  // packed A panel: MT x KT chunks
+  const double *Bp;  // packed B panel: NT x KT chunks
+  double *C;
+  int64_t ldc, M, N, MT, NT, KT;
+  Scalars<double> sc;
+};
+
+__device__ __forceinline__ void tile_coords(int64_t pid, int64_t MT, int64_t NT, int64_t &mt, int64_t &nt) {
+  const int64_t per_group = int64_t(kGroupM) * NT;
+  const int64_t g = pid / per_group;
+  const int64_t first_m = g * kGroupM;
+  const int64_t gsz = (MT - first_m) < kGroupM ? (MT - first_m) : kGroupM;
+  const int64_t in = pid - g * per_group;
+  mt = first_m + in % gsz;
+  nt = in / gsz;
+}
+
+__global__ void __launch_bounds__(kDmmaThreads, 1) qgemm_dmma_kernel(const DmmaArgs args) {
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  double *sA = reinterpret_cast<double *>(smem_raw);
+  double *sB = sA + kStages * kChunkElems;
+  uint64_t *full = reinterpret_cast<uint64_t *>(sB + kStages * kChunkElems);
+  uint64_t *empty = full + kStages;
+
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  int64_t mt, nt;
+  tile_coords(blockIdx.x, args.MT, args.NT, mt, nt);
+  const int64_t KT = args.KT;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kStages; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], kConsumerWarps);
+    }
+    fence_mbar_init();
+  }
+  __syncthreads();
+
+  if (warp == kConsumerWarps) {
+    // ---------------- producer: stream A/B chunks of this tile ----------------
+    if (lane == 0) {
+      const double *a_src = args.Ap + mt * KT * kChunkElems;
+      const double *b_src = args.Bp + nt * KT * kChunkElems;
+      constexpr uint32_t kBytes = kChunkElems * sizeof(double);
+      for (int64_t kt = 0; kt < KT; ++kt) {
+        const int slot = int(kt % kStages);
+        if (kt >= kStages) mbar_wait(&empty[slot], uint32_t((kt / kStages) - 1) & 1u);
+        mbar_arrive_expect_tx(&full[slot], 2 * kBytes);
+        bulk_g2s(sA + slot * kChunkElems, a_src + kt * kChunkElems, kBytes, &full[slot]);
+        bulk_g2s(sB + slot * kChunkElems, b_src + kt * kChunkElems, kBytes, &full[slot]);
+      }
+    }
+    return;
+  }
+
+  // ---------------- consumers ----------------
+  const int wm = warp & 1;   // 32-row half of the CTA tile
+  const int wn = warp >> 1;  // 16-column quarter
+  double acc[4][2][4][2];
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 2; ++j)
+#pragma unroll
+      for (int c = 0; c < 4; ++c) acc[i][j][c][0] = acc[i][j][c][1] = 0.0;
+
+  int slot = 0;
+  uint32_t phase = 0;
+  for (int64_t kt = 0; kt < KT; ++kt) {
+    mbar_wait(&full[slot], phase);
+    const double2 *a2 = reinterpret_cast<const double2 *>(sA + slot * kChunkElems);
+    const double2 *b2 = reinterpret_cast<const double2 *>(sB + slot * kChunkElems);
+#pragma unroll
+    for (int ks = 0; ks < kBK / 4; ++ks) {
+      double af[4][4], bf[2][4], bn[2][4];
+#pragma unroll
+      for (int ii = 0; ii < 4; ++ii)
+#pragma unroll
+        for (int pp = 0; pp < 2; ++pp) {
+          double2 v = a2[((ks * 8 + wm * 4 + ii) * 2 + pp) * 32 + lane];
+          af[ii][2 * pp] = v.x;
+          af[ii][2 * pp + 1] = v.y;
+        }
+#pragma unroll
+      for (int jj = 0; jj < 2; ++jj)
+#pragma unroll
+        for (int pp = 0; pp < 2; ++pp) {
+          double2 v = b2[((ks * 8 + wn * 2 + jj) * 2 + pp) * 32 + lane];
+          bf[jj][2 * pp] = v.x;
+          bf[jj][2 * pp + 1] = v.y;
+        }
+#pragma unroll
+      for (int jj = 0; jj < 2; ++jj)
+#pragma unroll
+        for (int s = 0; s < 4; ++s) bn[jj][s] = -bf[jj][s];
+      // 16 DMMA per (m8, n8) tile; p outermost so consecutive DMMAs hit
+      // different accumulators.
+#pragma unroll
+      for (int p = 0; p < 4; ++p)
+#pragma unroll
+        for (int ii = 0; ii < 4; ++ii)
+#pragma unroll
+          for (int jj = 0; jj < 2; ++jj)
+#pragma unroll
+            for (int c = 0; c < 4; ++c) {
+              const int s = p ^ c;
+              dmma_8x8x4(acc[ii][jj][c], af[ii][p], hneg(p, s) ? bn[jj][s] : bf[jj][s]);
+            }
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[slot]);
+    if (++slot == kStages) { slot = 0; phase ^= 1u; }
+  }
+
+  // ---------------- epilogue ----------------
+  // D fragment of m8n8k4: lane holds D[lane/4][2*(lane%4) + e], e = 0, 1.
+#pragma unroll
+  for (int ii = 0; ii < 4; ++ii) {
+    const int64_t row = mt * kBR + (wm * 4 + ii) * 8 + (lane >> 2);
+    if (row >= args.M) continue;
+#pragma unroll
+    for (int jj = 0; jj < 2; ++jj)
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int64_t col = nt * kBR + (wn * 2 + jj) * 8 + 2 * (lane & 3) + e;
+        if (col >= args.N) continue;
+        const double q[4] = {acc[ii][jj][0][e], acc[ii][jj][1][e], acc[ii][jj][2][e], acc[ii][jj][3][e]};
+        epilogue_one(args.sc, q, args.C + 4 * (row + col * args.ldc));
+      }
+  }
+}
+
+}  // namespace qg

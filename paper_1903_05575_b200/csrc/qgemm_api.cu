@@ -1,0 +1,340 @@
+// qgemm_api.cu -- C ABI and host planner of libqgemm.so (include/qgemm.h).
+//
+// SURVEY.md §8(a) row a1 "Plan / validate": BLAS-style argument checks, quick
+// returns, workspace carving and the K-panel loop (row a6, Alg. 2's kappa loop,
+// PAPER.md P:906-911), then per panel: pack A (a2), pack B (a3), mainloop with
+// fused epilogue (a4 + a5) -- all enqueued on the caller's stream.
+#include <algorithm>
+#include <cstdint>
+#include <cstring>
+#include <vector>
+#include <cuda_runtime.h>
+
+#include "../../include/qgemm.h"
+#include "qg_dmma.cuh"
+#include "qg_pack.cuh"
+#include "qg_simple.cuh"
+#include "qg_simt_f32.cuh"
+
+namespace {
+
+thread_local int g_last_launches = 0;
+
+// ---- optional per-launch event timing (qgemm_timing_enable / _collect)
+struct TimingRec {
+  int kind;
+  cudaEvent_t e0, e1;
+};
+struct Timing {
+  bool on = false;
+  std::vector<TimingRec> recs;
+  std::vector<cudaEvent_t> pool;
+  cudaEvent_t get() {
+    if (!pool.empty()) {
+      cudaEvent_t e = pool.back();
+      pool.pop_back();
+      return e;
+    }
+    cudaEvent_t e = nullptr;
+    cudaEventCreate(&e);
+    return e;
+  }
+};
+thread_local Timing g_timing;
+
+enum Kind { kPack = 0, kMain = 1, kScale = 2, kNaive = 3 };
+
+// Bracket one launch: call before (returns the record index or -1) and after.
+int tstart(int kind, cudaStream_t st) {
+  if (!g_timing.on) return -1;
+  TimingRec r{kind, g_timing.get(), g_timing.get()};
+  cudaEventRecord(r.e0, st);
+  g_timing.recs.push_back(r);
+  return int(g_timing.recs.size()) - 1;
+}
+void tstop(int idx, cudaStream_t st) {
+  if (idx >= 0) cudaEventRecord(g_timing.recs[size_t(idx)].e1, st);
+}
+
+int op_code(char t) {
+  switch (t) {
+    case 'N': case 'n': return 0;
+    case 'T': case 't': return 1;
+    case 'H': case 'h': case 'C': case 'c': return 2;
+    default: return -1;
+  }
+}
+
+template <typename T>
+bool is_zero_q(const T *q) { return q[0] == T(0) && q[1] == T(0) && q[2] == T(0) && q[3] == T(0); }
+
+template <typename T>
+qg::Scalars<T> make_scalars(const T *alpha, const T *beta) {
+  qg::Scalars<T> s;
+  for (int c = 0; c < 4; ++c) { s.alpha[c] = alpha[c]; s.beta[c] = beta[c]; }
+  s.alpha_real = alpha[1] == T(0) && alpha[2] == T(0) && alpha[3] == T(0);
+  s.beta_real = beta[1] == T(0) && beta[2] == T(0) && beta[3] == T(0);
+  s.beta_zero = is_zero_q(beta);
+  return s;
+}
+
+int64_t cdiv(int64_t a, int64_t b) { return (a + b - 1) / b; }
+size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
+
+// Byte extent [lo, hi) touched by a stored rows x cols matrix with leading dim ld.
+template <typename T>
+void extent(const T *p, int64_t rows, int64_t cols, int64_t ld, uintptr_t &lo, uintptr_t &hi) {
+  lo = reinterpret_cast<uintptr_t>(p);
+  hi = lo + uintptr_t(4 * sizeof(T)) * uintptr_t((cols - 1) * ld + rows);
+}
+bool overlaps(uintptr_t a0, uintptr_t a1, uintptr_t b0, uintptr_t b1) { return a0 < b1 && b0 < a1; }
+
+struct Shape {
+  int oa, ob;
+  int64_t M, N, K;
+};
+
+// Bytes of one K-tile column of packed panels (all MT + NT row tiles).
+template <typename T>
+size_t bytes_per_ktile(int64_t M, int64_t N) {
+  return size_t(cdiv(M, qg::kBR) + cdiv(N, qg::kBR)) * qg::kChunkElems * sizeof(T);
+}
+
+template <typename T>
+size_t workspace_for(int64_t M, int64_t N, int64_t ktiles) {
+  const size_t a = size_t(cdiv(M, qg::kBR)) * size_t(ktiles) * qg::kChunkElems * sizeof(T);
+  const size_t b = size_t(cdiv(N, qg::kBR)) * size_t(ktiles) * qg::kChunkElems * sizeof(T);
+  return align256(a) + align256(b);
+}
+
+// Argument validation common to all entry points.  Returns 0 or -i.
+template <typename T>
+int validate(char transA, char transB, int64_t M, int64_t N, int64_t K, const T *alpha, const T *A,
+             int64_t lda, const T *B, int64_t ldb, const T *beta, const T *C, int64_t ldc, Shape &sh,
+             bool &reads_ab) {
+  sh.oa = op_code(transA);
+  sh.ob = op_code(transB);
+  if (sh.oa < 0) return -1;
+  if (sh.ob < 0) return -2;
+  if (M < 0) return -3;
+  if (N < 0) return -4;
+  if (K < 0) return -5;
+  if (alpha == nullptr) return -6;
+  const int64_t a_rows = sh.oa == 0 ? M : K, a_cols = sh.oa == 0 ? K : M;
+  const int64_t b_rows = sh.ob == 0 ? K : N, b_cols = sh.ob == 0 ? N : K;
+  if (lda < std::max<int64_t>(1, a_rows)) return -8;
+  if (ldb < std::max<int64_t>(1, b_rows)) return -10;
+  if (beta == nullptr) return -11;
+  if (ldc < std::max<int64_t>(1, M)) return -13;
+  sh.M = M; sh.N = N; sh.K = K;
+  reads_ab = false;
+  if (M == 0 || N == 0) return 0;
+  if (C == nullptr || (reinterpret_cast<uintptr_t>(C) & 15u)) return -12;
+  reads_ab = K > 0 && !is_zero_q(alpha);
+  if (reads_ab) {
+    if (A == nullptr || (reinterpret_cast<uintptr_t>(A) & 15u)) return -7;
+    if (B == nullptr || (reinterpret_cast<uintptr_t>(B) & 15u)) return -9;
+    uintptr_t c0, c1, a0, a1, b0, b1;
+    extent(C, M, N, ldc, c0, c1);
+    extent(A, a_rows, a_cols, lda, a0, a1);
+    extent(B, b_rows, b_cols, ldb, b0, b1);
+    if (overlaps(c0, c1, a0, a1) || overlaps(c0, c1, b0, b1)) return -12;
+  }
+  return 0;
+}
+
+template <typename T>
+int launch_scale(T *C, int64_t ldc, int64_t M, int64_t N, const qg::Scalars<T> &sc, cudaStream_t st) {
+  const int64_t total = M * N;
+  const int threads = 256;
+  const int64_t blocks = std::min<int64_t>(cdiv(total, threads), 148 * 16);
+  { int ti = tstart(kScale, st);
+  qg::qgemm_scale_kernel<T><<<unsigned(blocks), threads, 0, st>>>(C, ldc, M, N, sc);
+  tstop(ti, st); }
+  ++g_last_launches;
+  return int(cudaGetLastError());
+}
+
+template <typename T>
+int launch_pack(const T *X, int64_t ldx, int row_contig, int conj, int64_t R, int64_t k_begin, int64_t k_end,
+                int64_t KT, T *out, cudaStream_t st) {
+  const int64_t blocks = cdiv(R, qg::kBR) * KT;
+  int ti = tstart(kPack, st);
+  if constexpr (sizeof(T) == 8)
+    qg::pack_kernel<T, qg::FragLayout><<<unsigned(blocks), 256, 0, st>>>(X, ldx, row_contig, conj, R, k_begin,
+                                                                        k_end, KT, out);
+  else
+    qg::pack_kernel<T, qg::PlanarLayout><<<unsigned(blocks), 256, 0, st>>>(X, ldx, row_contig, conj, R,
+                                                                          k_begin, k_end, KT, out);
+  tstop(ti, st);
+  ++g_last_launches;
+  return int(cudaGetLastError());
+}
+
+int launch_mainloop(const double *Ap, const double *Bp, double *C, int64_t ldc, int64_t M, int64_t N,
+                    int64_t KT, const qg::Scalars<double> &sc, cudaStream_t st) {
+  static bool attr_set = false;
+  if (!attr_set) {
+    cudaError_t e = cudaFuncSetAttribute(qg::qgemm_dmma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         int(qg::kDmmaSmemBytes));
+    if (e != cudaSuccess) return int(e);
+    attr_set = true;
+  }
+  qg::DmmaArgs a;
+  a.Ap = Ap; a.Bp = Bp; a.C = C; a.ldc = ldc; a.M = M; a.N = N;
+  a.MT = cdiv(M, qg::kBR); a.NT = cdiv(N, qg::kBR); a.KT = KT; a.sc = sc;
+  { int ti = tstart(kMain, st);
+  qg::qgemm_dmma_kernel<<<unsigned(a.MT * a.NT), qg::kDmmaThreads, qg::kDmmaSmemBytes, st>>>(a);
+  tstop(ti, st); }
+  ++g_last_launches;
+  return int(cudaGetLastError());
+}
+
+int launch_mainloop(const float *Ap, const float *Bp, float *C, int64_t ldc, int64_t M, int64_t N, int64_t KT,
+                    const qg::Scalars<float> &sc, cudaStream_t st) {
+  static bool attr_set = false;
+  if (!attr_set) {
+    cudaError_t e = cudaFuncSetAttribute(qg::qgemm_simt_f32_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         int(qg::kF32SmemBytes));
+    if (e != cudaSuccess) return int(e);
+    attr_set = true;
+  }
+  qg::F32Args a;
+  a.Ap = Ap; a.Bp = Bp; a.C = C; a.ldc = ldc; a.M = M; a.N = N;
+  a.MT = cdiv(M, qg::kBR); a.NT = cdiv(N, qg::kBR); a.KT = KT; a.sc = sc;
+  { int ti = tstart(kMain, st);
+  qg::qgemm_simt_f32_kernel<<<unsigned(a.MT * a.NT), qg::kF32Threads, qg::kF32SmemBytes, st>>>(a);
+  tstop(ti, st); }
+  ++g_last_launches;
+  return int(cudaGetLastError());
+}
+
+template <typename T>
+int qgemm_impl(char transA, char transB, int64_t M, int64_t N, int64_t K, const T *alpha, const T *A,
+               int64_t lda, const T *B, int64_t ldb, const T *beta, T *C, int64_t ldc, void *workspace,
+               size_t workspace_bytes, void *stream) {
+  g_last_launches = 0;
+  Shape sh;
+  bool reads_ab = false;
+  int rc = validate<T>(transA, transB, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, sh, reads_ab);
+  if (rc != 0) return rc;
+  if (M == 0 || N == 0) return 0;
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  qg::Scalars<T> sc = make_scalars(alpha, beta);
+  if (!reads_ab) return launch_scale(C, ldc, M, N, sc, st);
+
+  // ---- plan: how many K-tiles fit in the workspace at once (K-panel loop, a6)
+  const int64_t KT_total = cdiv(K, qg::kBK);
+  const size_t min_ws = workspace_for<T>(M, N, 1);
+  if (workspace == nullptr || (reinterpret_cast<uintptr_t>(workspace) & 255u)) return -14;
+  if (workspace_bytes < min_ws) return -15;
+  int64_t KTp = KT_total;
+  while (KTp > 1 && workspace_for<T>(M, N, KTp) > workspace_bytes) {
+    // largest panel that fits; start from a proportional estimate
+    int64_t est = int64_t(workspace_bytes / bytes_per_ktile<T>(M, N));
+    KTp = std::max<int64_t>(1, std::min<int64_t>(KTp - 1, est));
+  }
+  const int64_t MT = cdiv(M, qg::kBR);
+  T *Ap = reinterpret_cast<T *>(workspace);
+  T *Bp = reinterpret_cast<T *>(reinterpret_cast<char *>(workspace) +
+                                align256(size_t(MT) * size_t(KTp) * qg::kChunkElems * sizeof(T)));
+  const int a_row_contig = sh.oa == 0 ? 1 : 0;
+  const int b_row_contig = sh.ob == 0 ? 0 : 1;
+  qg::Scalars<T> sc_acc = sc;  // later panels accumulate: beta = 1
+  for (int c = 0; c < 4; ++c) sc_acc.beta[c] = T(c == 0 ? 1 : 0);
+  sc_acc.beta_real = 1;
+  sc_acc.beta_zero = 0;
+  for (int64_t kt0 = 0; kt0 < KT_total; kt0 += KTp) {
+    const int64_t k_begin = kt0 * qg::kBK;
+    const int64_t k_end = std::min<int64_t>(K, (kt0 + KTp) * qg::kBK);
+    const int64_t ktn = cdiv(k_end - k_begin, qg::kBK);
+    rc = launch_pack<T>(A, lda, a_row_contig, sh.oa == 2, M, k_begin, k_end, ktn, Ap, st);
+    if (rc) return rc;
+    rc = launch_pack<T>(B, ldb, b_row_contig, sh.ob == 2, N, k_begin, k_end, ktn, Bp, st);
+    if (rc) return rc;
+    rc = launch_mainloop(Ap, Bp, C, ldc, M, N, ktn, kt0 == 0 ? sc : sc_acc, st);
+    if (rc) return rc;
+  }
+  return 0;
+}
+
+template <typename T>
+size_t ws_bytes(char transA, char transB, int64_t M, int64_t N, int64_t K, bool minimum) {
+  if (op_code(transA) < 0 || op_code(transB) < 0 || M <= 0 || N <= 0 || K <= 0) return 0;
+  return workspace_for<T>(M, N, minimum ? 1 : cdiv(K, qg::kBK));
+}
+
+}  // namespace
+
+extern "C" {
+
+int qgemm(char transA, char transB, int64_t M, int64_t N, int64_t K, const double alpha[4], const double *A,
+          int64_t lda, const double *B, int64_t ldb, const double beta[4], double *C, int64_t ldc,
+          void *workspace, size_t workspace_bytes, void *stream) {
+  return qgemm_impl<double>(transA, transB, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, workspace,
+                            workspace_bytes, stream);
+}
+
+int qgemm_f32(char transA, char transB, int64_t M, int64_t N, int64_t K, const float alpha[4], const float *A,
+              int64_t lda, const float *B, int64_t ldb, const float beta[4], float *C, int64_t ldc,
+              void *workspace, size_t workspace_bytes, void *stream) {
+  return qgemm_impl<float>(transA, transB, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, workspace,
+                           workspace_bytes, stream);
+}
+
+size_t qgemm_workspace_bytes(char transA, char transB, int64_t M, int64_t N, int64_t K, int dtype) {
+  if (dtype == 0) return ws_bytes<double>(transA, transB, M, N, K, false);
+  if (dtype == 1) return ws_bytes<float>(transA, transB, M, N, K, false);
+  return 0;
+}
+
+size_t qgemm_workspace_min_bytes(char transA, char transB, int64_t M, int64_t N, int64_t K, int dtype) {
+  if (dtype == 0) return ws_bytes<double>(transA, transB, M, N, K, true);
+  if (dtype == 1) return ws_bytes<float>(transA, transB, M, N, K, true);
+  return 0;
+}
+
+int qgemm_naive(char transA, char transB, int64_t M, int64_t N, int64_t K, const double alpha[4],
+                const double *A, int64_t lda, const double *B, int64_t ldb, const double beta[4], double *C,
+                int64_t ldc, void *stream) {
+  g_last_launches = 0;
+  Shape sh;
+  bool reads_ab = false;
+  int rc = validate<double>(transA, transB, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, sh, reads_ab);
+  if (rc != 0) return rc;
+  if (M == 0 || N == 0) return 0;
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  qg::Scalars<double> sc = make_scalars(alpha, beta);
+  if (!reads_ab) return launch_scale(C, ldc, M, N, sc, st);
+  dim3 grid(unsigned(cdiv(M, 128)), unsigned(std::min<int64_t>(N, 65535)));
+  { int ti = tstart(kNaive, st);
+  qg::qgemm_naive_kernel<double><<<grid, 128, 0, st>>>(sh.oa, sh.ob, M, N, K, A, lda, B, ldb, C, ldc, sc);
+  tstop(ti, st); }
+  ++g_last_launches;
+  return int(cudaGetLastError());
+}
+
+int qgemm_last_launch_count(void) { return g_last_launches; }
+
+void qgemm_timing_enable(int on) { g_timing.on = on != 0; }
+
+int qgemm_timing_collect(double ms[4], int counts[4]) {
+  for (int k = 0; k < 4; ++k) { ms[k] = 0.0; counts[k] = 0; }
+  int rc = 0;
+  for (const TimingRec &r : g_timing.recs) {
+    cudaError_t e = cudaEventSynchronize(r.e1);
+    float t = 0.f;
+    if (e == cudaSuccess) e = cudaEventElapsedTime(&t, r.e0, r.e1);
+    if (e != cudaSuccess && rc == 0) rc = int(e);
+    ms[r.kind] += double(t);
+    counts[r.kind] += 1;
+    g_timing.pool.push_back(r.e0);
+    g_timing.pool.push_back(r.e1);
+  }
+  g_timing.recs.clear();
+  return rc;
+}
+
+const char *qgemm_version(void) { return "qgemm-b200 0.1 (sm_100a; FP64 DMMA.8x8x4, FP32 FFMA)"; }
+
+}  // extern "C"

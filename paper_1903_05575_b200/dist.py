@@ -1,0 +1,90 @@
+"""Row-block multi-GPU driver (north star item (4)).
+
+C <- alpha op(A) op(B) + beta C with C sharded by row blocks over the ranks of
+a process group (one process per GPU, NCCL over NVLink 5 / NVSwitch):
+
+  * rank r owns rows [r0, r1) of C and op(A): C_r = alpha op(A)_r op(B) + beta C_r,
+    an independent QGEMM of shape (r1 - r0) x N x K -- the sharded unit;
+  * op(B) is needed by every rank: ONE exchange step, `broadcast` of B's storage
+    from `root` (skipped with broadcast_b=False when B is already resident);
+  * ONE collection step: every rank sends its compact C_r (ld = r1 - r0) to
+    `root`, which copies it into the row block of the column-major full C
+    (ldc = M): the relayout of a strided row block.
+
+Row split: rows_for_rank() -- contiguous blocks, sizes differ by at most one
+64-row tile so every rank's mainloop tiles are full except the global tail.
+The local GEMM is libqgemm.so's qgemm (no CPU path); tests on CPU/gloo inject
+the oracle through `local_gemm` to exercise this host logic only.
+"""
+from __future__ import annotations
+
+from typing import Callable
+
+import torch
+import torch.distributed as dist
+
+TILE = 64
+
+
+def rows_for_rank(M: int, world: int, rank: int, tile: int = TILE) -> tuple[int, int]:
+    """[r0, r1) of the row block of `rank`: whole tiles split as evenly as possible."""
+    tiles = (M + tile - 1) // tile
+    base, extra = divmod(tiles, world)
+    t0 = rank * base + min(rank, extra)
+    t1 = t0 + base + (1 if rank < extra else 0)
+    return min(M, t0 * tile), min(M, t1 * tile)
+
+
+def qgemm_rowsharded(transA: str, transB: str, alpha, A_local: torch.Tensor, B: torch.Tensor,
+                     beta, C_local: torch.Tensor, M: int, N: int, K: int,
+                     group=None, root: int = 0, broadcast_b: bool = True,
+                     gather: bool = True, C_full: torch.Tensor | None = None,
+                     local_gemm: Callable | None = None):
+    """Sharded QGEMM step: broadcast B (from root) -> local QGEMM -> gather C.
+
+    A_local: stored operand whose op() is rows [r0, r1) of op(A):
+             opA = 'N': (K, M_loc, 4) with ld = M_loc; opA = 'T'/'H': (M_loc, K, 4).
+    B:       full stored B on every rank (contents only meaningful on root when
+             broadcast_b=True); shape (ncols, ldb, 4).
+    C_local: (N, M_loc, 4), this rank's rows of C (compact, ld = M_loc).
+    C_full:  on root when gather=True: (N, ldc >= M, 4) receiving all row blocks.
+    Returns C_full on root (gather=True), else C_local.
+    """
+    world = dist.get_world_size(group)
+    rank = dist.get_rank(group)
+    r0, r1 = rows_for_rank(M, world, rank)
+    m_loc = r1 - r0
+    assert C_local.shape[0] == N and C_local.shape[1] >= max(1, m_loc)
+    if broadcast_b:
+        dist.broadcast(B, src=root, group=group)
+    if local_gemm is None:
+        from .qgemm import qgemm as local_gemm_fn  # libqgemm.so, no fallback
+        local_gemm = local_gemm_fn
+    if m_loc > 0:
+        local_gemm(transA, transB, alpha, A_local, B, beta, C_local, M=m_loc, N=N, K=K)
+    if not gather:
+        return C_local
+    if rank == root:
+        assert C_full is not None and C_full.shape[0] == N and C_full.shape[1] >= M
+        C_full[:, r0:r1, :].copy_(C_local[:, :m_loc, :])
+        bufs = []
+        ops = []
+        for src in range(world):
+            if src == root:
+                continue
+            s0, s1 = rows_for_rank(M, world, src)
+            if s1 == s0:
+                continue
+            buf = torch.empty((N, s1 - s0, 4), dtype=C_local.dtype, device=C_local.device)
+            bufs.append((s0, s1, buf))
+            ops.append(dist.P2POp(dist.irecv, buf, src, group))
+        for w in dist.batch_isend_irecv(ops) if ops else []:
+            w.wait()
+        for s0, s1, buf in bufs:  # relayout: compact C_r -> strided row block of C
+            C_full[:, s0:s1, :].copy_(buf)
+        return C_full
+    if m_loc > 0:
+        send = C_local if C_local.shape[1] == m_loc else C_local[:, :m_loc, :].contiguous()
+        for w in dist.batch_isend_irecv([dist.P2POp(dist.isend, send, root, group)]):
+            w.wait()
+    return C_local

@@ -1,0 +1,161 @@
+"""Python binding of the C ABI (same names as include/qgemm.h).
+
+Tensors use the storage convention of the library: a CUDA tensor of shape
+(ncols, ld, 4), C-contiguous, is a column-major quaternion matrix with leading
+dimension ``ld`` (in quaternions) and interleaved components (PAPER.md
+P:727-734).  This module only marshals pointers, sizes, the
+current CUDA stream and a workspace; every step of the computation runs in the
+kernels of libqgemm.so.
+"""
+from __future__ import annotations
+
+import ctypes
+
+import torch
+
+from ._lib import QgemmError, load
+
+_workspaces: dict[int, torch.Tensor] = {}
+
+
+def _q4(x, dtype) -> ctypes.Array:
+    """Quaternion scalar (real number or 4-sequence) -> host double[4]/float[4]."""
+    vals = [0.0, 0.0, 0.0, 0.0]
+    if isinstance(x, (int, float)):
+        vals[0] = float(x)
+    else:
+        seq = [float(v) for v in (x.tolist() if hasattr(x, "tolist") else x)]
+        vals[: len(seq)] = seq
+    ct = ctypes.c_double if dtype == torch.float64 else ctypes.c_float
+    return (ct * 4)(*vals)
+
+
+def _ptr(t: torch.Tensor | None):
+    return None if t is None else ctypes.c_void_p(t.data_ptr())
+
+
+def _check(t: torch.Tensor, name: str, dtype):
+    if t.dtype != dtype:
+        raise TypeError(f"{name}: expected {dtype}, got {t.dtype}")
+    if not t.is_cuda:
+        raise TypeError(f"{name}: must be a CUDA tensor (no CPU path exists)")
+    if t.dim() != 3 or t.shape[2] != 4 or not t.is_contiguous():
+        raise ValueError(f"{name}: expected a contiguous (ncols, ld, 4) tensor")
+
+
+def infer_dims(transA: str, transB: str, A: torch.Tensor, B: torch.Tensor, C: torch.Tensor):
+    """(M, N, K) assuming no ld padding of C and A (explicit sizes override)."""
+    M, N = C.shape[1], C.shape[0]
+    K = A.shape[0] if transA.upper() == "N" else A.shape[1]
+    return M, N, K
+
+
+def workspace_bytes(transA: str, transB: str, M: int, N: int, K: int, dtype=torch.float64) -> int:
+    return int(load().qgemm_workspace_bytes(transA.encode(), transB.encode(), M, N, K,
+                                            0 if dtype == torch.float64 else 1))
+
+
+def workspace_min_bytes(transA: str, transB: str, M: int, N: int, K: int, dtype=torch.float64) -> int:
+    return int(load().qgemm_workspace_min_bytes(transA.encode(), transB.encode(), M, N, K,
+                                                0 if dtype == torch.float64 else 1))
+
+
+def get_workspace(nbytes: int, device) -> torch.Tensor:
+    dev = torch.device(device).index or 0
+    ws = _workspaces.get(dev)
+    if ws is None or ws.numel() < nbytes:
+        _workspaces.pop(dev, None)
+        ws = torch.empty(max(nbytes, 256), dtype=torch.uint8, device=device)
+        _workspaces[dev] = ws
+    return ws
+
+
+def _call(fn, name, transA, transB, M, N, K, alpha, A, B, beta, C, dtype, workspace, ws_bytes,
+          stream):
+    al, be = _q4(alpha, dtype), _q4(beta, dtype)
+    lda = A.shape[1] if A is not None else 1
+    ldb = B.shape[1] if B is not None else 1
+    ldc = C.shape[1]
+    args = [transA.encode(), transB.encode(), M, N, K, ctypes.cast(al, ctypes.c_void_p), _ptr(A),
+            lda, _ptr(B), ldb, ctypes.cast(be, ctypes.c_void_p), _ptr(C), ldc]
+    if workspace is not Ellipsis:
+        args += [_ptr(workspace), ws_bytes]
+    args += [ctypes.c_void_p(stream)]
+    rc = fn(*args)
+    if rc != 0:
+        raise QgemmError(name, rc)
+    return C
+
+
+def qgemm(transA: str, transB: str, alpha, A: torch.Tensor, B: torch.Tensor, beta,
+          C: torch.Tensor, M: int | None = None, N: int | None = None, K: int | None = None,
+          workspace: torch.Tensor | None = None, stream: torch.cuda.Stream | None = None):
+    """C <- alpha op(A) op(B) + beta C in FP64 (in place on C, asynchronous)."""
+    return _qgemm_typed(load().qgemm, "qgemm", torch.float64, transA, transB, alpha, A, B, beta, C,
+                        M, N, K, workspace, stream)
+
+
+def qgemm_f32(transA: str, transB: str, alpha, A: torch.Tensor, B: torch.Tensor, beta,
+              C: torch.Tensor, M: int | None = None, N: int | None = None, K: int | None = None,
+              workspace: torch.Tensor | None = None, stream: torch.cuda.Stream | None = None):
+    """FP32 variant (float storage, FP32 FMA arithmetic)."""
+    return _qgemm_typed(load().qgemm_f32, "qgemm_f32", torch.float32, transA, transB, alpha, A, B,
+                        beta, C, M, N, K, workspace, stream)
+
+
+def _qgemm_typed(fn, name, dtype, transA, transB, alpha, A, B, beta, C, M, N, K, workspace, stream):
+    _check(C, "C", dtype)
+    for t, nm in ((A, "A"), (B, "B")):
+        if t is not None:
+            _check(t, nm, dtype)
+    m0, n0, k0 = infer_dims(transA, transB, A, B, C)
+    M = m0 if M is None else M
+    N = n0 if N is None else N
+    K = k0 if K is None else K
+    st = (stream or torch.cuda.current_stream(C.device)).cuda_stream
+    need = workspace_bytes(transA, transB, M, N, K, dtype)
+    if workspace is None:
+        workspace = get_workspace(need, C.device) if need else None
+    nbytes = workspace.numel() * workspace.element_size() if workspace is not None else 0
+    return _call(fn, name, transA, transB, M, N, K, alpha, A, B, beta, C, dtype, workspace, nbytes,
+                 st)
+
+
+def qgemm_naive(transA: str, transB: str, alpha, A: torch.Tensor, B: torch.Tensor, beta,
+                C: torch.Tensor, M: int | None = None, N: int | None = None, K: int | None = None,
+                stream: torch.cuda.Stream | None = None):
+    """Debug path: one thread per output quaternion (not used by qgemm)."""
+    _check(C, "C", torch.float64)
+    m0, n0, k0 = infer_dims(transA, transB, A, B, C)
+    M = m0 if M is None else M
+    N = n0 if N is None else N
+    K = k0 if K is None else K
+    st = (stream or torch.cuda.current_stream(C.device)).cuda_stream
+    return _call(load().qgemm_naive, "qgemm_naive", transA, transB, M, N, K, alpha, A, B, beta, C,
+                 torch.float64, Ellipsis, 0, st)
+
+
+def last_launch_count() -> int:
+    return int(load().qgemm_last_launch_count())
+
+
+KINDS = ("pack", "mainloop", "scale", "naive")
+
+
+def timing_enable(on: bool = True) -> None:
+    """Bracket every library kernel launch of this thread with CUDA events."""
+    load().qgemm_timing_enable(1 if on else 0)
+
+
+def timing_collect() -> dict:
+    """Synchronise on the recorded events; {kind: (total_ms, launches)}; clears."""
+    ms = (ctypes.c_double * 4)()
+    cnt = (ctypes.c_int * 4)()
+    rc = load().qgemm_timing_collect(ms, cnt)
+    if rc != 0:
+        raise QgemmError("qgemm_timing_collect", rc)
+    return {k: (ms[i], cnt[i]) for i, k in enumerate(KINDS)}
+
+
+def version() -> str:
+    return load().qgemm_version().decode()

@@ -1,0 +1,188 @@
+"""CUDA path (through the C ABI) vs the CPU oracle, element by element (-m gpu).
+
+Tolerances are the north star's (tests/tolerance.py): FP64
+1e-12 K max|A| max|B|, FP32 1e-4 sqrt(K) max|A| max|B| (+ reading R8).
+Exact-integer inputs require bitwise equality.
+"""
+from __future__ import annotations
+
+import numpy as np
+import pytest
+import torch
+
+import oracle
+import paper_1903_05575_b200 as qg
+from synth import CONFIGS, make_problem
+from tests.gpu_helpers import assert_parity, oracle_full, run_gpu, to_dev
+
+pytestmark = pytest.mark.gpu
+OPS = [(a, b) for a in "NTH" for b in "NTH"]
+QALPHA = (0.3, -1.2, 0.7, 0.25)
+QBETA = (-0.5, 0.1, -0.9, 0.4)
+
+
+def _lds(opA, opB, M, N, K, pad):
+    lda = (M if opA == "N" else K) + pad
+    ldb = (K if opB == "N" else N) + pad
+    return lda, ldb, M + pad
+
+
+# ---------------------------------------------------------------- config 1
+def test_c1_full():
+    cfg = CONFIGS["c1"]
+    pr = make_problem(cfg["M"], cfg["N"], cfg["K"], "N", "N", cfg["alpha"], cfg["beta"], seed=0,
+                      c_init="nan")
+    assert_parity(pr, run_gpu(pr), oracle_full(pr))
+
+
+# ---------------------------------------------------------------- config 2
+@pytest.mark.parametrize("opA,opB", OPS)
+def test_c2_all_ops_padded_ld(opA, opB):
+    cfg = CONFIGS["c2"]
+    n = cfg["M"]
+    pr = make_problem(n, n, n, opA, opB, cfg["alpha"], cfg["beta"], seed=0, lda=cfg["ld"],
+                      ldb=cfg["ld"], ldc=cfg["ld"])
+    assert np.isnan(pr.A[:, n:, :]).all() and np.isnan(pr.B[:, n:, :]).all()
+    assert_parity(pr, run_gpu(pr), oracle_full(pr))
+
+
+# ---------------------------------------------------------------- ragged sweep
+SIZES = [1, 2, 3, 5, 7, 8, 17, 33, 63, 64, 65, 127, 129]
+
+
+@pytest.mark.parametrize("opA,opB", OPS)
+@pytest.mark.parametrize("seed", [0, 1, 2])
+def test_ragged_shapes_quaternion_scalars(opA, opB, seed):
+    rng = np.random.default_rng(100 + seed)
+    for _ in range(4):
+        M, N, K = (int(rng.choice(SIZES)) for _ in range(3))
+        lda, ldb, ldc = _lds(opA, opB, M, N, K, int(rng.integers(0, 3)))
+        pr = make_problem(M, N, K, opA, opB, QALPHA, QBETA, seed=seed, lda=lda, ldb=ldb, ldc=ldc)
+        assert_parity(pr, run_gpu(pr), oracle_full(pr))
+
+
+@pytest.mark.parametrize("M,N,K", [(200, 130, 300), (64, 64, 16), (65, 191, 33), (1, 300, 257)])
+@pytest.mark.parametrize("opA,opB", OPS)
+def test_exact_integer_bitwise_f64(M, N, K, opA, opB):
+    """P8: integer components in [-8, 8] -> exact in any order -> bitwise."""
+    pr = make_problem(M, N, K, opA, opB, (2, -1, 0, 3), (1, 0, -2, 1), seed=3, dist="int8")
+    assert_parity(pr, run_gpu(pr), oracle_full(pr), exact=True)
+
+
+@pytest.mark.parametrize("opA,opB", OPS)
+def test_exact_integer_bitwise_f32(opA, opB):
+    """P8 in FP32: |partial sums| <= 2^24, so FP32 is exact too."""
+    pr = make_problem(150, 70, 200, opA, opB, (1, 0, 0, 0), (-1, 0, 0, 0), seed=4, dist="int8")
+    assert_parity(pr, run_gpu(pr, "f32"), oracle_full(pr), exact=True)
+
+
+@pytest.mark.parametrize("opA,opB", OPS)
+def test_f32_tolerance(opA, opB):
+    """FP32 variant checked against the FP64 oracle on the FP64 inputs (R11)."""
+    pr = make_problem(257, 190, 513, opA, opB, QALPHA, QBETA, seed=5, dist="normal",
+                      lda=(257 if opA == "N" else 513) + 1)
+    assert_parity(pr, run_gpu(pr, "f32"), oracle_full(pr), precision="f32")
+
+
+# ---------------------------------------------------------------- K-panel loop (a6)
+@pytest.mark.parametrize("precision", ["f64", "f32"])
+def test_k_panel_loop_small_workspace(precision):
+    """Workspace for 3 K-tiles only: the call loops over K-panels, beta on the
+    first, accumulate afterwards (Alg. 2 kappa loop)."""
+    M, N, K = 130, 100, 16 * 7 + 5
+    pr = make_problem(M, N, K, "H", "T", QALPHA, QBETA, seed=6)
+    dt = torch.float64 if precision == "f64" else torch.float32
+    full = qg.workspace_bytes("H", "T", M, N, K, dt)
+    small = qg.workspace_min_bytes("H", "T", M, N, K, dt) * 3
+    assert small < full
+    ws = torch.empty(small, dtype=torch.uint8, device="cuda")
+    got = run_gpu(pr, precision, workspace=ws)
+    assert qg.last_launch_count() == 3 * 3  # 3 panels x (pack A, pack B, mainloop)
+    assert_parity(pr, got, oracle_full(pr), precision=precision)
+
+
+# ---------------------------------------------------------------- degenerate cases
+def test_quick_returns_and_beta_paths():
+    # M = 0 / N = 0: nothing enqueued, C untouched
+    pr = make_problem(5, 4, 3, seed=1)
+    C = to_dev(pr.C)
+    C0 = C.clone()
+    A, B = to_dev(pr.A), to_dev(pr.B)
+    qg.qgemm("N", "N", 1, A, B, 1, C, M=0, N=4, K=3)
+    assert qg.last_launch_count() == 0
+    qg.qgemm("N", "N", 1, A, B, 1, C, M=5, N=0, K=3)
+    assert torch.equal(C, C0)
+    # alpha = 0, beta = 1 -> bitwise unchanged
+    qg.qgemm("N", "N", 0, A, B, 1, C, M=5, N=4, K=3)
+    torch.cuda.synchronize()
+    assert torch.equal(C, C0)
+    # K = 0 -> beta C (quaternion beta, left)
+    pr = make_problem(6, 5, 0, "N", "N", 1, QBETA, seed=2)
+    assert_parity(pr, run_gpu(pr), oracle_full(pr))
+    # beta = 0 with NaN C -> finite
+    pr = make_problem(70, 33, 20, "T", "H", QALPHA, 0, seed=2, c_init="nan")
+    got = run_gpu(pr)
+    assert np.isfinite(got[:, :70]).all()
+    assert_parity(pr, got, oracle_full(pr))
+
+
+def test_alias_rejected_and_nothing_enqueued():
+    pr = make_problem(8, 8, 8, seed=0)
+    A = to_dev(pr.A)
+    with pytest.raises(qg.QgemmError) as ei:
+        qg.qgemm("N", "N", 1, A, A, 0, A)
+    assert ei.value.code == -12
+
+
+def test_naive_cross_check_and_stream():
+    """Debug kernel and tuned kernel agree on a side stream."""
+    pr = make_problem(190, 77, 140, "H", "N", QALPHA, QBETA, seed=9)
+    s = torch.cuda.Stream()
+    with torch.cuda.stream(s):
+        got = run_gpu(pr, stream=s)
+        nai = run_gpu(pr, naive=True, stream=s)
+    ref = oracle_full(pr)
+    assert_parity(pr, got, ref)
+    assert_parity(pr, nai, ref)
+
+
+def test_b_is_a_hermitian_rank_k_shape():
+    """c4's structure at reduced M: C <- A A^H + C with B == A (same buffer) and a
+    Hermitian C; the result is Hermitian (P12) and matches the oracle."""
+    n, K = 320, 256
+    pr = make_problem(n, n, K, "N", "H", 1, 1, seed=0, c_init="hermitian", b_is_a=True)
+    got = run_gpu(pr)
+    assert_parity(pr, got, oracle_full(pr))
+    L = got[:, :n, :].transpose(1, 0, 2)
+    LH = L.transpose(1, 0, 2).copy(); LH[..., 1:] *= -1
+    assert np.abs(L - LH).max() <= 1e-12 * K
+
+
+# ---------------------------------------------------------------- config 3 at full size
+@pytest.mark.parametrize("precision", ["f64", "f32"])
+def test_c3_full_size_sampled_and_freivalds(precision):
+    """c3 (8192^3, N/H, alpha = beta = 1, N(0,1)) in the bench's launch
+    configuration: 2 full rows + 2 full columns + 256 random entries from the
+    oracle one by one, plus a Freivalds check of the whole C."""
+    cfg = CONFIGS["c3"]
+    n = cfg["M"]
+    pr = make_problem(n, n, n, "N", "H", cfg["alpha"], cfg["beta"], seed=0, dist="normal")
+    got = run_gpu(pr, precision)
+    rng = np.random.default_rng(42)
+    rows = np.concatenate([np.full(n, 17), np.full(n, n - 1), np.arange(n), np.arange(n),
+                           rng.integers(0, n, 256)])
+    cols = np.concatenate([np.arange(n), np.arange(n), np.full(n, 5), np.full(n, n - 2),
+                           rng.integers(0, n, 256)])
+    ref = oracle.qgemm_entries("N", "H", n, n, n, pr.alpha, pr.A, pr.B, pr.beta, pr.C, rows, cols)
+    from tests.gpu_helpers import tol_for
+    tol = tol_for(pr, precision)
+    err = np.abs(got[cols, rows, :] - ref).max()
+    assert err <= tol, (err, tol)
+    # Freivalds: C x == alpha op(A) (op(B) x) + beta C0 x, x multiplied on the right
+    x = np.random.default_rng(7).standard_normal((n, 4))
+    lhs = oracle.qgemv("N", n, n, np.ascontiguousarray(got), x)
+    y = oracle.qgemv("H", n, n, pr.B, x)
+    rhs = oracle.qgemv("N", n, n, pr.A, y) + oracle.qgemv("N", n, n, pr.C, x)
+    # each entry of C x sums n products of an entry error (<= tol) and |x|
+    bound = tol * np.abs(x).sum() * 4
+    assert np.abs(lhs - rhs).max() <= bound
