@@ -144,8 +144,10 @@ def cpu_baseline(A, B, C, n, seconds):
     import oracle
     ncols = 4
     dt, fl = oracle_sample(A, B, C, n, ncols)
-    if dt < seconds / 2:
-        ncols = int(min(n, max(ncols, ncols * seconds / max(dt, 1e-3))))
+    for _ in range(3):  # grow the sample until it is ~`seconds` of CPU work
+        if dt >= 0.8 * seconds or ncols >= n:
+            break
+        ncols = int(min(n, max(ncols + 1, ncols * seconds / max(dt, 1e-3))))
         dt, fl = oracle_sample(A, B, C, n, ncols)
     return {"value": fl / dt / 1e12, "unit": "TFLOP/s", "cores": oracle.max_threads(),
             "kind": "oracle",

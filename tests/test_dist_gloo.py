@@ -1,0 +1,87 @@
+"""Host logic of the row-block multi-GPU driver (dist.py) on CPU with gloo,
+world_size 2 (-m "not gpu").  The local GEMM is injected (the oracle on CPU
+tensors) -- this exercises sharding, the broadcast of B, the gather and the
+strided relayout of C only; the GPU product path is tested in -m gpu."""
+from __future__ import annotations
+
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+import oracle
+from paper_1903_05575_b200.dist import qgemm_rowsharded, rows_for_rank
+from synth import make_problem
+
+
+def test_rows_for_rank_partition():
+    for M in (1, 63, 64, 65, 1000, 8192 * 3 + 5):
+        for world in (1, 2, 3, 4, 8):
+            blocks = [rows_for_rank(M, world, r) for r in range(world)]
+            assert blocks[0][0] == 0 and blocks[-1][1] == M
+            for (a0, a1), (b0, b1) in zip(blocks, blocks[1:]):
+                assert a1 == b0 and a0 <= a1
+            sizes = [b - a for a, b in blocks]
+            # whole 64-row tiles except the global tail; balanced within one tile
+            assert all(a % 64 == 0 or a == M for a, _ in blocks)
+            assert max(sizes) - min(sizes) <= 64 + 63
+
+
+def _oracle_local(transA, transB, alpha, A, B, beta, C, M, N, K):
+    a, b, c = A.numpy(), B.numpy(), C.numpy()
+    oracle.qgemm(transA, transB, M, N, K, alpha, np.ascontiguousarray(a), np.ascontiguousarray(b),
+                 beta, c)  # C is contiguous -> updated in place through the numpy view
+
+
+def _worker(rank, world, port, opA, opB, M, N, K, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        pr = make_problem(M, N, K, opA, opB, (0.5, 0.25, -1, 0.1), (1, -0.5, 0, 0.2), seed=3)
+        r0, r1 = rows_for_rank(M, world, rank)
+        # this rank's stored operand: op(A_local) = rows [r0, r1) of op(A)
+        if opA == "N":
+            A_loc = np.ascontiguousarray(pr.A[:, r0:r1, :])          # (K, m_loc, 4)
+        else:
+            A_loc = np.ascontiguousarray(pr.A[r0:r1, :, :])          # (m_loc, K, 4)
+        C_loc = pr.C[:, r0:r1, :].copy()  # never a view of pr.C (used for the reference)
+        B = torch.from_numpy(pr.B.copy()) if rank == 0 else torch.full(pr.B.shape, np.nan,
+                                                                        dtype=torch.float64)
+        C_full = torch.full((N, M, 4), np.nan, dtype=torch.float64) if rank == 0 else None
+        out = qgemm_rowsharded(opA, opB, pr.alpha, torch.from_numpy(A_loc), B, pr.beta,
+                               torch.from_numpy(C_loc), M, N, K, C_full=C_full,
+                               local_gemm=_oracle_local)
+        if rank == 0:
+            ref = pr.C.copy()
+            oracle.qgemm(opA, opB, M, N, K, pr.alpha, pr.A, pr.B, pr.beta, ref)
+            # same per-entry summation order -> bitwise equal to the unsharded oracle
+            q.put(bool(np.array_equal(out.numpy(), ref)))
+    finally:
+        dist.destroy_process_group()
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+@pytest.mark.parametrize("opA,opB,M", [("N", "H", 150), ("H", "N", 130), ("T", "T", 64)])
+def test_rowsharded_gloo_world2(opA, opB, M):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    N, K = 37, 29
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, opA, opB, M, N, K, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    for p in procs:
+        p.join(timeout=120)
+    assert all(p.exitcode == 0 for p in procs), [p.exitcode for p in procs]
+    assert q.get(timeout=5) is True
