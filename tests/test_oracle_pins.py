@@ -346,3 +346,20 @@ def test_embedding_roundtrip():
     np.testing.assert_array_equal(unchi(chi(L)), L)
     X = logical_to_storage(L, ld=7)
     np.testing.assert_array_equal(storage_to_logical(X, 5), L)
+
+
+def test_counter_generator_torch_cpu_matches_numpy():
+    """synth/gpu_gen.py (torch int64 ops) reproduces synth.inputs.counter_uniform bitwise."""
+    import torch
+    from synth.gpu_gen import counter_hermitian, counter_matrix, counter_uniform_t, host_rows_N
+    from synth.inputs import counter_uniform
+    idx = np.random.default_rng(0).integers(0, 1 << 40, 5000)
+    np.testing.assert_array_equal(counter_uniform_t(3, 1, torch.from_numpy(idx)).numpy(),
+                                  counter_uniform(3, 1, idx))
+    M = counter_matrix(3, 1, 50, 40, "cpu").numpy()
+    np.testing.assert_array_equal(M[:, [0, 7, 49], :], host_rows_N(3, 1, 50, [0, 7, 49], 40))
+    H = counter_hermitian(5, 2, 30, "cpu", chunk_cols=7).numpy()
+    L = H.transpose(1, 0, 2)
+    LH = L.transpose(1, 0, 2).copy()
+    LH[..., 1:] *= -1
+    np.testing.assert_array_equal(L, LH)
