@@ -22,6 +22,16 @@
 // SASS UBLKCP) completing on mbarriers.  Epilogue: alpha (x) acc + beta (x) C,
 // left products, masked at the M/N edges, C re-interleaved in
 // registers (each lane owns whole quaternions).
+//
+// Schedule: persistent (one CTA per SM), "data-parallel + stream-K" hybrid.
+// Whole tiles are dealt round-robin while at least two full waves remain; the
+// remaining tiles' k-iterations are split evenly over all CTAs (stream-K), so
+// no SM idles in a partial last wave (c2: 256 tiles on 148 SMs).  A tile split
+// across CTAs is finished by the CTA holding its k = 0 segment (the "owner"):
+// the others park their partial accumulators in the workspace and bump the
+// tile's arrival counter; the owner adds them and runs the epilogue.  The
+// producer warp walks the same work list, so the ring keeps streaming across
+// tile boundaries while the consumers run an epilogue.
 #pragma once
 #include "qg_pack.cuh"
 
@@ -29,9 +39,13 @@ namespace qg {
 
 constexpr int kStages = 3;
 constexpr int kConsumerWarps = 8;
+constexpr int kConsumerThreads = kConsumerWarps * 32;
 constexpr int kDmmaThreads = (kConsumerWarps + 1) * 32;
 constexpr int kGroupM = 8;  // rasterisation: 8 M-tiles share each B panel in flight
 constexpr size_t kDmmaSmemBytes = size_t(kStages) * 2 * kChunkElems * sizeof(double) + 2 * kStages * 8;
+constexpr int kAccPerThread = 64;                      // doubles
+constexpr size_t kPartialBytes = size_t(kConsumerThreads) * kAccPerThread * sizeof(double);  // 128 KiB
+constexpr int kMaxPersistentCTAs = 256;
 
 struct DmmaArgs {
   const double *Ap;  // packed A panel: MT x KT chunks
@@ -39,6 +53,13 @@ struct DmmaArgs {
   double *C;
   int64_t ldc, M, N, MT, NT, KT;
   Scalars<double> sc;
+  // persistent stream-K schedule
+  int64_t T;          // tiles
+  int64_t dp_tiles;   // tiles dealt whole, round-robin
+  int64_t sk_iters;   // (T - dp_tiles) * KT k-iterations split over the grid
+  double *partials;   // gridDim.x slots of kPartialBytes
+  int *flags;         // T - dp_tiles arrival counters (zero on entry; owners reset them)
+  int64_t grid;       // host side: CTAs launched
 };
 
 __device__ __forceinline__ void tile_coords(int64_t pid, int64_t MT, int64_t NT, int64_t &mt, int64_t &nt) {
@@ -51,6 +72,66 @@ __device__ __forceinline__ void tile_coords(int64_t pid, int64_t MT, int64_t NT,
   nt = in / gsz;
 }
 
+// Stream-K range of CTA c: [begin, end) in the SK iteration space.
+struct SkSplit {
+  int64_t per, extra;
+  __device__ __forceinline__ int64_t begin(int64_t c) const { return c * per + (c < extra ? c : extra); }
+  __device__ __forceinline__ int64_t end(int64_t c) const { return begin(c) + per + (c < extra ? 1 : 0); }
+  __device__ __forceinline__ int64_t owner_of(int64_t i) const {  // CTA whose range holds iteration i
+    const int64_t big = extra * (per + 1);
+    if (i < big) return i / (per + 1);
+    return extra + (i - big) / per;
+  }
+};
+
+// One unit of work: k-tiles [kb, ke) of tile t.
+struct Unit {
+  int64_t t, kb, ke;
+};
+
+// Enumerate this CTA's units in order; returns false when exhausted.
+struct WorkIter {
+  int64_t next_dp, sk_i, sk_end;
+  __device__ __forceinline__ bool next(const DmmaArgs &a, Unit &u) {
+    if (next_dp < a.dp_tiles) {
+      u.t = next_dp;
+      u.kb = 0;
+      u.ke = a.KT;
+      next_dp += gridDim.x;
+      return true;
+    }
+    if (sk_i < sk_end) {
+      const int64_t lt = sk_i / a.KT;
+      u.t = a.dp_tiles + lt;
+      u.kb = sk_i - lt * a.KT;
+      const int64_t tile_end = (lt + 1) * a.KT;
+      const int64_t stop = sk_end < tile_end ? sk_end : tile_end;
+      u.ke = u.kb + (stop - sk_i);
+      sk_i = stop;
+      return true;
+    }
+    return false;
+  }
+};
+
+__device__ __forceinline__ WorkIter make_iter(const DmmaArgs &a, const SkSplit &sp) {
+  WorkIter w;
+  w.next_dp = blockIdx.x;
+  w.sk_i = a.sk_iters ? sp.begin(blockIdx.x) : 0;
+  w.sk_end = a.sk_iters ? sp.end(blockIdx.x) : 0;
+  return w;
+}
+
+__device__ __forceinline__ void consumer_bar() {
+  asm volatile("bar.sync 1, %0;\n" ::"n"(kConsumerThreads) : "memory");
+}
+
+__device__ __forceinline__ int ld_acquire(const int *p) {
+  int v;
+  asm volatile("ld.global.acquire.gpu.b32 %0, [%1];\n" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
 __global__ void __launch_bounds__(kDmmaThreads, 1) qgemm_dmma_kernel(const DmmaArgs args) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   double *sA = reinterpret_cast<double *>(smem_raw);
@@ -60,9 +141,10 @@ __global__ void __launch_bounds__(kDmmaThreads, 1) qgemm_dmma_kernel(const DmmaA
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
-  int64_t mt, nt;
-  tile_coords(blockIdx.x, args.MT, args.NT, mt, nt);
   const int64_t KT = args.KT;
+  SkSplit sp;
+  sp.per = args.sk_iters / gridDim.x;
+  sp.extra = args.sk_iters - sp.per * gridDim.x;
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < kStages; ++s) {
@@ -74,17 +156,26 @@ __global__ void __launch_bounds__(kDmmaThreads, 1) qgemm_dmma_kernel(const DmmaA
   __syncthreads();
 
   if (warp == kConsumerWarps) {
-    // ---------------- producer: stream A/B chunks of this tile ----------------
+    // ---------------- producer: stream the A/B chunks of every unit ----------------
     if (lane == 0) {
-      const double *a_src = args.Ap + mt * KT * kChunkElems;
-      const double *b_src = args.Bp + nt * KT * kChunkElems;
       constexpr uint32_t kBytes = kChunkElems * sizeof(double);
-      for (int64_t kt = 0; kt < KT; ++kt) {
-        const int slot = int(kt % kStages);
-        if (kt >= kStages) mbar_wait(&empty[slot], uint32_t((kt / kStages) - 1) & 1u);
-        mbar_arrive_expect_tx(&full[slot], 2 * kBytes);
-        bulk_g2s(sA + slot * kChunkElems, a_src + kt * kChunkElems, kBytes, &full[slot]);
-        bulk_g2s(sB + slot * kChunkElems, b_src + kt * kChunkElems, kBytes, &full[slot]);
+      WorkIter it = make_iter(args, sp);
+      Unit u;
+      int slot = 0;
+      uint32_t phase = 0;
+      int64_t fills = 0;
+      while (it.next(args, u)) {
+        int64_t mt, nt;
+        tile_coords(u.t, args.MT, args.NT, mt, nt);
+        const double *a_src = args.Ap + mt * KT * kChunkElems;
+        const double *b_src = args.Bp + nt * KT * kChunkElems;
+        for (int64_t kt = u.kb; kt < u.ke; ++kt, ++fills) {
+          if (fills >= kStages) mbar_wait(&empty[slot], phase ^ 1u);
+          mbar_arrive_expect_tx(&full[slot], 2 * kBytes);
+          bulk_g2s(sA + slot * kChunkElems, a_src + kt * kChunkElems, kBytes, &full[slot]);
+          bulk_g2s(sB + slot * kChunkElems, b_src + kt * kChunkElems, kBytes, &full[slot]);
+          if (++slot == kStages) { slot = 0; phase ^= 1u; }
+        }
       }
     }
     return;
@@ -93,77 +184,135 @@ __global__ void __launch_bounds__(kDmmaThreads, 1) qgemm_dmma_kernel(const DmmaA
   // ---------------- consumers ----------------
   const int wm = warp & 1;   // 32-row half of the CTA tile
   const int wn = warp >> 1;  // 16-column quarter
-  double acc[4][2][4][2];
-#pragma unroll
-  for (int i = 0; i < 4; ++i)
-#pragma unroll
-    for (int j = 0; j < 2; ++j)
-#pragma unroll
-      for (int c = 0; c < 4; ++c) acc[i][j][c][0] = acc[i][j][c][1] = 0.0;
-
+  const int tid = threadIdx.x;
   int slot = 0;
   uint32_t phase = 0;
-  for (int64_t kt = 0; kt < KT; ++kt) {
-    mbar_wait(&full[slot], phase);
-    const double2 *a2 = reinterpret_cast<const double2 *>(sA + slot * kChunkElems);
-    const double2 *b2 = reinterpret_cast<const double2 *>(sB + slot * kChunkElems);
+  WorkIter it = make_iter(args, sp);
+  Unit u;
+  while (it.next(args, u)) {
+    double acc[4][2][4][2];
 #pragma unroll
-    for (int ks = 0; ks < kBK / 4; ++ks) {
-      double af[4][4], bf[2][4], bn[2][4];
+    for (int i = 0; i < 4; ++i)
 #pragma unroll
-      for (int ii = 0; ii < 4; ++ii)
+      for (int j = 0; j < 2; ++j)
 #pragma unroll
-        for (int pp = 0; pp < 2; ++pp) {
-          double2 v = a2[((ks * 8 + wm * 4 + ii) * 2 + pp) * 32 + lane];
-          af[ii][2 * pp] = v.x;
-          af[ii][2 * pp + 1] = v.y;
-        }
+        for (int c = 0; c < 4; ++c) acc[i][j][c][0] = acc[i][j][c][1] = 0.0;
+
+    for (int64_t kt = u.kb; kt < u.ke; ++kt) {
+      mbar_wait(&full[slot], phase);
+      const double2 *a2 = reinterpret_cast<const double2 *>(sA + slot * kChunkElems);
+      const double2 *b2 = reinterpret_cast<const double2 *>(sB + slot * kChunkElems);
 #pragma unroll
-      for (int jj = 0; jj < 2; ++jj)
-#pragma unroll
-        for (int pp = 0; pp < 2; ++pp) {
-          double2 v = b2[((ks * 8 + wn * 2 + jj) * 2 + pp) * 32 + lane];
-          bf[jj][2 * pp] = v.x;
-          bf[jj][2 * pp + 1] = v.y;
-        }
-#pragma unroll
-      for (int jj = 0; jj < 2; ++jj)
-#pragma unroll
-        for (int s = 0; s < 4; ++s) bn[jj][s] = -bf[jj][s];
-      // 16 DMMA per (m8, n8) tile; p outermost so consecutive DMMAs hit
-      // different accumulators.
-#pragma unroll
-      for (int p = 0; p < 4; ++p)
+      for (int ks = 0; ks < kBK / 4; ++ks) {
+        double af[4][4], bf[2][4], bn[2][4];
 #pragma unroll
         for (int ii = 0; ii < 4; ++ii)
 #pragma unroll
-          for (int jj = 0; jj < 2; ++jj)
+          for (int pp = 0; pp < 2; ++pp) {
+            double2 v = a2[((ks * 8 + wm * 4 + ii) * 2 + pp) * 32 + lane];
+            af[ii][2 * pp] = v.x;
+            af[ii][2 * pp + 1] = v.y;
+          }
+#pragma unroll
+        for (int jj = 0; jj < 2; ++jj)
+#pragma unroll
+          for (int pp = 0; pp < 2; ++pp) {
+            double2 v = b2[((ks * 8 + wn * 2 + jj) * 2 + pp) * 32 + lane];
+            bf[jj][2 * pp] = v.x;
+            bf[jj][2 * pp + 1] = v.y;
+          }
+#pragma unroll
+        for (int jj = 0; jj < 2; ++jj)
+#pragma unroll
+          for (int s = 0; s < 4; ++s) bn[jj][s] = -bf[jj][s];
+        // 16 DMMA per (m8, n8) tile; p outermost so consecutive DMMAs hit
+        // different accumulators.
+#pragma unroll
+        for (int p = 0; p < 4; ++p)
+#pragma unroll
+          for (int ii = 0; ii < 4; ++ii)
+#pragma unroll
+            for (int jj = 0; jj < 2; ++jj)
+#pragma unroll
+              for (int c = 0; c < 4; ++c) {
+                const int s = p ^ c;
+                dmma_8x8x4(acc[ii][jj][c], af[ii][p], hneg(p, s) ? bn[jj][s] : bf[jj][s]);
+              }
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[slot]);
+      if (++slot == kStages) { slot = 0; phase ^= 1u; }
+    }
+
+    const bool whole = (u.kb == 0 && u.ke == KT);
+    if (!whole) {
+      // stream-K fixup (only tiles >= dp_tiles are ever split)
+      const int64_t lt = u.t - args.dp_tiles;
+      double2 *mine = reinterpret_cast<double2 *>(args.partials + size_t(blockIdx.x) * (kPartialBytes / 8));
+      if (u.kb != 0) {
+        // contributor: park the partial sums, then signal the owner
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+#pragma unroll
+          for (int j = 0; j < 2; ++j)
+#pragma unroll
+            for (int c = 0; c < 4; ++c)
+              __stcg(&mine[((i * 2 + j) * 4 + c) * kConsumerThreads + tid],
+                     make_double2(acc[i][j][c][0], acc[i][j][c][1]));
+        __threadfence();
+        consumer_bar();
+        if (tid == 0) atomicAdd(&args.flags[lt], 1);
+        continue;
+      }
+      // owner: wait for every other CTA holding a piece of this tile, add their partials
+      const int64_t first = lt * KT;
+      const int64_t c_last = sp.owner_of(first + KT - 1);
+      const int expected = int(c_last - blockIdx.x);
+      if (tid == 0) {
+        // contributors are co-resident (grid <= resident CTAs) and never wait
+        // on anything, so this terminates; the trap turns a broken schedule
+        // into a launch error instead of a hung GPU.
+        uint32_t spins = 0;
+        while (ld_acquire(&args.flags[lt]) < expected) {
+          __nanosleep(100);
+          if (++spins == (1u << 27)) __trap();
+        }
+        args.flags[lt] = 0;  // ready for the next call
+      }
+      consumer_bar();
+      for (int64_t src = blockIdx.x + 1; src <= c_last; ++src) {
+        const double2 *p = reinterpret_cast<const double2 *>(args.partials + size_t(src) * (kPartialBytes / 8));
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+#pragma unroll
+          for (int j = 0; j < 2; ++j)
 #pragma unroll
             for (int c = 0; c < 4; ++c) {
-              const int s = p ^ c;
-              dmma_8x8x4(acc[ii][jj][c], af[ii][p], hneg(p, s) ? bn[jj][s] : bf[jj][s]);
+              const double2 v = __ldcg(&p[((i * 2 + j) * 4 + c) * kConsumerThreads + tid]);
+              acc[i][j][c][0] += v.x;
+              acc[i][j][c][1] += v.y;
             }
-    }
-    __syncwarp();
-    if (lane == 0) mbar_arrive(&empty[slot]);
-    if (++slot == kStages) { slot = 0; phase ^= 1u; }
-  }
-
-  // ---------------- epilogue ----------------
-  // D fragment of m8n8k4: lane holds D[lane/4][2*(lane%4) + e], e = 0, 1.
-#pragma unroll
-  for (int ii = 0; ii < 4; ++ii) {
-    const int64_t row = mt * kBR + (wm * 4 + ii) * 8 + (lane >> 2);
-    if (row >= args.M) continue;
-#pragma unroll
-    for (int jj = 0; jj < 2; ++jj)
-#pragma unroll
-      for (int e = 0; e < 2; ++e) {
-        const int64_t col = nt * kBR + (wn * 2 + jj) * 8 + 2 * (lane & 3) + e;
-        if (col >= args.N) continue;
-        const double q[4] = {acc[ii][jj][0][e], acc[ii][jj][1][e], acc[ii][jj][2][e], acc[ii][jj][3][e]};
-        epilogue_one(args.sc, q, args.C + 4 * (row + col * args.ldc));
       }
+    }
+
+    // ---------------- epilogue ----------------
+    // D fragment of m8n8k4: lane holds D[lane/4][2*(lane%4) + e], e = 0, 1.
+    int64_t mt, nt;
+    tile_coords(u.t, args.MT, args.NT, mt, nt);
+#pragma unroll
+    for (int ii = 0; ii < 4; ++ii) {
+      const int64_t row = mt * kBR + (wm * 4 + ii) * 8 + (lane >> 2);
+      if (row >= args.M) continue;
+#pragma unroll
+      for (int jj = 0; jj < 2; ++jj)
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const int64_t col = nt * kBR + (wn * 2 + jj) * 8 + 2 * (lane & 3) + e;
+          if (col >= args.N) continue;
+          const double q[4] = {acc[ii][jj][0][e], acc[ii][jj][1][e], acc[ii][jj][2][e], acc[ii][jj][3][e]};
+          epilogue_one(args.sc, q, args.C + 4 * (row + col * args.ldc));
+        }
+    }
   }
 }
 

@@ -100,11 +100,32 @@ size_t bytes_per_ktile(int64_t M, int64_t N) {
   return size_t(cdiv(M, qg::kBR) + cdiv(N, qg::kBR)) * qg::kChunkElems * sizeof(T);
 }
 
+// Upper bound of the persistent grid for a panel of `ktiles` k-tiles: the
+// schedule (plan_schedule) never launches more CTAs than this.
+int64_t max_grid(int64_t tiles, int64_t ktiles) {
+  return std::max<int64_t>(1, std::min<int64_t>(qg::kMaxPersistentCTAs, std::max<int64_t>(tiles, tiles * ktiles / 2)));
+}
+
+// Stream-K scratch of the persistent FP64 mainloop: one partial-accumulator slot
+// per CTA + the arrival counters (at most 2 per CTA).
 template <typename T>
-size_t workspace_for(int64_t M, int64_t N, int64_t ktiles) {
+size_t sk_slots_bytes(int64_t M, int64_t N, int64_t ktiles) {
+  const int64_t tiles = cdiv(M, qg::kBR) * cdiv(N, qg::kBR);
+  return align256(size_t(max_grid(tiles, ktiles)) * qg::kPartialBytes);
+}
+template <typename T>
+size_t sk_reserve(int64_t M, int64_t N, int64_t ktiles) {
+  if (sizeof(T) != 8) return 0;
+  return sk_slots_bytes<T>(M, N, ktiles) + align256(size_t(2 * qg::kMaxPersistentCTAs) * sizeof(int));
+}
+
+template <typename T>
+size_t workspace_for(int64_t M, int64_t N, int64_t K, int64_t ktiles) {
+  // the stream-K reserve is sized for the whole K (an upper bound for any panel),
+  // so the workspace grows linearly with the panel depth `ktiles`
   const size_t a = size_t(cdiv(M, qg::kBR)) * size_t(ktiles) * qg::kChunkElems * sizeof(T);
   const size_t b = size_t(cdiv(N, qg::kBR)) * size_t(ktiles) * qg::kChunkElems * sizeof(T);
-  return align256(a) + align256(b);
+  return align256(a) + align256(b) + sk_reserve<T>(M, N, cdiv(K, qg::kBK));
 }
 
 // Argument validation common to all entry points.  Returns 0 or -i.
@@ -171,8 +192,36 @@ int launch_pack(const T *X, int64_t ldx, int row_contig, int conj, int64_t R, in
   return int(cudaGetLastError());
 }
 
+// Resident CTAs of the persistent FP64 mainloop on the current device.
+int persistent_ctas() {
+  int dev = 0, sms = 0, per_sm = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return 0;
+  if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess) return 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, qg::qgemm_dmma_kernel, qg::kDmmaThreads,
+                                                    qg::kDmmaSmemBytes) != cudaSuccess)
+    return 0;
+  return std::min(qg::kMaxPersistentCTAs, sms * std::max(1, per_sm));
+}
+
+// Persistent "data-parallel + stream-K" schedule (see qg_dmma.cuh).
+void plan_schedule(qg::DmmaArgs &a, int resident) {
+  a.T = a.MT * a.NT;
+  // fewer tiles than SMs: split k too, but keep >= 2 k-tiles per CTA
+  const int64_t G = std::max<int64_t>(1, std::min<int64_t>(resident, std::max<int64_t>(a.T, (a.T * a.KT) / 2)));
+  const int64_t waves = a.T / G, rem = a.T % G;
+  if (rem == 0) {
+    a.dp_tiles = a.T;
+  } else if (waves >= 2) {
+    a.dp_tiles = (waves - 1) * G;  // last full wave + remainder go stream-K
+  } else {
+    a.dp_tiles = 0;
+  }
+  a.sk_iters = (a.T - a.dp_tiles) * a.KT;
+  a.grid = G;
+}
+
 int launch_mainloop(const double *Ap, const double *Bp, double *C, int64_t ldc, int64_t M, int64_t N,
-                    int64_t KT, const qg::Scalars<double> &sc, cudaStream_t st) {
+                    int64_t KT, const qg::Scalars<double> &sc, void *sk_scratch, cudaStream_t st) {
   static bool attr_set = false;
   if (!attr_set) {
     cudaError_t e = cudaFuncSetAttribute(qg::qgemm_dmma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -180,18 +229,29 @@ int launch_mainloop(const double *Ap, const double *Bp, double *C, int64_t ldc, 
     if (e != cudaSuccess) return int(e);
     attr_set = true;
   }
+  const int resident = persistent_ctas();
+  if (resident <= 0) return int(cudaErrorInvalidConfiguration);
   qg::DmmaArgs a;
   a.Ap = Ap; a.Bp = Bp; a.C = C; a.ldc = ldc; a.M = M; a.N = N;
   a.MT = cdiv(M, qg::kBR); a.NT = cdiv(N, qg::kBR); a.KT = KT; a.sc = sc;
+  plan_schedule(a, resident);
+  // scratch layout: [2*kMaxPersistentCTAs arrival counters][grid partial slots]
+  a.flags = reinterpret_cast<int *>(sk_scratch);
+  a.partials = reinterpret_cast<double *>(reinterpret_cast<char *>(sk_scratch) +
+                                          align256(size_t(2 * qg::kMaxPersistentCTAs) * sizeof(int)));
+  if (a.sk_iters) {
+    cudaError_t e = cudaMemsetAsync(a.flags, 0, size_t(a.T - a.dp_tiles) * sizeof(int), st);
+    if (e != cudaSuccess) return int(e);
+  }
   { int ti = tstart(kMain, st);
-  qg::qgemm_dmma_kernel<<<unsigned(a.MT * a.NT), qg::kDmmaThreads, qg::kDmmaSmemBytes, st>>>(a);
+  qg::qgemm_dmma_kernel<<<unsigned(a.grid), qg::kDmmaThreads, qg::kDmmaSmemBytes, st>>>(a);
   tstop(ti, st); }
   ++g_last_launches;
   return int(cudaGetLastError());
 }
 
 int launch_mainloop(const float *Ap, const float *Bp, float *C, int64_t ldc, int64_t M, int64_t N, int64_t KT,
-                    const qg::Scalars<float> &sc, cudaStream_t st) {
+                    const qg::Scalars<float> &sc, void * /*sk_scratch*/, cudaStream_t st) {
   static bool attr_set = false;
   if (!attr_set) {
     cudaError_t e = cudaFuncSetAttribute(qg::qgemm_simt_f32_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -225,19 +285,21 @@ int qgemm_impl(char transA, char transB, int64_t M, int64_t N, int64_t K, const 
 
   // ---- plan: how many K-tiles fit in the workspace at once (K-panel loop, a6)
   const int64_t KT_total = cdiv(K, qg::kBK);
-  const size_t min_ws = workspace_for<T>(M, N, 1);
+  const size_t min_ws = workspace_for<T>(M, N, K, 1);
   if (workspace == nullptr || (reinterpret_cast<uintptr_t>(workspace) & 255u)) return -14;
   if (workspace_bytes < min_ws) return -15;
   int64_t KTp = KT_total;
-  while (KTp > 1 && workspace_for<T>(M, N, KTp) > workspace_bytes) {
+  while (KTp > 1 && workspace_for<T>(M, N, K, KTp) > workspace_bytes) {
     // largest panel that fits; start from a proportional estimate
-    int64_t est = int64_t(workspace_bytes / bytes_per_ktile<T>(M, N));
+    const size_t res = sk_reserve<T>(M, N, KT_total);
+    int64_t est = int64_t((workspace_bytes - res) / bytes_per_ktile<T>(M, N));
     KTp = std::max<int64_t>(1, std::min<int64_t>(KTp - 1, est));
   }
-  const int64_t MT = cdiv(M, qg::kBR);
+  const int64_t MT = cdiv(M, qg::kBR), NT = cdiv(N, qg::kBR);
   T *Ap = reinterpret_cast<T *>(workspace);
   T *Bp = reinterpret_cast<T *>(reinterpret_cast<char *>(workspace) +
                                 align256(size_t(MT) * size_t(KTp) * qg::kChunkElems * sizeof(T)));
+  void *sk_scratch = reinterpret_cast<char *>(Bp) + align256(size_t(NT) * size_t(KTp) * qg::kChunkElems * sizeof(T));
   const int a_row_contig = sh.oa == 0 ? 1 : 0;
   const int b_row_contig = sh.ob == 0 ? 0 : 1;
   qg::Scalars<T> sc_acc = sc;  // later panels accumulate: beta = 1
@@ -252,7 +314,7 @@ int qgemm_impl(char transA, char transB, int64_t M, int64_t N, int64_t K, const 
     if (rc) return rc;
     rc = launch_pack<T>(B, ldb, b_row_contig, sh.ob == 2, N, k_begin, k_end, ktn, Bp, st);
     if (rc) return rc;
-    rc = launch_mainloop(Ap, Bp, C, ldc, M, N, ktn, kt0 == 0 ? sc : sc_acc, st);
+    rc = launch_mainloop(Ap, Bp, C, ldc, M, N, ktn, kt0 == 0 ? sc : sc_acc, sk_scratch, st);
     if (rc) return rc;
   }
   return 0;
@@ -261,7 +323,7 @@ int qgemm_impl(char transA, char transB, int64_t M, int64_t N, int64_t K, const 
 template <typename T>
 size_t ws_bytes(char transA, char transB, int64_t M, int64_t N, int64_t K, bool minimum) {
   if (op_code(transA) < 0 || op_code(transB) < 0 || M <= 0 || N <= 0 || K <= 0) return 0;
-  return workspace_for<T>(M, N, minimum ? 1 : cdiv(K, qg::kBK));
+  return workspace_for<T>(M, N, K, minimum ? 1 : cdiv(K, qg::kBK));
 }
 
 }  // namespace

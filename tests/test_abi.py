@@ -102,9 +102,14 @@ def test_null_AB_allowed_when_not_read(lib):
 def test_workspace_sizes(lib):
     f64 = lib.qgemm_workspace_bytes(b"N", b"H", 8192, 8192, 8192, 0)
     f32 = lib.qgemm_workspace_bytes(b"N", b"H", 8192, 8192, 8192, 1)
-    assert f64 == 2 * 8192 * 8192 * 32  # packed A + B, no padding at tile multiples
-    assert f32 == f64 // 2
-    # one K-tile: 2 row tiles of A + 2 of B, 32 KiB per (64 x 16)-quaternion chunk
-    assert lib.qgemm_workspace_min_bytes(b"N", b"N", 100, 70, 1000, 0) == 4 * 32768
+    # packed A + B (no padding at tile multiples) + stream-K scratch of the FP64
+    # mainloop: 256 partial slots of 128 KiB + 512 arrival counters
+    sk = 256 * 131072 + 2048
+    assert f64 == 2 * 8192 * 8192 * 32 + sk
+    assert f32 == 2 * 8192 * 8192 * 16
+    # one K-tile: 2 row tiles of A + 2 of B, 32 KiB per (64 x 16)-quaternion chunk,
+    # + partial slots for the largest grid over the whole K (4 tiles x 63 k-tiles
+    # / 2 = 126 CTAs) + counters
+    assert lib.qgemm_workspace_min_bytes(b"N", b"N", 100, 70, 1000, 0) == 4 * 32768 + 126 * 131072 + 2048
     assert lib.qgemm_workspace_bytes(b"N", b"N", 0, 5, 5, 0) == 0
     assert lib.qgemm_workspace_bytes(b"X", b"N", 5, 5, 5, 0) == 0

@@ -93,7 +93,10 @@ def test_k_panel_loop_small_workspace(precision):
     pr = make_problem(M, N, K, "H", "T", QALPHA, QBETA, seed=6)
     dt = torch.float64 if precision == "f64" else torch.float32
     full = qg.workspace_bytes("H", "T", M, N, K, dt)
-    small = qg.workspace_min_bytes("H", "T", M, N, K, dt) * 3
+    mn = qg.workspace_min_bytes("H", "T", M, N, K, dt)
+    kt = (K + 15) // 16
+    per_ktile = (full - mn) // (kt - 1)
+    small = mn + 2 * per_ktile  # room for 3 K-tiles -> panels of 3, 3, 2
     assert small < full
     ws = torch.empty(small, dtype=torch.uint8, device="cuda")
     got = run_gpu(pr, precision, workspace=ws)
