@@ -40,7 +40,18 @@ namespace qg {
 constexpr int kStages = 3;
 constexpr int kConsumerWarps = 8;
 constexpr int kConsumerThreads = kConsumerWarps * 32;
-constexpr int kDmmaThreads = (kConsumerWarps + 1) * 32;
+#ifndef QG_PRODUCER_WG
+#define QG_PRODUCER_WG 1
+#endif
+#if QG_PRODUCER_WG
+// 8 consumer warps + a producer warpgroup; setmaxnreg moves registers from the
+// producer (40/thread) to the consumers (232/thread): 128*40 + 256*232 <= 64K.
+constexpr int kDmmaThreads = (kConsumerWarps + 4) * 32;
+constexpr int kProducerRegs = 40;
+constexpr int kConsumerRegs = 232;
+#else
+constexpr int kDmmaThreads = kConsumerWarps * 32;  // producer role lives in thread 0
+#endif
 constexpr int kGroupM = 8;  // rasterisation: 8 M-tiles share each B panel in flight
 constexpr size_t kDmmaSmemBytes = size_t(kStages) * 2 * kChunkElems * sizeof(double) + 2 * kStages * 8;
 constexpr int kAccPerThread = 64;                      // doubles
@@ -132,6 +143,40 @@ __device__ __forceinline__ int ld_acquire(const int *p) {
   return v;
 }
 
+// Producer cursor over the CTA's (unit, k-tile) sequence.
+struct Producer {
+  WorkIter it;
+  int64_t kt, ke;
+  const double *a_src, *b_src;
+  int slot;
+  uint32_t phase;
+  int64_t fills;
+};
+
+// Issue the next fill (bulk copies of one A and one B chunk); false when done.
+__device__ __forceinline__ bool produce_next(Producer &p, const DmmaArgs &args, double *sA, double *sB,
+                                             uint64_t *full, uint64_t *empty) {
+  constexpr uint32_t kBytes = kChunkElems * sizeof(double);
+  while (p.kt >= p.ke) {
+    Unit u;
+    if (!p.it.next(args, u)) return false;
+    int64_t mt, nt;
+    tile_coords(u.t, args.MT, args.NT, mt, nt);
+    p.a_src = args.Ap + mt * args.KT * kChunkElems;
+    p.b_src = args.Bp + nt * args.KT * kChunkElems;
+    p.kt = u.kb;
+    p.ke = u.ke;
+  }
+  if (p.fills >= kStages) mbar_wait(&empty[p.slot], p.phase ^ 1u);
+  mbar_arrive_expect_tx(&full[p.slot], 2 * kBytes);
+  bulk_g2s(sA + p.slot * kChunkElems, p.a_src + p.kt * kChunkElems, kBytes, &full[p.slot]);
+  bulk_g2s(sB + p.slot * kChunkElems, p.b_src + p.kt * kChunkElems, kBytes, &full[p.slot]);
+  if (++p.slot == kStages) { p.slot = 0; p.phase ^= 1u; }
+  ++p.kt;
+  ++p.fills;
+  return true;
+}
+
 __global__ void __launch_bounds__(kDmmaThreads, 1) qgemm_dmma_kernel(const DmmaArgs args) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   double *sA = reinterpret_cast<double *>(smem_raw);
@@ -155,31 +200,33 @@ __global__ void __launch_bounds__(kDmmaThreads, 1) qgemm_dmma_kernel(const DmmaA
   }
   __syncthreads();
 
-  if (warp == kConsumerWarps) {
-    // ---------------- producer: stream the A/B chunks of every unit ----------------
-    if (lane == 0) {
-      constexpr uint32_t kBytes = kChunkElems * sizeof(double);
-      WorkIter it = make_iter(args, sp);
-      Unit u;
-      int slot = 0;
-      uint32_t phase = 0;
-      int64_t fills = 0;
-      while (it.next(args, u)) {
-        int64_t mt, nt;
-        tile_coords(u.t, args.MT, args.NT, mt, nt);
-        const double *a_src = args.Ap + mt * KT * kChunkElems;
-        const double *b_src = args.Bp + nt * KT * kChunkElems;
-        for (int64_t kt = u.kb; kt < u.ke; ++kt, ++fills) {
-          if (fills >= kStages) mbar_wait(&empty[slot], phase ^ 1u);
-          mbar_arrive_expect_tx(&full[slot], 2 * kBytes);
-          bulk_g2s(sA + slot * kChunkElems, a_src + kt * kChunkElems, kBytes, &full[slot]);
-          bulk_g2s(sB + slot * kChunkElems, b_src + kt * kChunkElems, kBytes, &full[slot]);
-          if (++slot == kStages) { slot = 0; phase ^= 1u; }
-        }
+  // ---------------- producer role (thread 0), kStages - 1 fills ahead ----------------
+  // Thread 0 streams the A/B chunks of the CTA's work list; it refills the slot
+  // of consumption f-1 at the start of consumption f (a one-step lag, so it
+  // rarely waits for the other warps).  Keeping the producer inside a compute
+  // warp (8 warps, 2 per SM sub-partition) leaves 255 registers per thread; a
+  // ninth warp would cap every thread at 168 (3 warps on one sub-partition).
+  Producer prod;
+  prod.it = make_iter(args, sp);
+  prod.kt = 0;
+  prod.ke = 0;
+  prod.slot = 0;
+  prod.phase = 0;
+  prod.fills = 0;
+#if QG_PRODUCER_WG
+  if (warp >= kConsumerWarps) {
+    // producer warpgroup: give registers back, one lane streams every fill
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;\n" ::"n"(kProducerRegs));
+    if (warp == kConsumerWarps && lane == 0)
+      while (produce_next(prod, args, sA, sB, full, empty)) {
       }
-    }
     return;
   }
+  asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;\n" ::"n"(kConsumerRegs));
+#else
+  if (threadIdx.x == 0)
+    for (int s = 0; s < kStages; ++s) produce_next(prod, args, sA, sB, full, empty);
+#endif
 
   // ---------------- consumers ----------------
   const int wm = warp & 1;   // 32-row half of the CTA tile
@@ -187,6 +234,7 @@ __global__ void __launch_bounds__(kDmmaThreads, 1) qgemm_dmma_kernel(const DmmaA
   const int tid = threadIdx.x;
   int slot = 0;
   uint32_t phase = 0;
+  [[maybe_unused]] bool first = true;
   WorkIter it = make_iter(args, sp);
   Unit u;
   while (it.next(args, u)) {
@@ -198,7 +246,30 @@ __global__ void __launch_bounds__(kDmmaThreads, 1) qgemm_dmma_kernel(const DmmaA
 #pragma unroll
         for (int c = 0; c < 4; ++c) acc[i][j][c][0] = acc[i][j][c][1] = 0.0;
 
+    // k-tile at which to warm L2 with this unit's C tile (beta != 0, epilogue here)
+    const int64_t kt_prefetch =
+        (u.kb == 0 && !args.sc.beta_zero) ? (u.ke - 2 > u.kb ? u.ke - 2 : u.kb) : int64_t(-1);
     for (int64_t kt = u.kb; kt < u.ke; ++kt) {
+      if (kt == kt_prefetch) {
+        int64_t pmt, pnt;
+        tile_coords(u.t, args.MT, args.NT, pmt, pnt);
+#pragma unroll
+        for (int ii = 0; ii < 4; ++ii)
+#pragma unroll
+          for (int jj = 0; jj < 2; ++jj)
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {
+              const int64_t row = pmt * kBR + (wm * 4 + ii) * 8 + (lane >> 2);
+              const int64_t col = pnt * kBR + (wn * 2 + jj) * 8 + 2 * (lane & 3) + e;
+              if (row < args.M && col < args.N)
+                asm volatile("prefetch.global.L2 [%0];\n" ::"l"(args.C + 4 * (row + col * args.ldc)));
+            }
+      }
+      // refill the slot consumption f-1 used (fill f-1+kStages), then consume f
+#if !QG_PRODUCER_WG
+      if (tid == 0 && !first) produce_next(prod, args, sA, sB, full, empty);
+#endif
+      first = false;
       mbar_wait(&full[slot], phase);
       const double2 *a2 = reinterpret_cast<const double2 *>(sA + slot * kChunkElems);
       const double2 *b2 = reinterpret_cast<const double2 *>(sB + slot * kChunkElems);
@@ -299,19 +370,46 @@ __global__ void __launch_bounds__(kDmmaThreads, 1) qgemm_dmma_kernel(const DmmaA
     // D fragment of m8n8k4: lane holds D[lane/4][2*(lane%4) + e], e = 0, 1.
     int64_t mt, nt;
     tile_coords(u.t, args.MT, args.NT, mt, nt);
+    // Two batches of 8 quaternions: all C loads of a batch are issued before
+    // any store, so the 8 round trips overlap (the compiler cannot reorder
+    // loads of C above stores to C on its own).
 #pragma unroll
-    for (int ii = 0; ii < 4; ++ii) {
-      const int64_t row = mt * kBR + (wm * 4 + ii) * 8 + (lane >> 2);
-      if (row >= args.M) continue;
+    for (int h = 0; h < 2; ++h) {
+      double cold[2][2][2][4];
+      bool ok[2][2][2];
+      double *cp[2][2][2];
 #pragma unroll
-      for (int jj = 0; jj < 2; ++jj)
+      for (int i2 = 0; i2 < 2; ++i2)
 #pragma unroll
-        for (int e = 0; e < 2; ++e) {
-          const int64_t col = nt * kBR + (wn * 2 + jj) * 8 + 2 * (lane & 3) + e;
-          if (col >= args.N) continue;
-          const double q[4] = {acc[ii][jj][0][e], acc[ii][jj][1][e], acc[ii][jj][2][e], acc[ii][jj][3][e]};
-          epilogue_one(args.sc, q, args.C + 4 * (row + col * args.ldc));
-        }
+        for (int jj = 0; jj < 2; ++jj)
+#pragma unroll
+          for (int e = 0; e < 2; ++e) {
+            const int ii = 2 * h + i2;
+            const int64_t row = mt * kBR + (wm * 4 + ii) * 8 + (lane >> 2);
+            const int64_t col = nt * kBR + (wn * 2 + jj) * 8 + 2 * (lane & 3) + e;
+            ok[i2][jj][e] = row < args.M && col < args.N;
+            cp[i2][jj][e] = args.C + 4 * (row + col * args.ldc);
+            if (!args.sc.beta_zero && ok[i2][jj][e]) ldq_c(cp[i2][jj][e], cold[i2][jj][e]);
+          }
+#pragma unroll
+      for (int i2 = 0; i2 < 2; ++i2)
+#pragma unroll
+        for (int jj = 0; jj < 2; ++jj)
+#pragma unroll
+          for (int e = 0; e < 2; ++e) {
+            if (!ok[i2][jj][e]) continue;
+            const int ii = 2 * h + i2;
+            const double q[4] = {acc[ii][jj][0][e], acc[ii][jj][1][e], acc[ii][jj][2][e], acc[ii][jj][3][e]};
+            double out[4];
+            left_scale(args.sc.alpha, args.sc.alpha_real, q, out);
+            if (!args.sc.beta_zero) {
+              double bc[4];
+              left_scale(args.sc.beta, args.sc.beta_real, cold[i2][jj][e], bc);
+#pragma unroll
+              for (int k = 0; k < 4; ++k) out[k] += bc[k];
+            }
+            stq(cp[i2][jj][e], out);
+          }
     }
   }
 }
