@@ -91,6 +91,27 @@ size_t qgemm_workspace_bytes(char transA, char transB, int64_t M, int64_t N, int
 /* Smallest accepted workspace (one K-panel), same arguments. */
 size_t qgemm_workspace_min_bytes(char transA, char transB, int64_t M, int64_t N, int64_t K, int dtype);
 
+/* Quaternion Hermitian rank-K update (the paper
+ * names rank-k updates as a reuse target of its GEMM kernels, and
+ * defines quaternion hermiticity Q = Q^H at P:483-492):
+ *     trans = 'N':        C <- alpha * A * A^H + beta * C,   A is N x K (lda >= max(1,N))
+ *     trans = 'H' or 'C': C <- alpha * A^H * A + beta * C,   A is K x N (lda >= max(1,K))
+ * alpha, beta REAL (so a Hermitian C stays Hermitian).  Only the `uplo`
+ * triangle of C ('L' lower or 'U' upper, diagonal included) is read and
+ * written; the other triangle is never touched.  The vector part of every
+ * diagonal entry is set to 0 on output (the diagonal of a Hermitian matrix is
+ * real; R18).  Tiles of the other triangle are not computed: about
+ * half the flops of the equivalent qgemm(N, H).
+ * Storage, ownership, asynchrony, workspace and K-panel behaviour as qgemm.
+ * Quick returns: N == 0, or (alpha == 0 or K == 0) with beta == 1.
+ * Errors: uplo=-1 trans=-2 N=-3 K=-4 A=-6 lda=-7 C=-9 (also: C overlaps A)
+ * ldc=-10 workspace=-11 workspace_bytes=-12; >0 cudaError_t. */
+int qherk(char uplo, char trans, int64_t N, int64_t K, double alpha, const double *A, int64_t lda,
+          double beta, double *C, int64_t ldc, void *workspace, size_t workspace_bytes, void *stream);
+
+/* Workspace bytes for a single-panel qherk call (0 for invalid/quick-return shapes). */
+size_t qherk_workspace_bytes(char uplo, char trans, int64_t N, int64_t K);
+
 /* Debug/cross-check path: one thread per output quaternion, reads op(A) and
  * op(B) in place (no pack, no workspace).  Same arguments, errors and
  * semantics as qgemm() minus the workspace.  Not used by qgemm(). */

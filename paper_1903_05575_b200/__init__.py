@@ -12,6 +12,7 @@ from .qgemm import (  # noqa: F401
     qgemm,
     qgemm_f32,
     qgemm_naive,
+    qherk,
     timing_collect,
     timing_enable,
     version,

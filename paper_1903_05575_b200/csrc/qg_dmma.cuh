@@ -71,6 +71,7 @@ struct DmmaArgs {
   double *partials;   // gridDim.x slots of kPartialBytes
   int *flags;         // T - dp_tiles arrival counters (zero on entry; owners reset them)
   int64_t grid;       // host side: CTAs launched
+  int tri;            // 0: all tiles; 1/2: only tiles of the lower/upper triangle (QHERK)
 };
 
 __device__ __forceinline__ void tile_coords(int64_t pid, int64_t MT, int64_t NT, int64_t &mt, int64_t &nt) {
@@ -81,6 +82,21 @@ __device__ __forceinline__ void tile_coords(int64_t pid, int64_t MT, int64_t NT,
   const int64_t in = pid - g * per_group;
   mt = first_m + in % gsz;
   nt = in / gsz;
+}
+
+// Tile t of the work list: full grid (grouped raster) or, for the triangular
+// (QHERK) schedule, row-major over the lower triangle t = mt(mt+1)/2 + nt.
+__device__ __forceinline__ void work_tile(const DmmaArgs &a, int64_t t, int64_t &mt, int64_t &nt) {
+  if (a.tri == 0) {
+    tile_coords(t, a.MT, a.NT, mt, nt);
+    return;
+  }
+  int64_t r = int64_t((sqrt(8.0 * double(t) + 1.0) - 1.0) * 0.5);
+  while (r * (r + 1) / 2 > t) --r;
+  while ((r + 1) * (r + 2) / 2 <= t) ++r;
+  const int64_t c = t - r * (r + 1) / 2;
+  if (a.tri == 1) { mt = r; nt = c; }
+  else            { mt = c; nt = r; }
 }
 
 // Stream-K range of CTA c: [begin, end) in the SK iteration space.
@@ -161,7 +177,7 @@ __device__ __forceinline__ bool produce_next(Producer &p, const DmmaArgs &args, 
     Unit u;
     if (!p.it.next(args, u)) return false;
     int64_t mt, nt;
-    tile_coords(u.t, args.MT, args.NT, mt, nt);
+    work_tile(args, u.t, mt, nt);
     p.a_src = args.Ap + mt * args.KT * kChunkElems;
     p.b_src = args.Bp + nt * args.KT * kChunkElems;
     p.kt = u.kb;
@@ -252,7 +268,7 @@ __global__ void __launch_bounds__(kDmmaThreads, 1) qgemm_dmma_kernel(const DmmaA
     for (int64_t kt = u.kb; kt < u.ke; ++kt) {
       if (kt == kt_prefetch) {
         int64_t pmt, pnt;
-        tile_coords(u.t, args.MT, args.NT, pmt, pnt);
+        work_tile(args, u.t, pmt, pnt);
 #pragma unroll
         for (int ii = 0; ii < 4; ++ii)
 #pragma unroll
@@ -369,7 +385,7 @@ __global__ void __launch_bounds__(kDmmaThreads, 1) qgemm_dmma_kernel(const DmmaA
     // ---------------- epilogue ----------------
     // D fragment of m8n8k4: lane holds D[lane/4][2*(lane%4) + e], e = 0, 1.
     int64_t mt, nt;
-    tile_coords(u.t, args.MT, args.NT, mt, nt);
+    work_tile(args, u.t, mt, nt);
     // Two batches of 8 quaternions: all C loads of a batch are issued before
     // any store, so the 8 round trips overlap (the compiler cannot reorder
     // loads of C above stores to C on its own).
@@ -387,7 +403,8 @@ __global__ void __launch_bounds__(kDmmaThreads, 1) qgemm_dmma_kernel(const DmmaA
             const int ii = 2 * h + i2;
             const int64_t row = mt * kBR + (wm * 4 + ii) * 8 + (lane >> 2);
             const int64_t col = nt * kBR + (wn * 2 + jj) * 8 + 2 * (lane & 3) + e;
-            ok[i2][jj][e] = row < args.M && col < args.N;
+            ok[i2][jj][e] = row < args.M && col < args.N &&
+                            (args.tri == 0 || (args.tri == 1 ? row >= col : row <= col));
             cp[i2][jj][e] = args.C + 4 * (row + col * args.ldc);
             if (!args.sc.beta_zero && ok[i2][jj][e]) ldq_c(cp[i2][jj][e], cold[i2][jj][e]);
           }
@@ -407,6 +424,12 @@ __global__ void __launch_bounds__(kDmmaThreads, 1) qgemm_dmma_kernel(const DmmaA
               left_scale(args.sc.beta, args.sc.beta_real, cold[i2][jj][e], bc);
 #pragma unroll
               for (int k = 0; k < 4; ++k) out[k] += bc[k];
+            }
+            if (args.tri != 0) {
+              // QHERK: the diagonal of a Hermitian matrix is real (R18)
+              const int64_t row = mt * kBR + (wm * 4 + 2 * h + i2) * 8 + (lane >> 2);
+              const int64_t col = nt * kBR + (wn * 2 + jj) * 8 + 2 * (lane & 3) + e;
+              if (row == col) out[1] = out[2] = out[3] = 0.0;
             }
             stq(cp[i2][jj][e], out);
           }

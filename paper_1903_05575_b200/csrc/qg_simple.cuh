@@ -10,12 +10,16 @@
 
 namespace qg {
 
+// tri = 1/2: only the lower/upper triangle (incl. diagonal) is touched and the
+// diagonal's vector part is set to 0 (QHERK, R18).
 template <typename T>
-__global__ void qgemm_scale_kernel(T *C, int64_t ldc, int64_t M, int64_t N, Scalars<T> sc) {
+__global__ void qgemm_scale_kernel(T *C, int64_t ldc, int64_t M, int64_t N, Scalars<T> sc, int tri) {
   const int64_t total = M * N;
   for (int64_t idx = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; idx < total;
        idx += int64_t(gridDim.x) * blockDim.x) {
     const int64_t i = idx % M, j = idx / M;
+    if (tri == 1 && i < j) continue;
+    if (tri == 2 && i > j) continue;
     T *p = C + 4 * (i + j * ldc);
     T out[4] = {T(0), T(0), T(0), T(0)};
     if (!sc.beta_zero) {
@@ -23,6 +27,7 @@ __global__ void qgemm_scale_kernel(T *C, int64_t ldc, int64_t M, int64_t N, Scal
       ldq_c(p, c);
       left_scale(sc.beta, sc.beta_real, c, out);
     }
+    if (tri != 0 && i == j) out[1] = out[2] = out[3] = T(0);
     stq(p, out);
   }
 }

@@ -165,12 +165,13 @@ int validate(char transA, char transB, int64_t M, int64_t N, int64_t K, const T 
 }
 
 template <typename T>
-int launch_scale(T *C, int64_t ldc, int64_t M, int64_t N, const qg::Scalars<T> &sc, cudaStream_t st) {
+int launch_scale(T *C, int64_t ldc, int64_t M, int64_t N, const qg::Scalars<T> &sc, cudaStream_t st,
+                 int tri = 0) {
   const int64_t total = M * N;
   const int threads = 256;
   const int64_t blocks = std::min<int64_t>(cdiv(total, threads), 148 * 16);
   { int ti = tstart(kScale, st);
-  qg::qgemm_scale_kernel<T><<<unsigned(blocks), threads, 0, st>>>(C, ldc, M, N, sc);
+  qg::qgemm_scale_kernel<T><<<unsigned(blocks), threads, 0, st>>>(C, ldc, M, N, sc, tri);
   tstop(ti, st); }
   ++g_last_launches;
   return int(cudaGetLastError());
@@ -205,7 +206,7 @@ int persistent_ctas() {
 
 // Persistent "data-parallel + stream-K" schedule (see qg_dmma.cuh).
 void plan_schedule(qg::DmmaArgs &a, int resident) {
-  a.T = a.MT * a.NT;
+  a.T = a.tri ? a.MT * (a.MT + 1) / 2 : a.MT * a.NT;
   // fewer tiles than SMs: split k too, but keep >= 2 k-tiles per CTA
   const int64_t G = std::max<int64_t>(1, std::min<int64_t>(resident, std::max<int64_t>(a.T, (a.T * a.KT) / 2)));
   const int64_t waves = a.T / G, rem = a.T % G;
@@ -221,7 +222,7 @@ void plan_schedule(qg::DmmaArgs &a, int resident) {
 }
 
 int launch_mainloop(const double *Ap, const double *Bp, double *C, int64_t ldc, int64_t M, int64_t N,
-                    int64_t KT, const qg::Scalars<double> &sc, void *sk_scratch, cudaStream_t st) {
+                    int64_t KT, const qg::Scalars<double> &sc, void *sk_scratch, cudaStream_t st, int tri = 0) {
   static bool attr_set = false;
   if (!attr_set) {
     cudaError_t e = cudaFuncSetAttribute(qg::qgemm_dmma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -234,6 +235,7 @@ int launch_mainloop(const double *Ap, const double *Bp, double *C, int64_t ldc, 
   qg::DmmaArgs a;
   a.Ap = Ap; a.Bp = Bp; a.C = C; a.ldc = ldc; a.M = M; a.N = N;
   a.MT = cdiv(M, qg::kBR); a.NT = cdiv(N, qg::kBR); a.KT = KT; a.sc = sc;
+  a.tri = tri;
   plan_schedule(a, resident);
   // scratch layout: [2*kMaxPersistentCTAs arrival counters][grid partial slots]
   a.flags = reinterpret_cast<int *>(sk_scratch);
@@ -251,7 +253,8 @@ int launch_mainloop(const double *Ap, const double *Bp, double *C, int64_t ldc, 
 }
 
 int launch_mainloop(const float *Ap, const float *Bp, float *C, int64_t ldc, int64_t M, int64_t N, int64_t KT,
-                    const qg::Scalars<float> &sc, void * /*sk_scratch*/, cudaStream_t st) {
+                    const qg::Scalars<float> &sc, void * /*sk_scratch*/, cudaStream_t st,
+                    int /*tri: FP64 only*/ = 0) {
   static bool attr_set = false;
   if (!attr_set) {
     cudaError_t e = cudaFuncSetAttribute(qg::qgemm_simt_f32_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -269,6 +272,18 @@ int launch_mainloop(const float *Ap, const float *Bp, float *C, int64_t ldc, int
   return int(cudaGetLastError());
 }
 
+// Rows (r) x K panel of an operand as the pack kernel sees it (qg_pack.cuh).
+template <typename T>
+struct PackSpec {
+  const T *X;
+  int64_t ldx;
+  int row_contig, conj;
+};
+template <typename T>
+int panel_loop(const PackSpec<T> &pa, const PackSpec<T> &pb, int64_t M, int64_t N, int64_t K,
+               const qg::Scalars<T> &sc, T *C, int64_t ldc, void *workspace, size_t workspace_bytes,
+               cudaStream_t st, int tri);
+
 template <typename T>
 int qgemm_impl(char transA, char transB, int64_t M, int64_t N, int64_t K, const T *alpha, const T *A,
                int64_t lda, const T *B, int64_t ldb, const T *beta, T *C, int64_t ldc, void *workspace,
@@ -282,8 +297,17 @@ int qgemm_impl(char transA, char transB, int64_t M, int64_t N, int64_t K, const 
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   qg::Scalars<T> sc = make_scalars(alpha, beta);
   if (!reads_ab) return launch_scale(C, ldc, M, N, sc, st);
+  PackSpec<T> pa{A, lda, sh.oa == 0 ? 1 : 0, sh.oa == 2 ? 1 : 0};
+  PackSpec<T> pb{B, ldb, sh.ob == 0 ? 0 : 1, sh.ob == 2 ? 1 : 0};
+  return panel_loop<T>(pa, pb, M, N, K, sc, C, ldc, workspace, workspace_bytes, st, 0);
+}
 
-  // ---- plan: how many K-tiles fit in the workspace at once (K-panel loop, a6)
+// K-panel loop (row a6): pack A, pack B, mainloop per panel that fits.
+template <typename T>
+int panel_loop(const PackSpec<T> &pa, const PackSpec<T> &pb, int64_t M, int64_t N, int64_t K,
+               const qg::Scalars<T> &sc, T *C, int64_t ldc, void *workspace, size_t workspace_bytes,
+               cudaStream_t st, int tri) {
+  int rc = 0;
   const int64_t KT_total = cdiv(K, qg::kBK);
   const size_t min_ws = workspace_for<T>(M, N, K, 1);
   if (workspace == nullptr || (reinterpret_cast<uintptr_t>(workspace) & 255u)) return -14;
@@ -300,8 +324,6 @@ int qgemm_impl(char transA, char transB, int64_t M, int64_t N, int64_t K, const 
   T *Bp = reinterpret_cast<T *>(reinterpret_cast<char *>(workspace) +
                                 align256(size_t(MT) * size_t(KTp) * qg::kChunkElems * sizeof(T)));
   void *sk_scratch = reinterpret_cast<char *>(Bp) + align256(size_t(NT) * size_t(KTp) * qg::kChunkElems * sizeof(T));
-  const int a_row_contig = sh.oa == 0 ? 1 : 0;
-  const int b_row_contig = sh.ob == 0 ? 0 : 1;
   qg::Scalars<T> sc_acc = sc;  // later panels accumulate: beta = 1
   for (int c = 0; c < 4; ++c) sc_acc.beta[c] = T(c == 0 ? 1 : 0);
   sc_acc.beta_real = 1;
@@ -310,14 +332,56 @@ int qgemm_impl(char transA, char transB, int64_t M, int64_t N, int64_t K, const 
     const int64_t k_begin = kt0 * qg::kBK;
     const int64_t k_end = std::min<int64_t>(K, (kt0 + KTp) * qg::kBK);
     const int64_t ktn = cdiv(k_end - k_begin, qg::kBK);
-    rc = launch_pack<T>(A, lda, a_row_contig, sh.oa == 2, M, k_begin, k_end, ktn, Ap, st);
+    rc = launch_pack<T>(pa.X, pa.ldx, pa.row_contig, pa.conj, M, k_begin, k_end, ktn, Ap, st);
     if (rc) return rc;
-    rc = launch_pack<T>(B, ldb, b_row_contig, sh.ob == 2, N, k_begin, k_end, ktn, Bp, st);
+    rc = launch_pack<T>(pb.X, pb.ldx, pb.row_contig, pb.conj, N, k_begin, k_end, ktn, Bp, st);
     if (rc) return rc;
-    rc = launch_mainloop(Ap, Bp, C, ldc, M, N, ktn, kt0 == 0 ? sc : sc_acc, sk_scratch, st);
+    rc = launch_mainloop(Ap, Bp, C, ldc, M, N, ktn, kt0 == 0 ? sc : sc_acc, sk_scratch, st, tri);
     if (rc) return rc;
   }
   return 0;
+}
+
+template <typename T>
+size_t ws_bytes(char transA, char transB, int64_t M, int64_t N, int64_t K, bool minimum);
+
+// QHERK: C <- alpha op(A) op(A)^H + beta C on one
+// triangle, alpha/beta real; same pack + DMMA mainloop, triangular tile list.
+int qherk_impl(char uplo, char trans, int64_t N, int64_t K, double alpha, const double *A, int64_t lda,
+               double beta, double *C, int64_t ldc, void *workspace, size_t workspace_bytes, void *stream) {
+  g_last_launches = 0;
+  const int tri = (uplo == 'L' || uplo == 'l') ? 1 : (uplo == 'U' || uplo == 'u') ? 2 : 0;
+  if (!tri) return -1;
+  const int ot = op_code(trans);
+  if (ot != 0 && ot != 2) return -2;  // 'N' or 'H'/'C' (no plain transpose, as BLAS xHERK)
+  if (N < 0) return -3;
+  if (K < 0) return -4;
+  const int64_t a_rows = ot == 0 ? N : K, a_cols = ot == 0 ? K : N;
+  if (lda < std::max<int64_t>(1, a_rows)) return -7;
+  if (ldc < std::max<int64_t>(1, N)) return -10;
+  if (N == 0) return 0;
+  if (C == nullptr || (reinterpret_cast<uintptr_t>(C) & 15u)) return -9;
+  const bool reads_a = K > 0 && alpha != 0.0;
+  if (!reads_a && beta == 1.0) return 0;  // BLAS quick return
+  if (reads_a) {
+    if (A == nullptr || (reinterpret_cast<uintptr_t>(A) & 15u)) return -6;
+    uintptr_t c0, c1, a0, a1;
+    extent(C, N, N, ldc, c0, c1);
+    extent(A, a_rows, a_cols, lda, a0, a1);
+    if (overlaps(c0, c1, a0, a1)) return -9;
+  }
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  const double al[4] = {alpha, 0, 0, 0}, be[4] = {beta, 0, 0, 0};
+  qg::Scalars<double> sc = make_scalars(al, be);
+  if (!reads_a) return launch_scale(C, ldc, N, N, sc, st, tri);
+  if (workspace == nullptr || (reinterpret_cast<uintptr_t>(workspace) & 255u)) return -11;
+  if (workspace_bytes < workspace_for<double>(N, N, K, 1)) return -12;
+  // op(A) as the A operand; op(B) = op(A)^H as the B operand (same buffer):
+  //   trans N: op(A)(n,k) = A(n,k) -> rows contiguous;  B~(k,n) = conj(A(n,k))
+  //   trans H: op(A)(n,k) = conj(A(k,n));                B~(k,n) = A(k,n)
+  PackSpec<double> pa{A, lda, ot == 0 ? 1 : 0, ot == 0 ? 0 : 1};
+  PackSpec<double> pb{A, lda, ot == 0 ? 1 : 0, ot == 0 ? 1 : 0};
+  return panel_loop<double>(pa, pb, N, N, K, sc, C, ldc, workspace, workspace_bytes, st, tri);
 }
 
 template <typename T>
@@ -374,6 +438,18 @@ int qgemm_naive(char transA, char transB, int64_t M, int64_t N, int64_t K, const
   tstop(ti, st); }
   ++g_last_launches;
   return int(cudaGetLastError());
+}
+
+int qherk(char uplo, char trans, int64_t N, int64_t K, double alpha, const double *A, int64_t lda, double beta,
+          double *C, int64_t ldc, void *workspace, size_t workspace_bytes, void *stream) {
+  return qherk_impl(uplo, trans, N, K, alpha, A, lda, beta, C, ldc, workspace, workspace_bytes, stream);
+}
+
+size_t qherk_workspace_bytes(char uplo, char trans, int64_t N, int64_t K) {
+  const int ot = op_code(trans);
+  if (!(uplo == 'L' || uplo == 'l' || uplo == 'U' || uplo == 'u') || (ot != 0 && ot != 2) || N <= 0 || K <= 0)
+    return 0;
+  return workspace_for<double>(N, N, K, cdiv(K, qg::kBK));
 }
 
 int qgemm_last_launch_count(void) { return g_last_launches; }

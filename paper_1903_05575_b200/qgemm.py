@@ -139,6 +139,36 @@ def last_launch_count() -> int:
     return int(load().qgemm_last_launch_count())
 
 
+HERK_ARGNAMES = {1: "uplo", 2: "trans", 3: "N", 4: "K", 6: "A", 7: "lda", 9: "C", 10: "ldc",
+                 11: "workspace", 12: "workspace_bytes"}
+
+
+def qherk(uplo: str, trans: str, alpha: float, A: torch.Tensor, beta: float, C: torch.Tensor,
+          N: int | None = None, K: int | None = None, workspace: torch.Tensor | None = None,
+          stream: torch.cuda.Stream | None = None):
+    """FP64 Hermitian rank-K update on one triangle of C (include/qgemm.h qherk):
+    trans 'N': C <- alpha A A^H + beta C (A stored N x K); 'H': C <- alpha A^H A + beta C."""
+    _check(C, "C", torch.float64)
+    _check(A, "A", torch.float64)
+    N = C.shape[0] if N is None else N
+    if K is None:
+        K = A.shape[0] if trans.upper() == "N" else A.shape[1]
+    st = (stream or torch.cuda.current_stream(C.device)).cuda_stream
+    lib = load()
+    need = int(lib.qherk_workspace_bytes(uplo.encode(), trans.encode(), N, K))
+    if workspace is None:
+        workspace = get_workspace(need, C.device) if need else None
+    nbytes = workspace.numel() * workspace.element_size() if workspace is not None else 0
+    rc = lib.qherk(uplo.encode(), trans.encode(), N, K, float(alpha), _ptr(A), A.shape[1],
+                   float(beta), _ptr(C), C.shape[1], _ptr(workspace), nbytes, ctypes.c_void_p(st))
+    if rc != 0:
+        err = QgemmError("qherk", rc)
+        if rc < 0:
+            err.args = (f"qherk: argument {-rc} ({HERK_ARGNAMES.get(-rc, '?')}) invalid",)
+        raise err
+    return C
+
+
 KINDS = ("pack", "mainloop", "scale", "naive")
 
 

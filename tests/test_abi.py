@@ -24,7 +24,7 @@ def lib():
 def _header_symbols():
     txt = open(os.path.join(ROOT, "include", "qgemm.h")).read()
     body = txt[txt.index('extern "C" {'):]
-    return set(re.findall(r"\b(qgemm\w*)\s*\(", body))
+    return set(re.findall(r"\b(q(?:gemm|herk)\w*)\s*\(", body))
 
 
 def test_exports_match_header(lib):
@@ -32,7 +32,7 @@ def test_exports_match_header(lib):
     assert declared == set(_lib.EXPORTS)
     out = subprocess.run(["nm", "-D", "--defined-only", _lib.SO_PATH], capture_output=True,
                          text=True, check=True).stdout
-    exported = set(re.findall(r" T (qgemm\w*)$", out, re.M))
+    exported = set(re.findall(r" T (q(?:gemm|herk)\w*)$", out, re.M))
     assert declared <= exported, declared - exported
     for name in declared:
         assert hasattr(lib, name)
@@ -97,6 +97,25 @@ def test_null_AB_allowed_when_not_read(lib):
     # that the first failing argument is C, not A/B.
     assert _call(lib, alpha=0.0, A=None, B=None, C=0x300008) == -12
     assert _call(lib, K=0, A=None, B=None, C=0x300008) == -12
+
+
+def _herk(lib, uplo=b"L", trans=b"N", N=8, K=8, alpha=1.0, A=0x100000, lda=8, beta=1.0, C=0x300000,
+          ldc=8, ws=0x400000, wsb=1 << 30):
+    return lib.qherk(uplo, trans, N, K, alpha, ctypes.c_void_p(A) if A else None, lda, beta,
+                     ctypes.c_void_p(C) if C else None, ldc, ctypes.c_void_p(ws) if ws else None,
+                     wsb, None)
+
+
+@pytest.mark.parametrize("kw,code", [
+    (dict(uplo=b"X"), -1), (dict(trans=b"T"), -2), (dict(N=-1), -3), (dict(K=-1), -4),
+    (dict(lda=7), -7), (dict(trans=b"H", K=9, lda=8), -7), (dict(ldc=7), -10),
+    (dict(A=0x100008), -6), (dict(A=None), -6), (dict(C=0x300004), -9), (dict(C=None), -9),
+    (dict(C=0x100000 + 64), -9), (dict(ws=None), -11), (dict(wsb=100), -12),
+    (dict(N=0, A=None, C=None), 0), (dict(alpha=0.0, A=None), 0), (dict(K=0, A=None), 0),
+])
+def test_qherk_invalid_arguments(lib, kw, code):
+    assert _herk(lib, **kw) == code
+    assert lib.qgemm_last_launch_count() == 0
 
 
 def test_workspace_sizes(lib):

@@ -81,5 +81,21 @@ for c in a.configs.split(","):
         run("c3", 8192, 8192, 8192, "N", "H", 1.0, 1.0, dt=torch.float32, reps=a.reps)
     elif c == "c4":
         run("c4", 32768, 32768, 256, "N", "H", 1.0, 1.0, reps=a.reps)
+    elif c == "c4herk":
+        n, K = 32768, 256
+        A = rnd(K, n, torch.float64)
+        C = rnd(n, n, torch.float64)
+        qg.timing_enable(True)
+        tmin, tmed = timeit(lambda: qg.qherk("L", "N", 1.0, A, 1.0, C), a.reps)
+        kt = qg.timing_collect()
+        qg.timing_enable(False)
+        fl = 32.0 * n * n * K  # the qgemm-equivalent work, for comparison with c4
+        print(json.dumps({"config": "c4herk", "M": n, "N": n, "K": K, "ops": "herk-L-N",
+                          "dtype": "f64", "ms_min": tmin, "ms_med": tmed,
+                          "tflops_best_gemm_equiv": fl / tmin / 1e9,
+                          "tflops_best_actual": fl * (n / 64 + 1) / (2 * n / 64) / tmin / 1e9,
+                          "main_ms_per_call": kt["mainloop"][0] / (a.reps + 1)}), flush=True)
+        del A, C
+        torch.cuda.empty_cache()
     elif c == "c5":
         run("c5", 32768, 32768, 32768, "N", "N", 1.0, 0.0, ws_cap=a.c5_workspace_gb * 1e9, reps=1)
