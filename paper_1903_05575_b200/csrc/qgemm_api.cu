@@ -194,14 +194,20 @@ int launch_pack(const T *X, int64_t ldx, int row_contig, int conj, int64_t R, in
 }
 
 // Resident CTAs of the persistent FP64 mainloop on the current device.
+// (cached per device: the query costs microseconds, which matter at c1 sizes)
 int persistent_ctas() {
+  constexpr int kMaxDev = 64;
+  static int cache[kMaxDev] = {0};
   int dev = 0, sms = 0, per_sm = 0;
   if (cudaGetDevice(&dev) != cudaSuccess) return 0;
+  if (dev < kMaxDev && cache[dev] > 0) return cache[dev];
   if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess) return 0;
   if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, qg::qgemm_dmma_kernel, qg::kDmmaThreads,
                                                     qg::kDmmaSmemBytes) != cudaSuccess)
     return 0;
-  return std::min(qg::kMaxPersistentCTAs, sms * std::max(1, per_sm));
+  const int r = std::min(qg::kMaxPersistentCTAs, sms * std::max(1, per_sm));
+  if (dev < kMaxDev) cache[dev] = r;
+  return r;
 }
 
 // Persistent "data-parallel + stream-K" schedule (see qg_dmma.cuh).
