@@ -15,6 +15,12 @@
 #include "qg_pack.cuh"
 #include "qg_simple.cuh"
 #include "qg_simt_f32.cuh"
+#include "qg_tc32.cuh"
+
+// FP32 mainloop: 1 = tcgen05 3xTF32 (qg_tc32.cuh), 0 = FFMA (qg_simt_f32.cuh)
+#ifndef QG_F32_TC
+#define QG_F32_TC 1
+#endif
 
 namespace {
 
@@ -94,10 +100,32 @@ struct Shape {
   int64_t M, N, K;
 };
 
+// Packed-operand geometry per precision: rows per tile, k per tile, bytes per chunk.
+template <typename T>
+struct Geo;
+template <>
+struct Geo<double> {  // DMMA path (qg_dmma.cuh)
+  static constexpr int64_t rows = qg::kBR, kq = qg::kBK;
+  static constexpr size_t chunk = size_t(qg::kChunkElems) * sizeof(double);
+};
+#if QG_F32_TC
+template <>
+struct Geo<float> {  // tcgen05 3xTF32 path (qg_tc32.cuh): hi + lo planes
+  static constexpr int64_t rows = qg::kTcBM, kq = qg::kTcBK;
+  static constexpr size_t chunk = qg::kTcChunkBytes;
+};
+#else
+template <>
+struct Geo<float> {  // FFMA path (qg_simt_f32.cuh)
+  static constexpr int64_t rows = qg::kBR, kq = qg::kBK;
+  static constexpr size_t chunk = size_t(qg::kChunkElems) * sizeof(float);
+};
+#endif
+
 // Bytes of one K-tile column of packed panels (all MT + NT row tiles).
 template <typename T>
 size_t bytes_per_ktile(int64_t M, int64_t N) {
-  return size_t(cdiv(M, qg::kBR) + cdiv(N, qg::kBR)) * qg::kChunkElems * sizeof(T);
+  return size_t(cdiv(M, Geo<T>::rows) + cdiv(N, Geo<T>::rows)) * Geo<T>::chunk;
 }
 
 // Upper bound of the persistent grid for a panel of `ktiles` k-tiles: the
@@ -123,9 +151,9 @@ template <typename T>
 size_t workspace_for(int64_t M, int64_t N, int64_t K, int64_t ktiles) {
   // the stream-K reserve is sized for the whole K (an upper bound for any panel),
   // so the workspace grows linearly with the panel depth `ktiles`
-  const size_t a = size_t(cdiv(M, qg::kBR)) * size_t(ktiles) * qg::kChunkElems * sizeof(T);
-  const size_t b = size_t(cdiv(N, qg::kBR)) * size_t(ktiles) * qg::kChunkElems * sizeof(T);
-  return align256(a) + align256(b) + sk_reserve<T>(M, N, cdiv(K, qg::kBK));
+  const size_t a = size_t(cdiv(M, Geo<T>::rows)) * size_t(ktiles) * Geo<T>::chunk;
+  const size_t b = size_t(cdiv(N, Geo<T>::rows)) * size_t(ktiles) * Geo<T>::chunk;
+  return align256(a) + align256(b) + sk_reserve<T>(M, N, cdiv(K, Geo<T>::kq));
 }
 
 // Argument validation common to all entry points.  Returns 0 or -i.
@@ -180,14 +208,18 @@ int launch_scale(T *C, int64_t ldc, int64_t M, int64_t N, const qg::Scalars<T> &
 template <typename T>
 int launch_pack(const T *X, int64_t ldx, int row_contig, int conj, int64_t R, int64_t k_begin, int64_t k_end,
                 int64_t KT, T *out, cudaStream_t st) {
-  const int64_t blocks = cdiv(R, qg::kBR) * KT;
+  const int64_t blocks = cdiv(R, Geo<T>::rows) * KT;
   int ti = tstart(kPack, st);
   if constexpr (sizeof(T) == 8)
     qg::pack_kernel<T, qg::FragLayout><<<unsigned(blocks), 256, 0, st>>>(X, ldx, row_contig, conj, R, k_begin,
                                                                         k_end, KT, out);
   else
+#if QG_F32_TC
+    qg::pack_tc32_kernel<<<unsigned(blocks), 256, 0, st>>>(X, ldx, row_contig, conj, R, k_begin, k_end, KT, out);
+#else
     qg::pack_kernel<T, qg::PlanarLayout><<<unsigned(blocks), 256, 0, st>>>(X, ldx, row_contig, conj, R,
                                                                           k_begin, k_end, KT, out);
+#endif
   tstop(ti, st);
   ++g_last_launches;
   return int(cudaGetLastError());
@@ -261,6 +293,23 @@ int launch_mainloop(const double *Ap, const double *Bp, double *C, int64_t ldc, 
 int launch_mainloop(const float *Ap, const float *Bp, float *C, int64_t ldc, int64_t M, int64_t N, int64_t KT,
                     const qg::Scalars<float> &sc, void * /*sk_scratch*/, cudaStream_t st,
                     int /*tri: FP64 only*/ = 0) {
+#if QG_F32_TC
+  static bool tc_attr_set = false;
+  if (!tc_attr_set) {
+    cudaError_t e = cudaFuncSetAttribute(qg::qgemm_tc32_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         int(qg::kTcSmemBytes));
+    if (e != cudaSuccess) return int(e);
+    tc_attr_set = true;
+  }
+  qg::Tc32Args t;
+  t.Ap = Ap; t.Bp = Bp; t.C = C; t.ldc = ldc; t.M = M; t.N = N;
+  t.MT = cdiv(M, qg::kTcBM); t.NT = cdiv(N, qg::kTcBN); t.KT = KT; t.sc = sc;
+  { int ti = tstart(kMain, st);
+  qg::qgemm_tc32_kernel<<<unsigned(t.MT * t.NT), qg::kTcThreads, qg::kTcSmemBytes, st>>>(t);
+  tstop(ti, st); }
+  ++g_last_launches;
+  return int(cudaGetLastError());
+#endif
   static bool attr_set = false;
   if (!attr_set) {
     cudaError_t e = cudaFuncSetAttribute(qg::qgemm_simt_f32_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -314,7 +363,7 @@ int panel_loop(const PackSpec<T> &pa, const PackSpec<T> &pb, int64_t M, int64_t 
                const qg::Scalars<T> &sc, T *C, int64_t ldc, void *workspace, size_t workspace_bytes,
                cudaStream_t st, int tri) {
   int rc = 0;
-  const int64_t KT_total = cdiv(K, qg::kBK);
+  const int64_t KT_total = cdiv(K, Geo<T>::kq);
   const size_t min_ws = workspace_for<T>(M, N, K, 1);
   if (workspace == nullptr || (reinterpret_cast<uintptr_t>(workspace) & 255u)) return -14;
   if (workspace_bytes < min_ws) return -15;
@@ -325,19 +374,19 @@ int panel_loop(const PackSpec<T> &pa, const PackSpec<T> &pb, int64_t M, int64_t 
     int64_t est = int64_t((workspace_bytes - res) / bytes_per_ktile<T>(M, N));
     KTp = std::max<int64_t>(1, std::min<int64_t>(KTp - 1, est));
   }
-  const int64_t MT = cdiv(M, qg::kBR), NT = cdiv(N, qg::kBR);
+  const int64_t MT = cdiv(M, Geo<T>::rows), NT = cdiv(N, Geo<T>::rows);
   T *Ap = reinterpret_cast<T *>(workspace);
   T *Bp = reinterpret_cast<T *>(reinterpret_cast<char *>(workspace) +
-                                align256(size_t(MT) * size_t(KTp) * qg::kChunkElems * sizeof(T)));
-  void *sk_scratch = reinterpret_cast<char *>(Bp) + align256(size_t(NT) * size_t(KTp) * qg::kChunkElems * sizeof(T));
+                                align256(size_t(MT) * size_t(KTp) * Geo<T>::chunk));
+  void *sk_scratch = reinterpret_cast<char *>(Bp) + align256(size_t(NT) * size_t(KTp) * Geo<T>::chunk);
   qg::Scalars<T> sc_acc = sc;  // later panels accumulate: beta = 1
   for (int c = 0; c < 4; ++c) sc_acc.beta[c] = T(c == 0 ? 1 : 0);
   sc_acc.beta_real = 1;
   sc_acc.beta_zero = 0;
   for (int64_t kt0 = 0; kt0 < KT_total; kt0 += KTp) {
-    const int64_t k_begin = kt0 * qg::kBK;
-    const int64_t k_end = std::min<int64_t>(K, (kt0 + KTp) * qg::kBK);
-    const int64_t ktn = cdiv(k_end - k_begin, qg::kBK);
+    const int64_t k_begin = kt0 * Geo<T>::kq;
+    const int64_t k_end = std::min<int64_t>(K, (kt0 + KTp) * Geo<T>::kq);
+    const int64_t ktn = cdiv(k_end - k_begin, Geo<T>::kq);
     rc = launch_pack<T>(pa.X, pa.ldx, pa.row_contig, pa.conj, M, k_begin, k_end, ktn, Ap, st);
     if (rc) return rc;
     rc = launch_pack<T>(pb.X, pb.ldx, pb.row_contig, pb.conj, N, k_begin, k_end, ktn, Bp, st);
@@ -393,7 +442,7 @@ int qherk_impl(char uplo, char trans, int64_t N, int64_t K, double alpha, const 
 template <typename T>
 size_t ws_bytes(char transA, char transB, int64_t M, int64_t N, int64_t K, bool minimum) {
   if (op_code(transA) < 0 || op_code(transB) < 0 || M <= 0 || N <= 0 || K <= 0) return 0;
-  return workspace_for<T>(M, N, K, minimum ? 1 : cdiv(K, qg::kBK));
+  return workspace_for<T>(M, N, K, minimum ? 1 : cdiv(K, Geo<T>::kq));
 }
 
 }  // namespace

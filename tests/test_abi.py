@@ -125,7 +125,7 @@ def test_workspace_sizes(lib):
     # mainloop: 256 partial slots of 128 KiB + 512 arrival counters
     sk = 256 * 131072 + 2048
     assert f64 == 2 * 8192 * 8192 * 32 + sk
-    assert f32 == 2 * 8192 * 8192 * 16
+    assert f32 == 2 * 8192 * 8192 * 32  # tcgen05 3xTF32 path: tf32 hi + lo planes
     # one K-tile: 2 row tiles of A + 2 of B, 32 KiB per (64 x 16)-quaternion chunk,
     # + partial slots for the largest grid over the whole K (4 tiles x 63 k-tiles
     # / 2 = 126 CTAs) + counters
