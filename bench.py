@@ -35,6 +35,8 @@ METRIC = "QGEMM FP64 TFLOP/s (32 flops/quat-MAC) and % of FP64 peak at 1/2/4/8 G
 FP64_DMMA_PEAK_TFLOPS = 37.0
 FP64_NOMINAL_TFLOPS = 148 * 64 * 2 * 1.965e9 / 1e12  # 37.22
 FP32_NOMINAL_TFLOPS = 148 * 128 * 2 * 1.965e9 / 1e12  # 74.4 (FFMA pipe)
+# tf32 dense tensor peak: measured bf16 (MEASURED_PEAKS.json) x nominal tf32/bf16 (1.1/2.25)
+TF32_PEAK_TFLOPS = 1646.9 * 1.1 / 2.25
 
 
 def parse():
@@ -48,6 +50,7 @@ def parse():
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-f32", action="store_true", help="skip the FP32 (tcgen05) variant")
     return ap.parse_args()
 
 
@@ -191,6 +194,74 @@ def run_reference(args):
     return 0
 
 
+# ------------------------------------------------------------------ rooflines
+def _traffic(key):
+    tp = os.path.join(ROOT, "profiles", "traffic.json")
+    try:
+        return json.load(open(tp)).get(key)
+    except Exception:
+        return None
+
+
+def make_roofline(precision, achieved, main_ms, step_ms, pack_ms, steps):
+    """Roofline of the dominant kernel.  achieved = algorithmic flops (32 per
+    quaternion MAC) per launch / measured mean launch time."""
+    if precision == "f64":
+        return {"bound": "tensor", "kernel": "qgemm_dmma_kernel", "achieved": achieved,
+                "peak": FP64_DMMA_PEAK_TFLOPS, "unit": "TFLOP/s",
+                "frac": (achieved / FP64_DMMA_PEAK_TFLOPS) if achieved else None,
+                "traffic": _traffic("f64_mainloop_bytes_per_launch"),
+                "peak_source": "measured DMMA.8x8x4 loop on this pool's B200, "
+                               "tools/microbench/fp64_pipes.cu (profiles/r01_fp64_pipes.txt)",
+                "frac_of_nominal_37_22": (achieved / FP64_NOMINAL_TFLOPS) if achieved else None,
+                "kernel_share_of_step": main_ms / step_ms if step_ms else None,
+                "pack_ms_per_step": pack_ms / max(1, steps)}
+    # FP32: tcgen05 kind::tf32, 3 MMAs per real product (3xTF32)
+    mma = 3 * achieved if achieved else None
+    return {"bound": "tensor", "kernel": "qgemm_tc32_kernel", "achieved": mma,
+            "peak": TF32_PEAK_TFLOPS, "unit": "TFLOP/s", "frac": (mma / TF32_PEAK_TFLOPS) if mma else None,
+            "achieved_algorithmic": achieved,
+            "frac_algorithmic": (achieved / TF32_PEAK_TFLOPS) if achieved else None,
+            "traffic": _traffic("f32_mainloop_bytes_per_launch"),
+            "peak_source": "MEASURED_PEAKS.json bf16_tflops 1646.9 x nominal tf32/bf16 ratio "
+                           "(1.1/2.25, B200_PROFILING.md); achieved counts the 3 tf32 MMAs per "
+                           "real product of 3xTF32",
+            "kernel_share_of_step": main_ms / step_ms if step_ms else None,
+            "pack_ms_per_step": pack_ms / max(1, steps)}
+
+
+def measure_f32_variant(A, B, C, n, warmup, steps):
+    """c3 in FP32 (BASELINE config 3's second precision) on the same inputs,
+    rounded to FP32 on the device; device-resident, CUDA events."""
+    import torch
+    import paper_1903_05575_b200 as qg
+    A32, B32, C32 = A.float(), B.float(), C.float()
+    ws = qg.get_workspace(qg.workspace_bytes("N", "H", n, n, n, torch.float32), A.device)
+    for _ in range(max(1, warmup)):
+        qg.qgemm_f32("N", "H", 1.0, A32, B32, 1.0, C32, workspace=ws)
+    torch.cuda.synchronize()
+    qg.timing_enable(True)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(steps):
+        qg.qgemm_f32("N", "H", 1.0, A32, B32, 1.0, C32, workspace=ws)
+    e1.record()
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1)
+    kt = qg.timing_collect()
+    qg.timing_enable(False)
+    fl = 32.0 * n ** 3
+    main_ms, main_cnt = kt["mainloop"]
+    achieved = fl / (main_ms / max(1, main_cnt) / 1e3) / 1e12 if main_cnt else None
+    del A32, B32, C32
+    torch.cuda.empty_cache()
+    return {"workload": "c3 FP32: M=N=K=8192 opA=N opB=H alpha=beta=1 (inputs = FP64 draws "
+                        "rounded to FP32)", "dtype": "f32 (3xTF32 on tcgen05, FP32 accumulate)",
+            "value": fl * steps / (ms / 1e3) / 1e12, "unit": "TFLOP/s", "ms_per_step": ms / steps,
+            "steps": steps, "roofline": make_roofline("f32", achieved, main_ms, ms, kt["pack"][0],
+                                                      steps)}
+
+
 # ------------------------------------------------------------------ our arm
 def run_ours(args):
     import torch
@@ -261,25 +332,7 @@ def run_ours(args):
     pack_ms, pack_cnt = kt["pack"]
     main_avg_s = main_ms / max(1, main_cnt) / 1e3
     achieved = 32.0 * n * n * n / main_avg_s / 1e12 if main_cnt else None
-    peak = FP64_DMMA_PEAK_TFLOPS if args.precision == "f64" else FP32_NOMINAL_TFLOPS
-    traffic = None
-    tp = os.path.join(ROOT, "profiles", "traffic.json")
-    if os.path.exists(tp):
-        try:
-            traffic = json.load(open(tp)).get(f"{args.precision}_mainloop_bytes_per_launch")
-        except Exception:
-            traffic = None
-    roofline = {"bound": "tensor" if args.precision == "f64" else "alu",
-                "kernel": "qgemm_dmma_kernel" if args.precision == "f64" else "qgemm_simt_f32_kernel",
-                "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
-                "frac": (achieved / peak) if achieved else None, "traffic": traffic,
-                "peak_source": ("measured DMMA.8x8x4 loop, tools/microbench/fp64_pipes.cu "
-                                "(profiles/r01_fp64_pipes.txt)" if args.precision == "f64"
-                                else "nominal 148 SM x 128 FFMA/clk x 2 x 1.965 GHz"),
-                "frac_of_nominal_37_22": (achieved / FP64_NOMINAL_TFLOPS) if achieved and
-                args.precision == "f64" else None,
-                "kernel_share_of_step": main_ms / ms if ms else None,
-                "pack_ms_per_step": pack_ms / max(1, args.steps)}
+    roofline = make_roofline(args.precision, achieved, main_ms, ms, pack_ms, args.steps)
 
     # ---------------- e2e through the public API with host buffers
     e2e = None
@@ -322,6 +375,10 @@ def run_ours(args):
                "steps": e_steps, "ms_per_step": ems / e_steps,
                "path": "pinned host -> qgemm C ABI (ctypes) -> pinned host"}
 
+    variants = None
+    if world == 1 and args.precision == "f64" and not args.no_f32:
+        variants = {"c3_fp32": measure_f32_variant(A, B, C, n, args.warmup, args.steps)}
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
         cpu = cpu_baseline(A_h, B_h, C_h, n, args.cpu_seconds)
@@ -342,7 +399,7 @@ def run_ours(args):
                            "l2": "inputs (2.15 GB/matrix) >> 126 MB L2; no flush",
                            "timed": "pack A + pack B + DMMA mainloop/epilogue per step"
                                     + (" + NCCL broadcast(B) + gather(C)" if world > 1 else "")},
-                "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
+                "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "variants": variants,
                 "gpu_launches": launches, "clocks": clocks,
                 "library": qg.version()}
         print(json.dumps(line), flush=True)

@@ -528,6 +528,12 @@ int qgemm_timing_collect(double ms[4], int counts[4]) {
   return rc;
 }
 
-const char *qgemm_version(void) { return "qgemm-b200 0.1 (sm_100a; FP64 DMMA.8x8x4, FP32 FFMA)"; }
+const char *qgemm_version(void) {
+#if QG_F32_TC
+  return "qgemm-b200 0.2 (sm_100a; FP64 DMMA.8x8x4 persistent stream-K; FP32 tcgen05 3xTF32)";
+#else
+  return "qgemm-b200 0.2 (sm_100a; FP64 DMMA.8x8x4 persistent stream-K; FP32 FFMA)";
+#endif
+}
 
 }  // extern "C"
