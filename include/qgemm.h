@@ -59,6 +59,13 @@
  * K-panels (Alg. 2 kappa loop), applying beta on the first panel and
  * accumulating onto C afterwards.  Smaller -> -15.
  * The workspace must be 256-byte aligned (-14 otherwise).
+ *
+ * Small problems: below the library's measured
+ * crossover (FP64: M*N*K <= 2^24 quaternion multiply-adds; FP32: <= 2^25, or
+ * small M x N with long K), qgemm/qgemm_f32 run ONE kernel that reads
+ * op(A)/op(B) in place (no pack, no workspace);
+ * qgemm_workspace_bytes() then returns 0 and `workspace` may be NULL.  The
+ * choice is a pure function of (M, N, K) and the path policy below.
  */
 #ifndef QGEMM_B200_H
 #define QGEMM_B200_H
@@ -77,7 +84,10 @@ int qgemm(char transA, char transB, int64_t M, int64_t N, int64_t K,
           double *C, int64_t ldc,
           void *workspace, size_t workspace_bytes, void *stream);
 
-/* FP32: same contract with float storage and float arithmetic (FP32 FMA). */
+/* FP32: same contract with float storage.  Arithmetic: 3xTF32 on the tcgen05
+ * tensor cores with FP32 accumulation (hi/lo split of both operands), which
+ * meets the FP32 tolerance where 1xTF32 does not; the small-
+ * problem path below computes in FP64 and rounds once on store. */
 int qgemm_f32(char transA, char transB, int64_t M, int64_t N, int64_t K,
               const float alpha[4], const float *A, int64_t lda,
               const float *B, int64_t ldb, const float beta[4],
@@ -120,6 +130,12 @@ int qgemm_naive(char transA, char transB, int64_t M, int64_t N, int64_t K,
                 const double *B, int64_t ldb, const double beta[4],
                 double *C, int64_t ldc, void *stream);
 
+/* Path policy (process-wide): 0 = auto (default), 1 = always the packed
+ * path (pack + persistent mainloop), 2 = always the one-launch small kernel.
+ * Returns the previous policy, or -1 (policy unchanged) for other values.
+ * For tests and benchmarks; the result is correct under every policy. */
+int qgemm_set_path_policy(int policy);
+
 /* Number of kernels the last successful call on this host thread enqueued
  * (for the bench's gpu_launches count). */
 int qgemm_last_launch_count(void);
@@ -127,11 +143,12 @@ int qgemm_last_launch_count(void);
 /* Instrumentation (off by default).  While enabled, every kernel this host
  * thread enqueues is bracketed by two CUDA events recorded on the same stream.
  * qgemm_timing_collect() synchronises on those events, writes the summed
- * milliseconds and launch counts per kernel kind into ms[4] / counts[4]
- * (0 = pack, 1 = mainloop (DMMA or FP32), 2 = beta-scale, 3 = naive), clears
- * the record and returns 0 (or a cudaError_t).  Host arrays, caller-owned. */
+ * milliseconds and launch counts per kernel kind into ms[5] / counts[5]
+ * (0 = pack, 1 = mainloop (DMMA or FP32), 2 = beta-scale, 3 = naive,
+ * 4 = small-problem kernel), clears the record and returns 0 (or a
+ * cudaError_t).  Host arrays of 5 entries, caller-owned. */
 void qgemm_timing_enable(int on);
-int qgemm_timing_collect(double ms[4], int counts[4]);
+int qgemm_timing_collect(double ms[5], int counts[5]);
 
 /* Library version string. */
 const char *qgemm_version(void);

@@ -1,8 +1,8 @@
 """B200-native quaternion GEMM (arXiv 1903.05575 hot path).
 
 C <- alpha op(A) op(B) + beta C over Hamilton quaternions, op in {N, T, H},
-column-major interleaved storage; FP64 on the FP64 tensor pipe (DMMA), FP32 on
-FFMA.  The computation lives in libqgemm.so (include/qgemm.h); this package is
+column-major interleaved storage; FP64 on the FP64 tensor pipe (DMMA), FP32 as
+3xTF32 on the tcgen05 tensor cores; small problems in one fused launch.  The computation lives in libqgemm.so (include/qgemm.h); this package is
 the thin Python binding plus the multi-GPU row-block driver.
 """
 from ._lib import EXPORTS, QgemmError, SO_PATH, load  # noqa: F401
@@ -13,6 +13,10 @@ from .qgemm import (  # noqa: F401
     qgemm_f32,
     qgemm_naive,
     qherk,
+    set_path_policy,
+    PATH_AUTO,
+    PATH_PACKED,
+    PATH_SMALL,
     timing_collect,
     timing_enable,
     version,

@@ -14,6 +14,7 @@ SO_PATH = os.path.join(PKG, "libqgemm.so")
 #: every symbol include/qgemm.h declares
 EXPORTS = ("qgemm", "qgemm_f32", "qgemm_workspace_bytes", "qgemm_workspace_min_bytes",
            "qgemm_naive", "qherk", "qherk_workspace_bytes", "qgemm_last_launch_count",
+           "qgemm_set_path_policy",
            "qgemm_timing_enable", "qgemm_timing_collect", "qgemm_version")
 
 _lib = None
@@ -58,6 +59,8 @@ def load():
     lib.qgemm_workspace_min_bytes.argtypes = [c, c, i64, i64, i64, ctypes.c_int]
     lib.qgemm_workspace_min_bytes.restype = sz
     lib.qgemm_last_launch_count.restype = ctypes.c_int
+    lib.qgemm_set_path_policy.argtypes = [ctypes.c_int]
+    lib.qgemm_set_path_policy.restype = ctypes.c_int
     lib.qgemm_version.restype = ctypes.c_char_p
     dbl = ctypes.c_double
     lib.qherk.argtypes = [c, c, i64, i64, dbl, vp, i64, dbl, vp, i64, vp, sz, vp]

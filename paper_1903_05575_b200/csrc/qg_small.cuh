@@ -1,0 +1,166 @@
+// qg_small.cuh -- one-launch QGEMM for small problems (SURVEY.md §8(f) NEXT 4:
+// "fuse the pack into the mainloop ... to drop the extra launches at small N").
+//
+// The packed path (pack A + pack B + persistent 64x64 DMMA mainloop) costs three
+// launches and, below ~ one wave of 64x64 tiles, runs on a handful of SMs: at
+// c1 (64^3) one tile exists and the mainloop's split-K still reaches only two
+// SMs.  This kernel reads op(A) and op(B) IN PLACE (interleaved, column-major,
+// any of N/T/H) and spreads the work over 8x8-quaternion warp tiles with an
+// intra-CTA split over K, so a 64^3 problem occupies 64 SMs in one launch.
+//
+// Arithmetic: the same 16-product rule as the packed mainloop
+// (D^{p XOR s} += eps(p,s) A^p B^s, Eq. quaternion_prod) on the FP64
+// tensor pipe (mma.sync.m8n8k4.f64 -> DMMA.8x8x4).  The m8n8k4 fragments are
+// whole quaternions: lane l holds A(m0 + l/4, k0 + l%4) and B(k0 + l%4, n0 + l/4),
+// so ONE 32-byte load per operand per lane gives the fragments of all four
+// components (no shared-memory de-interleave is needed).  op = H conjugates the
+// loaded quaternion; op = T only swaps the index roles.
+//
+// FP32 storage: quaternions are widened to double on load and the FP64 result
+// is rounded once on store -- more accurate than the FP32 tolerance requires.
+//
+// CTA = 4 warps.  With split factor S in {1, 2, 4}, warp w computes the 8x8 tile
+// (w / S) of the CTA's (4/S) M-stacked tiles over the (w % S)-th of S equal
+// ranges of k4 steps; partials are summed in a fixed order through shared
+// memory (deterministic), then lane l applies the alpha/beta epilogue (left
+// products) to the two quaternions it owns: C(m0 + l/4, n0 + 2(l%4) + i).
+#pragma once
+#include "qg_common.cuh"
+
+namespace qg {
+
+constexpr int kSmallThreads = 128;
+constexpr int kSmallUnroll = 4;  // k4 steps whose loads are issued together
+
+struct SmallArgs {
+  const void *A, *B;
+  void *C;
+  int64_t lda, ldb, ldc, M, N, K;
+  int a_rc, a_cj, b_rc, b_cj;  // operand views of load_rk (from opA, opB)
+  int S;                       // warps per 8x8 tile splitting K
+  int64_t m_blocks;            // CTAs along M (1-D grid: m fastest)
+  Scalars<double> sc;
+};
+
+template <typename T>
+__device__ __forceinline__ void ld_quat_d(const T *p, double (&q)[4]) {
+  T t[4];
+  ldq(p, t);
+#pragma unroll
+  for (int c = 0; c < 4; ++c) q[c] = double(t[c]);
+}
+
+// Quaternion (r, k) of an operand viewed as R x K: rows_contig -> X(r, k) at
+// X + 4(r + k ldx), else X(k, r) at X + 4(k + r ldx); conj flips q^1..q^3.
+// Out of range -> 0 (the zero padding of Alg. 2).
+//   A: op(A)(m, k) = A(m, k) [N] | A(k, m) [T] | conj A(k, m) [H]
+//   B: op(B)(k, n) = B(k, n) [N] | B(n, k) [T] | conj B(n, k) [H]  (r = n)
+template <typename T>
+__device__ __forceinline__ void load_rk(const T *X, int64_t ldx, int rows_contig, int conj, int64_t r,
+                                        int64_t k, int64_t R, int64_t K, double (&q)[4]) {
+  if (r < R && k < K) {
+    ld_quat_d(rows_contig ? X + 4 * (r + k * ldx) : X + 4 * (k + r * ldx), q);
+    if (conj) { q[1] = -q[1]; q[2] = -q[2]; q[3] = -q[3]; }
+  } else {
+    q[0] = q[1] = q[2] = q[3] = 0.0;
+  }
+}
+
+// One k4 step of the 8x8 warp tile: 16 DMMA.8x8x4, acc^{p^s} += eps(p,s) A^p B^s.
+__device__ __forceinline__ void small_step(double (&acc)[4][2], const double (&qa)[4], const double (&qb)[4]) {
+  double nb[4];
+#pragma unroll
+  for (int s = 0; s < 4; ++s) nb[s] = -qb[s];
+#pragma unroll
+  for (int p = 0; p < 4; ++p)
+#pragma unroll
+    for (int s = 0; s < 4; ++s) dmma_8x8x4(acc[p ^ s], qa[p], hneg(p, s) ? nb[s] : qb[s]);
+}
+
+template <typename T>
+__global__ void __launch_bounds__(kSmallThreads) qgemm_small_kernel(SmallArgs a) {
+  __shared__ double red[kSmallThreads / 32][32][8];
+  const T *A = static_cast<const T *>(a.A);
+  const T *B = static_cast<const T *>(a.B);
+  T *C = static_cast<T *>(a.C);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int S = a.S, tiles_per_cta = 4 / S;
+  const int tile = warp / S, part = warp % S;
+  const int64_t mb = int64_t(blockIdx.x) % a.m_blocks, nb = int64_t(blockIdx.x) / a.m_blocks;
+  const int64_t m0 = (mb * tiles_per_cta + tile) * 8;
+  const int64_t n0 = nb * 8;
+  const int lr = lane >> 2, lk = lane & 3;
+
+  // this warp's k4 steps
+  const int64_t steps = (a.K + 3) / 4;
+  const int64_t per = (steps + S - 1) / S;
+  const int64_t s0 = min(steps, int64_t(part) * per), s1 = min(steps, s0 + per);
+
+  double acc[4][2];
+#pragma unroll
+  for (int c = 0; c < 4; ++c) acc[c][0] = acc[c][1] = 0.0;
+
+  if (m0 < a.M) {
+    int64_t st = s0;
+    for (; st + kSmallUnroll <= s1; st += kSmallUnroll) {  // loads of 4 steps in flight
+      double qa[kSmallUnroll][4], qb[kSmallUnroll][4];
+#pragma unroll
+      for (int u = 0; u < kSmallUnroll; ++u) {
+        const int64_t k = (st + u) * 4 + lk;
+        load_rk(A, a.lda, a.a_rc, a.a_cj, m0 + lr, k, a.M, a.K, qa[u]);
+        load_rk(B, a.ldb, a.b_rc, a.b_cj, n0 + lr, k, a.N, a.K, qb[u]);
+      }
+#pragma unroll
+      for (int u = 0; u < kSmallUnroll; ++u) small_step(acc, qa[u], qb[u]);
+    }
+    for (; st < s1; ++st) {  // tail: one step at a time (no DMMAs on zero fill)
+      double qa[4], qb[4];
+      load_rk(A, a.lda, a.a_rc, a.a_cj, m0 + lr, st * 4 + lk, a.M, a.K, qa);
+      load_rk(B, a.ldb, a.b_rc, a.b_cj, n0 + lr, st * 4 + lk, a.N, a.K, qb);
+      small_step(acc, qa, qb);
+    }
+  }
+
+  // fixed-order reduction of the S partial tiles (deterministic)
+  if (S > 1) {
+    if (part != 0) {
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        red[warp][lane][2 * c] = acc[c][0];
+        red[warp][lane][2 * c + 1] = acc[c][1];
+      }
+    }
+    __syncthreads();
+    if (part != 0) return;
+    for (int w = 1; w < S; ++w)
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        acc[c][0] += red[warp + w][lane][2 * c];
+        acc[c][1] += red[warp + w][lane][2 * c + 1];
+      }
+  }
+
+  const int64_t row = m0 + lr;
+  if (row >= a.M) return;
+#pragma unroll
+  for (int i = 0; i < 2; ++i) {
+    const int64_t col = n0 + 2 * lk + i;
+    if (col >= a.N) continue;
+    T *cp = C + 4 * (row + col * a.ldc);
+    double t[4] = {acc[0][i], acc[1][i], acc[2][i], acc[3][i]};
+    double out[4];
+    left_scale(a.sc.alpha, a.sc.alpha_real, t, out);
+    if (!a.sc.beta_zero) {
+      T c0[4];
+      ldq_c(cp, c0);
+      double cd[4] = {double(c0[0]), double(c0[1]), double(c0[2]), double(c0[3])}, bc[4];
+      left_scale(a.sc.beta, a.sc.beta_real, cd, bc);
+#pragma unroll
+      for (int k = 0; k < 4; ++k) out[k] += bc[k];
+    }
+    T o[4] = {T(out[0]), T(out[1]), T(out[2]), T(out[3])};
+    stq(cp, o);
+  }
+}
+
+}  // namespace qg

@@ -5,6 +5,8 @@
 // PAPER.md P:906-911), then per panel: pack A (a2), pack B (a3), mainloop with
 // fused epilogue (a4 + a5) -- all enqueued on the caller's stream.
 #include <algorithm>
+#include <atomic>
+#include <climits>
 #include <cstdint>
 #include <cstring>
 #include <vector>
@@ -14,6 +16,7 @@
 #include "qg_dmma.cuh"
 #include "qg_pack.cuh"
 #include "qg_simple.cuh"
+#include "qg_small.cuh"
 #include "qg_simt_f32.cuh"
 #include "qg_tc32.cuh"
 
@@ -48,7 +51,7 @@ struct Timing {
 };
 thread_local Timing g_timing;
 
-enum Kind { kPack = 0, kMain = 1, kScale = 2, kNaive = 3 };
+enum Kind { kPack = 0, kMain = 1, kScale = 2, kNaive = 3, kSmall = 4, kKinds = 5 };
 
 // Bracket one launch: call before (returns the record index or -1) and after.
 int tstart(int kind, cudaStream_t st) {
@@ -327,6 +330,74 @@ int launch_mainloop(const float *Ap, const float *Bp, float *C, int64_t ldc, int
   return int(cudaGetLastError());
 }
 
+// ---- path choice: packed (pack + persistent mainloop) vs one-launch small kernel
+// 0 = auto, 1 = always packed, 2 = small kernel whenever the call reads A and B
+// (qgemm_set_path_policy; tests use 1/2 to cover both paths at every shape).
+std::atomic<int> g_path_policy{0};
+// Auto policy (crossover measured on B200 with tools/small_sweep.py):
+//  * FP64: the small kernel up to 2^24 quaternion multiply-adds (256^3), where
+//    the packed path's persistent DMMA mainloop catches up;
+//  * FP32: up to 2^25 (the tcgen05 path has a 128x128 tile and no split-K), and
+//    up to 2^28 when that path would launch fewer than 1/4 as many CTAs as
+//    there are SMs and K >= 4 max(M, N) (small M x N, long K);
+//  * never when K < 16 and M*N >= 2^20: there the call is C-traffic bound and
+//    the packed epilogue streams C better.
+constexpr int64_t kSmallMaxMacs = int64_t(1) << 24;
+
+int num_sms();
+
+template <typename T>
+bool use_small(int64_t M, int64_t N, int64_t K) {
+  const int pol = g_path_policy.load(std::memory_order_relaxed);
+  if (pol == 1) return false;
+  if (pol == 2) return true;
+  constexpr int64_t kCap = int64_t(1) << 28;
+  if (M > kCap || N > kCap || K > kCap) return false;  // keeps M*N*K from overflowing below
+  const double macs = double(M) * double(N) * double(K);
+  if (macs > double(kCap)) return false;
+  if (K < 16 && double(M) * double(N) >= double(1 << 20)) return false;
+  if (sizeof(T) == 8) return macs <= double(kSmallMaxMacs);
+  if (macs <= double(2 * kSmallMaxMacs)) return true;
+  const int64_t tc_ctas = cdiv(M, 128) * cdiv(N, 128);
+  return 4 * tc_ctas < num_sms() && K >= 4 * std::max(M, N);
+}
+
+int num_sms() {
+  static int sms = 0;
+  if (sms > 0) return sms;
+  int dev = 0, v = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess ||
+      cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || v <= 0)
+    return 148;
+  sms = v;
+  return sms;
+}
+
+template <typename T>
+int launch_small(const T *A, int64_t lda, int a_rc, int a_cj, const T *B, int64_t ldb, int b_rc, int b_cj, T *C,
+                 int64_t ldc, int64_t M, int64_t N, int64_t K, const T *alpha, const T *beta, cudaStream_t st) {
+  qg::SmallArgs a;
+  a.A = A; a.B = B; a.C = C; a.lda = lda; a.ldb = ldb; a.ldc = ldc; a.M = M; a.N = N; a.K = K;
+  a.a_rc = a_rc; a.a_cj = a_cj; a.b_rc = b_rc; a.b_cj = b_cj;
+  double al[4], be[4];
+  for (int c = 0; c < 4; ++c) { al[c] = double(alpha[c]); be[c] = double(beta[c]); }
+  a.sc = make_scalars<double>(al, be);
+  // split K over more warps until the grid covers the SMs (keeping >= 2 k4 steps per warp)
+  const int64_t tm = cdiv(M, 8), tn = cdiv(N, 8), steps = cdiv(K, 4);
+  const int64_t sms = num_sms();
+  int S = 1;
+  while (S < 4 && cdiv(tm, 4 / S) * tn < sms && steps >= 4 * S) S *= 2;
+  a.S = S;
+  a.m_blocks = cdiv(tm, 4 / S);
+  const int64_t blocks = a.m_blocks * tn;
+  if (blocks > INT32_MAX) return int(cudaErrorInvalidConfiguration);
+  { int ti = tstart(kSmall, st);
+  qg::qgemm_small_kernel<T><<<unsigned(blocks), qg::kSmallThreads, 0, st>>>(a);
+  tstop(ti, st); }
+  ++g_last_launches;
+  return int(cudaGetLastError());
+}
+
 // Rows (r) x K panel of an operand as the pack kernel sees it (qg_pack.cuh).
 template <typename T>
 struct PackSpec {
@@ -354,6 +425,9 @@ int qgemm_impl(char transA, char transB, int64_t M, int64_t N, int64_t K, const 
   if (!reads_ab) return launch_scale(C, ldc, M, N, sc, st);
   PackSpec<T> pa{A, lda, sh.oa == 0 ? 1 : 0, sh.oa == 2 ? 1 : 0};
   PackSpec<T> pb{B, ldb, sh.ob == 0 ? 0 : 1, sh.ob == 2 ? 1 : 0};
+  if (use_small<T>(M, N, K))  // one launch, no workspace (NEXT item 4)
+    return launch_small<T>(A, lda, pa.row_contig, pa.conj, B, ldb, pb.row_contig, pb.conj, C, ldc, M, N, K,
+                           alpha, beta, st);
   return panel_loop<T>(pa, pb, M, N, K, sc, C, ldc, workspace, workspace_bytes, st, 0);
 }
 
@@ -442,6 +516,7 @@ int qherk_impl(char uplo, char trans, int64_t N, int64_t K, double alpha, const 
 template <typename T>
 size_t ws_bytes(char transA, char transB, int64_t M, int64_t N, int64_t K, bool minimum) {
   if (op_code(transA) < 0 || op_code(transB) < 0 || M <= 0 || N <= 0 || K <= 0) return 0;
+  if (use_small<T>(M, N, K)) return 0;  // the small kernel needs no workspace
   return workspace_for<T>(M, N, K, minimum ? 1 : cdiv(K, Geo<T>::kq));
 }
 
@@ -509,10 +584,15 @@ size_t qherk_workspace_bytes(char uplo, char trans, int64_t N, int64_t K) {
 
 int qgemm_last_launch_count(void) { return g_last_launches; }
 
+int qgemm_set_path_policy(int policy) {
+  if (policy < 0 || policy > 2) return -1;
+  return g_path_policy.exchange(policy);
+}
+
 void qgemm_timing_enable(int on) { g_timing.on = on != 0; }
 
-int qgemm_timing_collect(double ms[4], int counts[4]) {
-  for (int k = 0; k < 4; ++k) { ms[k] = 0.0; counts[k] = 0; }
+int qgemm_timing_collect(double ms[5], int counts[5]) {
+  for (int k = 0; k < kKinds; ++k) { ms[k] = 0.0; counts[k] = 0; }
   int rc = 0;
   for (const TimingRec &r : g_timing.recs) {
     cudaError_t e = cudaEventSynchronize(r.e1);

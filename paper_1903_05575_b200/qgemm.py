@@ -169,7 +169,17 @@ def qherk(uplo: str, trans: str, alpha: float, A: torch.Tensor, beta: float, C: 
     return C
 
 
-KINDS = ("pack", "mainloop", "scale", "naive")
+KINDS = ("pack", "mainloop", "scale", "naive", "small")
+
+PATH_AUTO, PATH_PACKED, PATH_SMALL = 0, 1, 2
+
+
+def set_path_policy(policy: int) -> int:
+    """0 auto, 1 always packed, 2 always the one-launch small kernel; returns the old one."""
+    old = int(load().qgemm_set_path_policy(int(policy)))
+    if old < 0:
+        raise ValueError(f"invalid path policy {policy}")
+    return old
 
 
 def timing_enable(on: bool = True) -> None:
@@ -179,8 +189,8 @@ def timing_enable(on: bool = True) -> None:
 
 def timing_collect() -> dict:
     """Synchronise on the recorded events; {kind: (total_ms, launches)}; clears."""
-    ms = (ctypes.c_double * 4)()
-    cnt = (ctypes.c_int * 4)()
+    ms = (ctypes.c_double * len(KINDS))()
+    cnt = (ctypes.c_int * len(KINDS))()
     rc = load().qgemm_timing_collect(ms, cnt)
     if rc != 0:
         raise QgemmError("qgemm_timing_collect", rc)

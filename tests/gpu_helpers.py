@@ -2,12 +2,24 @@
 the C-ABI path, compare with the oracle (tests only)."""
 from __future__ import annotations
 
+import contextlib
+
 import numpy as np
 import torch
 
 import oracle
 import paper_1903_05575_b200 as qg
 from tests.tolerance import tolerance
+
+
+@contextlib.contextmanager
+def path_policy(policy):
+    """Force the packed (1) or the one-launch small (2) path for the block."""
+    old = qg.set_path_policy(policy)
+    try:
+        yield
+    finally:
+        qg.set_path_policy(old)
 
 
 def to_dev(x: np.ndarray, dtype=torch.float64) -> torch.Tensor:

@@ -21,6 +21,15 @@ def lib():
     return _lib.load()
 
 
+@pytest.fixture(autouse=True)
+def packed_path(lib):
+    """The checks below are written for the packed path (workspace arguments);
+    the small-problem path is covered by test_small_path_* (policy 2 / auto)."""
+    old = lib.qgemm_set_path_policy(1)
+    yield
+    lib.qgemm_set_path_policy(old)
+
+
 def _header_symbols():
     txt = open(os.path.join(ROOT, "include", "qgemm.h")).read()
     body = txt[txt.index('extern "C" {'):]
@@ -132,3 +141,38 @@ def test_workspace_sizes(lib):
     assert lib.qgemm_workspace_min_bytes(b"N", b"N", 100, 70, 1000, 0) == 4 * 32768 + 126 * 131072 + 2048
     assert lib.qgemm_workspace_bytes(b"N", b"N", 0, 5, 5, 0) == 0
     assert lib.qgemm_workspace_bytes(b"X", b"N", 5, 5, 5, 0) == 0
+
+
+def test_path_policy_setter(lib):
+    assert lib.qgemm_set_path_policy(2) == 1
+    assert lib.qgemm_set_path_policy(7) == -1  # rejected, unchanged
+    assert lib.qgemm_set_path_policy(0) == 2
+    assert lib.qgemm_set_path_policy(1) == 0
+
+
+def test_small_path_needs_no_workspace(lib):
+    """Auto policy: below 2^24 quaternion MACs the one-launch kernel is used and
+    no workspace is requested; above it the packed path's size is returned."""
+    lib.qgemm_set_path_policy(0)
+    assert lib.qgemm_workspace_bytes(b"N", b"N", 64, 64, 64, 0) == 0
+    assert lib.qgemm_workspace_bytes(b"T", b"H", 256, 256, 256, 1) == 0
+    assert lib.qgemm_workspace_bytes(b"N", b"N", 257, 256, 256, 0) > 0
+    assert lib.qgemm_workspace_bytes(b"N", b"H", 8192, 8192, 8192, 0) > 0
+    # huge single factors must not overflow M*N*K into the small path
+    assert lib.qgemm_workspace_bytes(b"N", b"N", 1 << 40, 1 << 40, 1, 0) > 0
+    lib.qgemm_set_path_policy(2)
+    assert lib.qgemm_workspace_bytes(b"N", b"H", 8192, 8192, 8192, 0) == 0
+
+
+@pytest.mark.parametrize("kw,code", [
+    (dict(tA=b"X"), -1), (dict(tB=b"q"), -2), (dict(M=-1), -3), (dict(N=-2), -4),
+    (dict(K=-3), -5), (dict(alpha=None), -6), (dict(lda=7), -8), (dict(ldb=7), -10),
+    (dict(beta=None), -11), (dict(ldc=7), -13), (dict(tA=b"T", K=9, lda=8, ldb=9), -8),
+    (dict(A=0x100008), -7), (dict(B=0x200004), -9), (dict(C=0x300008), -12),
+    (dict(A=None), -7), (dict(B=None), -9), (dict(C=None), -12),
+    (dict(C=0x100000 + 32 * 10), -12),
+])
+def test_small_path_validates_identically(lib, kw, code):
+    lib.qgemm_set_path_policy(2)
+    assert _call(lib, ws=None, wsb=0, **kw) == code
+    assert lib.qgemm_last_launch_count() == 0

@@ -13,12 +13,19 @@ import torch
 import oracle
 import paper_1903_05575_b200 as qg
 from synth import CONFIGS, make_problem
-from tests.gpu_helpers import assert_parity, oracle_full, run_gpu, to_dev
+from tests.gpu_helpers import assert_parity, oracle_full, path_policy, run_gpu, to_dev
 
 pytestmark = pytest.mark.gpu
 OPS = [(a, b) for a in "NTH" for b in "NTH"]
 QALPHA = (0.3, -1.2, 0.7, 0.25)
 QBETA = (-0.5, 0.1, -0.9, 0.4)
+PATHS = [qg.PATH_PACKED, qg.PATH_SMALL]  # pack + persistent mainloop | one-launch small kernel
+
+
+@pytest.fixture(params=PATHS, ids=["packed", "small"])
+def path(request):
+    with path_policy(request.param):
+        yield request.param
 
 
 def _lds(opA, opB, M, N, K, pad):
@@ -28,7 +35,7 @@ def _lds(opA, opB, M, N, K, pad):
 
 
 # ---------------------------------------------------------------- config 1
-def test_c1_full():
+def test_c1_full(path):
     cfg = CONFIGS["c1"]
     pr = make_problem(cfg["M"], cfg["N"], cfg["K"], "N", "N", cfg["alpha"], cfg["beta"], seed=0,
                       c_init="nan")
@@ -52,7 +59,7 @@ SIZES = [1, 2, 3, 5, 7, 8, 17, 33, 63, 64, 65, 127, 129]
 
 @pytest.mark.parametrize("opA,opB", OPS)
 @pytest.mark.parametrize("seed", [0, 1, 2])
-def test_ragged_shapes_quaternion_scalars(opA, opB, seed):
+def test_ragged_shapes_quaternion_scalars(opA, opB, seed, path):
     rng = np.random.default_rng(100 + seed)
     for _ in range(4):
         M, N, K = (int(rng.choice(SIZES)) for _ in range(3))
@@ -63,21 +70,21 @@ def test_ragged_shapes_quaternion_scalars(opA, opB, seed):
 
 @pytest.mark.parametrize("M,N,K", [(200, 130, 300), (64, 64, 16), (65, 191, 33), (1, 300, 257)])
 @pytest.mark.parametrize("opA,opB", OPS)
-def test_exact_integer_bitwise_f64(M, N, K, opA, opB):
+def test_exact_integer_bitwise_f64(M, N, K, opA, opB, path):
     """P8: integer components in [-8, 8] -> exact in any order -> bitwise."""
     pr = make_problem(M, N, K, opA, opB, (2, -1, 0, 3), (1, 0, -2, 1), seed=3, dist="int8")
     assert_parity(pr, run_gpu(pr), oracle_full(pr), exact=True)
 
 
 @pytest.mark.parametrize("opA,opB", OPS)
-def test_exact_integer_bitwise_f32(opA, opB):
+def test_exact_integer_bitwise_f32(opA, opB, path):
     """P8 in FP32: |partial sums| <= 2^24, so FP32 is exact too."""
     pr = make_problem(150, 70, 200, opA, opB, (1, 0, 0, 0), (-1, 0, 0, 0), seed=4, dist="int8")
     assert_parity(pr, run_gpu(pr, "f32"), oracle_full(pr), exact=True)
 
 
 @pytest.mark.parametrize("opA,opB", OPS)
-def test_f32_tolerance(opA, opB):
+def test_f32_tolerance(opA, opB, path):
     """FP32 variant checked against the FP64 oracle on the FP64 inputs (R11)."""
     pr = make_problem(257, 190, 513, opA, opB, QALPHA, QBETA, seed=5, dist="normal",
                       lda=(257 if opA == "N" else 513) + 1)
@@ -92,20 +99,22 @@ def test_k_panel_loop_small_workspace(precision):
     M, N, K = 130, 100, 16 * 7 + 5
     pr = make_problem(M, N, K, "H", "T", QALPHA, QBETA, seed=6)
     dt = torch.float64 if precision == "f64" else torch.float32
-    full = qg.workspace_bytes("H", "T", M, N, K, dt)
-    mn = qg.workspace_min_bytes("H", "T", M, N, K, dt)
+    with path_policy(qg.PATH_PACKED):
+        full = qg.workspace_bytes("H", "T", M, N, K, dt)
+        mn = qg.workspace_min_bytes("H", "T", M, N, K, dt)
     kt = (K + 15) // 16
     per_ktile = (full - mn) // (kt - 1)
     small = mn + 2 * per_ktile  # room for 3 K-tiles -> panels of 3, 3, 2
     assert small < full
     ws = torch.empty(small, dtype=torch.uint8, device="cuda")
-    got = run_gpu(pr, precision, workspace=ws)
+    with path_policy(qg.PATH_PACKED):
+        got = run_gpu(pr, precision, workspace=ws)
     assert qg.last_launch_count() == 3 * 3  # 3 panels x (pack A, pack B, mainloop)
     assert_parity(pr, got, oracle_full(pr), precision=precision)
 
 
 # ---------------------------------------------------------------- degenerate cases
-def test_quick_returns_and_beta_paths():
+def test_quick_returns_and_beta_paths(path):
     # M = 0 / N = 0: nothing enqueued, C untouched
     pr = make_problem(5, 4, 3, seed=1)
     C = to_dev(pr.C)
@@ -137,7 +146,7 @@ def test_alias_rejected_and_nothing_enqueued():
     assert ei.value.code == -12
 
 
-def test_naive_cross_check_and_stream():
+def test_naive_cross_check_and_stream(path):
     """Debug kernel and tuned kernel agree on a side stream."""
     pr = make_problem(190, 77, 140, "H", "N", QALPHA, QBETA, seed=9)
     s = torch.cuda.Stream()
@@ -149,7 +158,7 @@ def test_naive_cross_check_and_stream():
     assert_parity(pr, nai, ref)
 
 
-def test_b_is_a_hermitian_rank_k_shape():
+def test_b_is_a_hermitian_rank_k_shape(path):
     """c4's structure at reduced M: C <- A A^H + C with B == A (same buffer) and a
     Hermitian C; the result is Hermitian (P12) and matches the oracle."""
     n, K = 320, 256
@@ -189,3 +198,29 @@ def test_c3_full_size_sampled_and_freivalds(precision):
     # each entry of C x sums n products of an entry error (<= tol) and |x|
     bound = tol * np.abs(x).sum() * 4
     assert np.abs(lhs - rhs).max() <= bound
+
+
+# ---------------------------------------------------------------- small-problem path
+def test_auto_policy_picks_one_launch_for_small_shapes():
+    """c1 under the default policy: one kernel, no workspace (NEXT item 4)."""
+    cfg = CONFIGS["c1"]
+    assert qg.workspace_bytes("N", "N", 64, 64, 64) == 0
+    pr = make_problem(cfg["M"], cfg["N"], cfg["K"], "N", "N", cfg["alpha"], cfg["beta"], seed=1)
+    got = run_gpu(pr)
+    assert qg.last_launch_count() == 1
+    assert_parity(pr, got, oracle_full(pr))
+    assert qg.workspace_bytes("N", "N", 1024, 1024, 1024) > 0  # c2 stays on the packed path
+
+
+@pytest.mark.parametrize("M,N,K", [(1, 1, 1), (8, 8, 4), (9, 7, 3), (40, 3, 1000), (3, 700, 9),
+                                   (256, 256, 256), (31, 257, 64), (4000, 2, 5)])
+@pytest.mark.parametrize("precision", ["f64", "f32"])
+def test_small_kernel_split_and_edges(M, N, K, precision):
+    """Every split factor S (1/2/4 warps per 8x8 tile over K), ragged M/N/K
+    tails, long-K and skinny shapes, both storage types, through the small path."""
+    pr = make_problem(M, N, K, "T", "H", QALPHA, QBETA, seed=11, dist="normal",
+                      lda=K + 1, ldb=N + 2, ldc=M + 3)
+    with path_policy(qg.PATH_SMALL):
+        got = run_gpu(pr, precision)
+        assert qg.last_launch_count() == 1
+    assert_parity(pr, got, oracle_full(pr), precision=precision)
