@@ -101,6 +101,40 @@ size_t qgemm_workspace_bytes(char transA, char transB, int64_t M, int64_t N, int
 /* Smallest accepted workspace (one K-panel), same arguments. */
 size_t qgemm_workspace_min_bytes(char transA, char transB, int64_t M, int64_t N, int64_t K, int dtype);
 
+/* End-to-end call on HOST-resident operands (the call a user with host data
+ * makes).  Same arguments, semantics, quick returns and error codes as
+ * qgemm()/qgemm_f32(), except:
+ *   A, B, C   may be host memory (pinned -- cudaHostAlloc / cudaHostRegister --
+ *             for the transfers to overlap compute; pageable memory is correct
+ *             but serialises) or device memory: every access is a
+ *             cudaMemcpy2DAsync with cudaMemcpyDefault;
+ *   workspace DEVICE memory of at least qgemm_host_workspace_bytes() bytes,
+ *             256-byte aligned; it holds the device copy of C plus
+ *             double-buffered staging and packed chunks of op(A)/op(B).
+ * The call streams K in chunks (Alg. 2's kappa loop) host->device
+ * on a private upload stream while `stream` packs and multiplies the previous
+ * chunk; the first and last chunks run per column panel of C so that C's
+ * upload and download overlap the mainloop too.  It returns
+ * after enqueueing; the result is in the caller's C once `stream` has
+ * synchronised (host buffers must stay valid until then).  The library creates
+ * two streams and a few events per call and releases them once their work
+ * completes.  A positive return (cudaError_t) can leave part of the work
+ * enqueued. */
+int qgemm_host(char transA, char transB, int64_t M, int64_t N, int64_t K,
+               const double alpha[4], const double *A, int64_t lda,
+               const double *B, int64_t ldb, const double beta[4],
+               double *C, int64_t ldc,
+               void *workspace, size_t workspace_bytes, void *stream);
+int qgemm_host_f32(char transA, char transB, int64_t M, int64_t N, int64_t K,
+                   const float alpha[4], const float *A, int64_t lda,
+                   const float *B, int64_t ldb, const float beta[4],
+                   float *C, int64_t ldc,
+                   void *workspace, size_t workspace_bytes, void *stream);
+
+/* Device workspace bytes of qgemm_host (dtype 0) / qgemm_host_f32 (dtype 1);
+ * 0 for invalid op characters or M, N <= 0. */
+size_t qgemm_host_workspace_bytes(char transA, char transB, int64_t M, int64_t N, int64_t K, int dtype);
+
 /* Quaternion Hermitian rank-K update (the paper
  * names rank-k updates as a reuse target of its GEMM kernels, and
  * defines quaternion hermiticity Q = Q^H at P:483-492):

@@ -8,9 +8,11 @@ the thin Python binding plus the multi-GPU row-block driver.
 from ._lib import EXPORTS, QgemmError, SO_PATH, load  # noqa: F401
 from .qgemm import (  # noqa: F401
     get_workspace,
+    host_workspace_bytes,
     last_launch_count,
     qgemm,
     qgemm_f32,
+    qgemm_host,
     qgemm_naive,
     qherk,
     set_path_policy,

@@ -14,7 +14,7 @@ SO_PATH = os.path.join(PKG, "libqgemm.so")
 #: every symbol include/qgemm.h declares
 EXPORTS = ("qgemm", "qgemm_f32", "qgemm_workspace_bytes", "qgemm_workspace_min_bytes",
            "qgemm_naive", "qherk", "qherk_workspace_bytes", "qgemm_last_launch_count",
-           "qgemm_set_path_policy",
+           "qgemm_set_path_policy", "qgemm_host", "qgemm_host_f32", "qgemm_host_workspace_bytes",
            "qgemm_timing_enable", "qgemm_timing_collect", "qgemm_version")
 
 _lib = None
@@ -52,6 +52,12 @@ def load():
     lib.qgemm.restype = ctypes.c_int
     lib.qgemm_f32.argtypes = common + [vp, sz, vp]
     lib.qgemm_f32.restype = ctypes.c_int
+    lib.qgemm_host.argtypes = common + [vp, sz, vp]
+    lib.qgemm_host.restype = ctypes.c_int
+    lib.qgemm_host_f32.argtypes = common + [vp, sz, vp]
+    lib.qgemm_host_f32.restype = ctypes.c_int
+    lib.qgemm_host_workspace_bytes.argtypes = [c, c, i64, i64, i64, ctypes.c_int]
+    lib.qgemm_host_workspace_bytes.restype = sz
     lib.qgemm_naive.argtypes = common + [vp]
     lib.qgemm_naive.restype = ctypes.c_int
     lib.qgemm_workspace_bytes.argtypes = [c, c, i64, i64, i64, ctypes.c_int]

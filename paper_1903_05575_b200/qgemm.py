@@ -121,6 +121,49 @@ def _qgemm_typed(fn, name, dtype, transA, transB, alpha, A, B, beta, C, M, N, K,
                  st)
 
 
+def host_workspace_bytes(transA: str, transB: str, M: int, N: int, K: int,
+                         dtype=torch.float64) -> int:
+    return int(load().qgemm_host_workspace_bytes(transA.encode(), transB.encode(), M, N, K,
+                                                 0 if dtype == torch.float64 else 1))
+
+
+def qgemm_host(transA: str, transB: str, alpha, A: torch.Tensor, B: torch.Tensor, beta,
+               C: torch.Tensor, M: int | None = None, N: int | None = None, K: int | None = None,
+               workspace: torch.Tensor | None = None, device=None,
+               stream: torch.cuda.Stream | None = None):
+    """End-to-end QGEMM on HOST tensors (include/qgemm.h qgemm_host[_f32]): the
+    library streams A/B/C through device staging (pin them for overlap) and
+    writes the result back into the host C.  Asynchronous on `stream`; C is
+    valid after the stream synchronises.  float64 -> qgemm_host, float32 ->
+    qgemm_host_f32."""
+    dtype = C.dtype
+    if dtype not in (torch.float64, torch.float32):
+        raise TypeError(f"C: expected float64/float32, got {dtype}")
+    for t, nm in ((A, "A"), (B, "B"), (C, "C")):
+        if t is None:
+            continue
+        if t.dtype != dtype:
+            raise TypeError(f"{nm}: expected {dtype}, got {t.dtype}")
+        if t.dim() != 3 or t.shape[2] != 4 or not t.is_contiguous():
+            raise ValueError(f"{nm}: expected a contiguous (ncols, ld, 4) tensor")
+    m0, n0, k0 = infer_dims(transA, transB, A, B, C)
+    M = m0 if M is None else M
+    N = n0 if N is None else N
+    K = k0 if K is None else K
+    dev = torch.device(device) if device is not None else torch.device("cuda",
+                                                                       torch.cuda.current_device())
+    st = (stream or torch.cuda.current_stream(dev)).cuda_stream
+    need = host_workspace_bytes(transA, transB, M, N, K, dtype)
+    if workspace is None:
+        workspace = get_workspace(need, dev) if need else None
+    elif not workspace.is_cuda:
+        raise TypeError("workspace: must be device memory")
+    nbytes = workspace.numel() * workspace.element_size() if workspace is not None else 0
+    fn = load().qgemm_host if dtype == torch.float64 else load().qgemm_host_f32
+    return _call(fn, "qgemm_host", transA, transB, M, N, K, alpha, A, B, beta, C, dtype, workspace,
+                 nbytes, st)
+
+
 def qgemm_naive(transA: str, transB: str, alpha, A: torch.Tensor, B: torch.Tensor, beta,
                 C: torch.Tensor, M: int | None = None, N: int | None = None, K: int | None = None,
                 stream: torch.cuda.Stream | None = None):

@@ -1,0 +1,95 @@
+"""qgemm_host / qgemm_host_f32 (host-resident operands streamed through device
+staging, include/qgemm.h) vs the CPU oracle, element by element (-m gpu).
+
+Shapes are chosen so the K-chunk loop has several chunks (Q > 2: staging
+double buffer reused) and C several column panels (P > 1), with ragged tails
+and ld padding (NaN in A/B padding, sentinel in C padding must survive)."""
+from __future__ import annotations
+
+import numpy as np
+import pytest
+import torch
+
+import paper_1903_05575_b200 as qg
+from synth import make_problem
+from tests.gpu_helpers import assert_parity, oracle_full, path_policy
+
+pytestmark = pytest.mark.gpu
+OPS = [(a, b) for a in "NTH" for b in "NTH"]
+QALPHA = (0.3, -1.2, 0.7, 0.25)
+QBETA = (-0.5, 0.1, -0.9, 0.4)
+
+
+def run_host(pr, precision="f64", pin=True, stream=None, workspace=None):
+    dt = torch.float64 if precision == "f64" else torch.float32
+
+    def host(x):
+        t = torch.from_numpy(np.array(x, copy=True)).to(dt)  # never alias the problem's arrays
+        return t.pin_memory() if pin else t
+
+    A = host(pr.A)
+    B = A if pr.B is pr.A else host(pr.B)
+    C = host(pr.C)
+    qg.qgemm_host(pr.transA, pr.transB, pr.alpha, A, B, pr.beta, C, M=pr.M, N=pr.N, K=pr.K,
+                  stream=stream, workspace=workspace)
+    (stream or torch.cuda.current_stream()).synchronize()
+    return C.double().numpy()
+
+
+@pytest.mark.parametrize("opA,opB", OPS)
+def test_host_chunked_all_ops(opA, opB):
+    M, N, K = 300, 520, 700  # K chunks 256/256/188, C panels 256/256/8
+    lda = (M if opA == "N" else K) + 3
+    ldb = (K if opB == "N" else N) + 1
+    pr = make_problem(M, N, K, opA, opB, QALPHA, QBETA, seed=21, lda=lda, ldb=ldb, ldc=M + 2)
+    assert_parity(pr, run_host(pr), oracle_full(pr))
+    assert qg.last_launch_count() == 3 * 2 + 3 + 1 + 3  # packs, panels of chunk 0, chunk 1, last
+
+
+@pytest.mark.parametrize("opA,opB", [("N", "H"), ("T", "N"), ("H", "T")])
+def test_host_f32_chunked(opA, opB):
+    pr = make_problem(260, 700, 900, opA, opB, QALPHA, QBETA, seed=22, dist="normal")
+    assert_parity(pr, run_host(pr, "f32"), oracle_full(pr), precision="f32")
+
+
+def test_host_beta_zero_nan_c_and_single_chunk():
+    """beta = 0: C is never uploaded (NaN host C), K fits one chunk (first == last)."""
+    pr = make_problem(400, 300, 200, "N", "H", QALPHA, 0, seed=23, c_init="nan")
+    got = run_host(pr)
+    assert np.isfinite(got[:, :400]).all()
+    assert_parity(pr, got, oracle_full(pr))
+
+
+def test_host_small_path_and_quick_paths():
+    pr = make_problem(64, 64, 64, "N", "N", 1, 0, seed=24)
+    assert_parity(pr, run_host(pr), oracle_full(pr))
+    assert qg.last_launch_count() == 1  # one-launch small kernel
+    with path_policy(qg.PATH_SMALL):
+        pr = make_problem(300, 200, 500, "H", "T", QALPHA, QBETA, seed=25, lda=503)
+        assert_parity(pr, run_host(pr, pin=False), oracle_full(pr))  # pageable host memory
+    # alpha = 0: C <- beta C on the device, no A/B traffic
+    pr = make_problem(70, 50, 30, "N", "N", 0, QBETA, seed=26)
+    assert_parity(pr, run_host(pr), oracle_full(pr))
+    # K = 0
+    pr = make_problem(70, 50, 0, "N", "N", 1, QBETA, seed=26)
+    assert_parity(pr, run_host(pr), oracle_full(pr))
+
+
+def test_host_side_stream_and_workspace_errors():
+    pr = make_problem(200, 300, 600, "T", "H", QALPHA, QBETA, seed=27)
+    need = qg.host_workspace_bytes("T", "H", 200, 300, 600)
+    ws = torch.empty(need, dtype=torch.uint8, device="cuda")
+    s = torch.cuda.Stream()
+    assert_parity(pr, run_host(pr, stream=s, workspace=ws), oracle_full(pr))
+    with pytest.raises(qg.QgemmError) as ei:
+        run_host(pr, workspace=ws[: need - 256])
+    assert ei.value.code == -15
+
+
+def test_host_repeated_calls_agree_with_device_path():
+    """Back-to-back calls reuse one workspace (stream-ordered), and the host
+    path equals the device path bitwise in exact-integer mode (P8)."""
+    pr = make_problem(330, 610, 650, "N", "N", (2, -1, 0, 3), (1, 0, -2, 1), seed=28, dist="int8")
+    ref = oracle_full(pr)
+    for _ in range(3):
+        assert_parity(pr, run_host(pr), ref, exact=True)
