@@ -35,8 +35,10 @@ METRIC = "QGEMM FP64 TFLOP/s (32 flops/quat-MAC) and % of FP64 peak at 1/2/4/8 G
 FP64_DMMA_PEAK_TFLOPS = 37.0
 FP64_NOMINAL_TFLOPS = 148 * 64 * 2 * 1.965e9 / 1e12  # 37.22
 FP32_NOMINAL_TFLOPS = 148 * 128 * 2 * 1.965e9 / 1e12  # 74.4 (FFMA pipe)
-# tf32 dense tensor peak: measured bf16 (MEASURED_PEAKS.json) x nominal tf32/bf16 (1.1/2.25)
-TF32_PEAK_TFLOPS = 1646.9 * 1.1 / 2.25
+# tcgen05.mma kind::tf32 peak MEASURED on this pool's B200 with the MMA loop of
+# tools/microbench/tf32_peak.cu (M=128 N=256 K=8, smem-resident operands, ~1.8 s
+# back to back: 1117 TFLOP/s; profiles/r01_tf32_peak.txt) -- the nominal 1.1 PF
+TF32_PEAK_TFLOPS = 1117.0
 
 
 def parse():
@@ -223,9 +225,9 @@ def make_roofline(precision, achieved, main_ms, step_ms, pack_ms, steps):
             "achieved_algorithmic": achieved,
             "frac_algorithmic": (achieved / TF32_PEAK_TFLOPS) if achieved else None,
             "traffic": _traffic("f32_mainloop_bytes_per_launch"),
-            "peak_source": "MEASURED_PEAKS.json bf16_tflops 1646.9 x nominal tf32/bf16 ratio "
-                           "(1.1/2.25, B200_PROFILING.md); achieved counts the 3 tf32 MMAs per "
-                           "real product of 3xTF32",
+            "peak_source": "measured tcgen05.mma kind::tf32 loop on this pool's B200, "
+                           "tools/microbench/tf32_peak.cu (profiles/r01_tf32_peak.txt); achieved "
+                           "counts the 3 tf32 MMAs per real product of 3xTF32",
             "kernel_share_of_step": main_ms / step_ms if step_ms else None,
             "pack_ms_per_step": pack_ms / max(1, steps)}
 
@@ -240,6 +242,8 @@ def measure_f32_variant(A, B, C, n, warmup, steps):
     for _ in range(max(1, warmup)):
         qg.qgemm_f32("N", "H", 1.0, A32, B32, 1.0, C32, workspace=ws)
     torch.cuda.synchronize()
+    sampler = ClockSampler(A.device.index or 0)
+    sampler.start()
     qg.timing_enable(True)
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record()
@@ -250,6 +254,7 @@ def measure_f32_variant(A, B, C, n, warmup, steps):
     ms = e0.elapsed_time(e1)
     kt = qg.timing_collect()
     qg.timing_enable(False)
+    clocks = sampler.stop()
     fl = 32.0 * n ** 3
     main_ms, main_cnt = kt["mainloop"]
     achieved = fl / (main_ms / max(1, main_cnt) / 1e3) / 1e12 if main_cnt else None
@@ -259,7 +264,7 @@ def measure_f32_variant(A, B, C, n, warmup, steps):
                         "rounded to FP32)", "dtype": "f32 (3xTF32 on tcgen05, FP32 accumulate)",
             "value": fl * steps / (ms / 1e3) / 1e12, "unit": "TFLOP/s", "ms_per_step": ms / steps,
             "steps": steps, "roofline": make_roofline("f32", achieved, main_ms, ms, kt["pack"][0],
-                                                      steps)}
+                                                      steps), "clocks": clocks}
 
 
 # ------------------------------------------------------------------ our arm

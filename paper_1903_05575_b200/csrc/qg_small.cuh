@@ -78,7 +78,8 @@ __device__ __forceinline__ void small_step(double (&acc)[4][2], const double (&q
 }
 
 template <typename T>
-__global__ void __launch_bounds__(kSmallThreads) qgemm_small_kernel(SmallArgs a) {
+// (<= 128 registers: 4 CTAs per SM -- occupancy, not ILP, sets its speed; measured)
+__global__ void __launch_bounds__(kSmallThreads, 4) qgemm_small_kernel(SmallArgs a) {
   __shared__ double red[kSmallThreads / 32][32][8];
   const T *A = static_cast<const T *>(a.A);
   const T *B = static_cast<const T *>(a.B);
@@ -95,6 +96,16 @@ __global__ void __launch_bounds__(kSmallThreads) qgemm_small_kernel(SmallArgs a)
   const int64_t steps = (a.K + 3) / 4;
   const int64_t per = (steps + S - 1) / S;
   const int64_t s0 = min(steps, int64_t(part) * per), s1 = min(steps, s0 + per);
+
+  // C is independent of the k loop: the epilogue warps prefetch their two
+  // quaternions into L1 first, so the C read latency overlaps the mainloop
+  // (a prefetch, not a load: no registers held across the loop)
+  if (part == 0 && !a.sc.beta_zero && m0 + lr < a.M) {
+#pragma unroll
+    for (int i = 0; i < 2; ++i)
+      if (n0 + 2 * lk + i < a.N)
+        asm volatile("prefetch.global.L1 [%0];" ::"l"(C + 4 * (m0 + lr + (n0 + 2 * lk + i) * a.ldc)));
+  }
 
   double acc[4][2];
 #pragma unroll

@@ -340,8 +340,8 @@ std::atomic<int> g_path_policy{0};
 //  * FP32: up to 2^25 (the tcgen05 path has a 128x128 tile and no split-K), and
 //    up to 2^28 when that path would launch fewer than 1/4 as many CTAs as
 //    there are SMs and K >= 4 max(M, N) (small M x N, long K);
-//  * never when K < 16 and M*N >= 2^20: there the call is C-traffic bound and
-//    the packed epilogue streams C better.
+//    but not for K <= 16 with M*N >= 2^20: there the FP32 call is C-traffic
+//    bound and the packed tcgen05 epilogue streams C better.
 constexpr int64_t kSmallMaxMacs = int64_t(1) << 24;
 
 int num_sms();
@@ -355,8 +355,8 @@ bool use_small(int64_t M, int64_t N, int64_t K) {
   if (M > kCap || N > kCap || K > kCap) return false;  // keeps M*N*K from overflowing below
   const double macs = double(M) * double(N) * double(K);
   if (macs > double(kCap)) return false;
-  if (K < 16 && double(M) * double(N) >= double(1 << 20)) return false;
   if (sizeof(T) == 8) return macs <= double(kSmallMaxMacs);
+  if (K <= 16 && double(M) * double(N) >= double(1 << 20)) return false;
   if (macs <= double(2 * kSmallMaxMacs)) return true;
   const int64_t tc_ctas = cdiv(M, 128) * cdiv(N, 128);
   return 4 * tc_ctas < num_sms() && K >= 4 * std::max(M, N);

@@ -18,7 +18,7 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import paper_1903_05575_b200 as qg  # noqa: E402
 
 ap = argparse.ArgumentParser()
-ap.add_argument("--sizes", default="256,512,1024,2048,3072,4096,6144,8192")
+ap.add_argument("--sizes", default="64,128,256,384,512,768,1024,2048,3072,4096,6144,8192")
 ap.add_argument("--reps", type=int, default=5)
 a = ap.parse_args()
 dev = torch.device("cuda")
@@ -26,17 +26,34 @@ g = torch.Generator(device="cuda").manual_seed(0)
 
 
 def timeit(fn, reps):
-    for _ in range(2):
+    """Device time per call: the call is captured once in a CUDA graph and
+    replayed (host-side Python/ctypes/dispatch cost is off the timeline for all
+    three arms alike); best of `reps` batches of replays, CUDA events."""
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(s):
         fn()
+        gr = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(gr, stream=s):
+            fn()
+    torch.cuda.current_stream().wait_stream(s)
     torch.cuda.synchronize()
+    gr.replay()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    gr.replay()
+    e1.record()
+    torch.cuda.synchronize()
+    nrep = max(1, min(200, int(50.0 / max(e0.elapsed_time(e1), 1e-3))))  # ~50 ms per batch
     best = 1e30
     for _ in range(reps):
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
-        fn()
+        for _ in range(nrep):
+            gr.replay()
         e1.record()
         torch.cuda.synchronize()
-        best = min(best, e0.elapsed_time(e1))
+        best = min(best, e0.elapsed_time(e1) / nrep)
     return best
 
 
@@ -44,7 +61,8 @@ for n in [int(s) for s in a.sizes.split(",")]:
     A = 2 * torch.rand((n, n, 4), dtype=torch.float64, device=dev, generator=g) - 1
     B = 2 * torch.rand((n, n, 4), dtype=torch.float64, device=dev, generator=g) - 1
     C = torch.empty((n, n, 4), dtype=torch.float64, device=dev)
-    t_q = timeit(lambda: qg.qgemm("N", "N", 1.0, A, B, 0.0, C), a.reps)
+    ws = qg.get_workspace(max(256, qg.workspace_bytes("N", "N", n, n, n)), dev)
+    t_q = timeit(lambda: qg.qgemm("N", "N", 1.0, A, B, 0.0, C, workspace=ws), a.reps)
     del A, B, C
     Z1 = torch.randn((2 * n, 2 * n), dtype=torch.complex128, device=dev, generator=g)
     Z2 = torch.randn((2 * n, 2 * n), dtype=torch.complex128, device=dev, generator=g)
