@@ -48,9 +48,16 @@ def parse():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--precision", choices=["f64", "f32"], default="f64")
-    ap.add_argument("--n", type=int, default=8192, help="M_loc = N = K (default: c3)")
+    ap.add_argument("--size", "--n", dest="n", type=int, default=8192,
+                    help="M_loc = N = K (default: c3)")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--debug-one-device", action="store_true",
+                    help="all ranks on cuda:0 with gloo: functional check of the multi-rank "
+                         "paths on a 1-GPU box; its numbers are not a measurement")
+    ap.add_argument("--collect", choices=["p2p", "nccl"], default="p2p",
+                    help="N>1: C row blocks stored into root's C by the epilogue over peer "
+                         "memory (p2p, fused) or gathered with NCCL send/recv after compute")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-f32", action="store_true", help="skip the FP32 (tcgen05) variant")
     return ap.parse_args()
@@ -273,15 +280,20 @@ def run_ours(args):
     import torch.distributed as dist
 
     import paper_1903_05575_b200 as qg
-    from paper_1903_05575_b200.dist import qgemm_rowsharded
+    from paper_1903_05575_b200.dist import PeerC, qgemm_rowsharded, qgemm_rowsharded_p2p
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.debug_one_device:
+        local = 0  # functional check of the N>1 code paths on a 1-GPU box (no timing claim)
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if args.debug_one_device:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=dev)
     n = args.n
     M_total = n * world
     dt = torch.float64 if args.precision == "f64" else torch.float32
@@ -292,6 +304,15 @@ def run_ours(args):
     B = torch.from_numpy(B_h).to(dev)
     C = torch.from_numpy(C_h).to(dev)
     C_full = torch.empty((n, M_total, 4), dtype=dt, device=dev) if (world > 1 and rank == 0) else None
+    peer = None
+    if world > 1 and args.collect == "p2p":
+        # C lives on root: every row block starts as root's C draw (synthetic;
+        # same flops and bytes as distinct draws); each rank's epilogue stores
+        # into it over peer memory (dist.qgemm_rowsharded_p2p)
+        if rank == 0:
+            for r in range(world):
+                C_full[:, r * n:(r + 1) * n, :].copy_(C)
+        peer = PeerC(C_full)
     ws = qg.get_workspace(qg.workspace_bytes("N", "H", n, n, n, dt), dev)
     stream = torch.cuda.current_stream(dev)
 
@@ -299,13 +320,19 @@ def run_ours(args):
         if world == 1:
             fn("N", "H", 1.0, A, B, 1.0, C, workspace=ws)
             return qg.last_launch_count()
+        if peer is not None:
+            qgemm_rowsharded_p2p("N", "H", 1.0, A, B, 1.0, peer, M_total, n, n, workspace=ws)
+            return qg.last_launch_count()
         qgemm_rowsharded("N", "H", 1.0, A, B, 1.0, C, M_total, n, n, C_full=C_full,
                          local_gemm=lambda *a, **k: fn(*a, workspace=ws, **k))
         return qg.last_launch_count()
 
     def barrier():
         if world > 1:
-            dist.barrier(device_ids=[local])
+            if args.debug_one_device:
+                dist.barrier()
+            else:
+                dist.barrier(device_ids=[local])
         torch.cuda.synchronize(dev)
 
     for _ in range(args.warmup):
@@ -363,7 +390,11 @@ def run_ours(args):
             A.copy_(pinA, non_blocking=True)
             if rank == 0:
                 B.copy_(pinB, non_blocking=True)
-            C.copy_(pinC, non_blocking=True)
+            if peer is None:
+                C.copy_(pinC, non_blocking=True)
+            elif rank == 0:
+                for r in range(world):  # C lives on root: upload every row block
+                    C_full[:, r * n:(r + 1) * n, :].copy_(pinC, non_blocking=True)
             step()
             src = C_full if C_full is not None else C
             if rank == 0:
@@ -384,14 +415,15 @@ def run_ours(args):
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             ems = float(t.item())
         el = A.element_size()
-        h2d = (A.numel() + C.numel()) * el * world + B.numel() * el
+        h2d = (A.numel() + C.numel()) * el * world + B.numel() * el  # same bytes either way
         d2h = (C_full.numel() if C_full is not None else C.numel()) * el
         e2e = {"value": flops_step * e_steps / (ems / 1e3) / 1e12, "unit": "TFLOP/s",
                "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
                "steps": e_steps, "ms_per_step": ems / e_steps,
                "path": ("pinned host -> qgemm_host C ABI (K-chunked H2D / column-panel D2H "
                         "overlapped with the mainloop) -> pinned host") if world == 1 else
-                       "pinned host -> qgemm_rowsharded (NCCL) -> pinned host"}
+                       f"pinned host -> qgemm_rowsharded{'_p2p' if peer is not None else ''} -> "
+                       "pinned host"}
 
     variants = None
     if world == 1 and args.precision == "f64" and not args.no_f32:
@@ -413,15 +445,24 @@ def run_ours(args):
                 "config": {"workload": f"c3: QGEMM M={M_total} (={world}x{n}) N=K={n} opA=N opB=H "
                                        "alpha=beta=1 N(0,1) components, column-major interleaved",
                            "global_batch": 1, "seq_len": None,
-                           "parallelism": f"rowblock{world}" + ("+bcastB+gatherC" if world > 1 else ""),
+                           "parallelism": f"rowblock{world}" + (
+                               ("+bcastB+p2p-epilogue-into-root-C" if peer is not None
+                                else "+bcastB+gatherC") if world > 1 else ""),
                            "l2": "inputs (2.15 GB/matrix) >> 126 MB L2; no flush",
                            "timed": "pack A + pack B + DMMA mainloop/epilogue per step"
-                                    + (" + NCCL broadcast(B) + gather(C)" if world > 1 else "")},
+                                    + ((" + NCCL broadcast(B) + epilogue stores into root's C "
+                                        "over NVLink + completion all_reduce" if peer is not None
+                                        else " + NCCL broadcast(B) + gather(C)")
+                                       if world > 1 else "")},
                 "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "variants": variants,
                 "gpu_launches": launches, "clocks": clocks,
                 "library": qg.version()}
         print(json.dumps(line), flush=True)
     if world > 1:
+        if peer is not None:  # root's C must outlive the peers' mappings
+            dist.barrier()
+            peer.close()
+            dist.barrier()
         dist.destroy_process_group()
     return 0
 

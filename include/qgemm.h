@@ -156,6 +156,26 @@ int qherk(char uplo, char trans, int64_t N, int64_t K, double alpha, const doubl
 /* Workspace bytes for a single-panel qherk call (0 for invalid/quick-return shapes). */
 size_t qherk_workspace_bytes(char uplo, char trans, int64_t N, int64_t K);
 
+/* Peer memory (multi-GPU driver).  The
+ * row-sharded QGEMM fuses its collection step into the epilogue: each rank
+ * passes root's C, mapped into its own address space, as the `C` argument of
+ * qgemm() (row offset r0, ldc = root's leading dimension), so finished tiles
+ * are stored over NVLink / NVSwitch while the rest of the mainloop runs.
+ *
+ * qgemm_ipc_handle: CUDA IPC handle (64 bytes, written to `handle`) of the
+ *   device allocation containing `dptr`, and the byte offset of `dptr` inside
+ *   it (*offset; *alloc_bytes = allocation size if non-NULL).  Works for
+ *   interior pointers of caching allocators.  Returns 0, -1 (dptr NULL),
+ *   -2 (handle NULL), -3 (offset NULL), or a cudaError_t.
+ * qgemm_ipc_open: map a handle from another process of this node into this
+ *   process (cudaIpcMemLazyEnablePeerAccess); *dptr = mapped base + offset,
+ *   *base = the mapping to pass to qgemm_ipc_close.  Returns 0, -1/-3/-4 for
+ *   NULL arguments, or a cudaError_t (e.g. opening in the exporting process).
+ * qgemm_ipc_close: unmap a base returned by qgemm_ipc_open. */
+int qgemm_ipc_handle(const void *dptr, unsigned char handle[64], uint64_t *offset, uint64_t *alloc_bytes);
+int qgemm_ipc_open(const unsigned char handle[64], uint64_t offset, void **dptr, void **base);
+int qgemm_ipc_close(void *base);
+
 /* Debug/cross-check path: one thread per output quaternion, reads op(A) and
  * op(B) in place (no pack, no workspace).  Same arguments, errors and
  * semantics as qgemm() minus the workspace.  Not used by qgemm(). */

@@ -13,6 +13,10 @@ from .qgemm import (  # noqa: F401
     qgemm,
     qgemm_f32,
     qgemm_host,
+    qgemm_ptr,
+    ipc_handle,
+    ipc_open,
+    ipc_close,
     qgemm_naive,
     qherk,
     set_path_policy,

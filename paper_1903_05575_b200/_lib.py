@@ -15,6 +15,7 @@ SO_PATH = os.path.join(PKG, "libqgemm.so")
 EXPORTS = ("qgemm", "qgemm_f32", "qgemm_workspace_bytes", "qgemm_workspace_min_bytes",
            "qgemm_naive", "qherk", "qherk_workspace_bytes", "qgemm_last_launch_count",
            "qgemm_set_path_policy", "qgemm_host", "qgemm_host_f32", "qgemm_host_workspace_bytes",
+           "qgemm_ipc_handle", "qgemm_ipc_open", "qgemm_ipc_close",
            "qgemm_timing_enable", "qgemm_timing_collect", "qgemm_version")
 
 _lib = None
@@ -58,6 +59,14 @@ def load():
     lib.qgemm_host_f32.restype = ctypes.c_int
     lib.qgemm_host_workspace_bytes.argtypes = [c, c, i64, i64, i64, ctypes.c_int]
     lib.qgemm_host_workspace_bytes.restype = sz
+    u64p = ctypes.POINTER(ctypes.c_uint64)
+    lib.qgemm_ipc_handle.argtypes = [vp, ctypes.c_char_p, u64p, u64p]
+    lib.qgemm_ipc_handle.restype = ctypes.c_int
+    lib.qgemm_ipc_open.argtypes = [ctypes.c_char_p, ctypes.c_uint64, ctypes.POINTER(vp),
+                                   ctypes.POINTER(vp)]
+    lib.qgemm_ipc_open.restype = ctypes.c_int
+    lib.qgemm_ipc_close.argtypes = [vp]
+    lib.qgemm_ipc_close.restype = ctypes.c_int
     lib.qgemm_naive.argtypes = common + [vp]
     lib.qgemm_naive.restype = ctypes.c_int
     lib.qgemm_workspace_bytes.argtypes = [c, c, i64, i64, i64, ctypes.c_int]

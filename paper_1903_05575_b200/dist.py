@@ -11,6 +11,15 @@ a process group (one process per GPU, NCCL over NVLink 5 / NVSwitch):
     `root`, which copies it into the row block of the column-major full C
     (ldc = M): the relayout of a strided row block.
 
+Fused collection (qgemm_rowsharded_p2p, the default of bench.py at N > 1): C
+lives on root only.  Root's C allocation is mapped into every rank once
+(PeerC: CUDA IPC handle + offset, include/qgemm.h "Peer memory"), and each
+rank's qgemm writes its finished tiles straight into root's C over NVLink /
+NVSwitch (C argument = root's C + r0 rows, ldc = root's leading dimension):
+the collection overlaps the mainloop tile by tile and neither a gather nor a
+relayout pass exists.  A one-element all_reduce after the local QGEMM is the
+completion barrier (stream-ordered, so root's later work sees every row block).
+
 Row split: rows_for_rank() -- contiguous blocks, sizes differ by at most one
 64-row tile so every rank's mainloop tiles are full except the global tail.
 The local GEMM is libqgemm.so's qgemm (no CPU path); tests on CPU/gloo inject
@@ -88,3 +97,82 @@ def qgemm_rowsharded(transA: str, transB: str, alpha, A_local: torch.Tensor, B: 
         for w in dist.batch_isend_irecv([dist.P2POp(dist.isend, send, root, group)]):
             w.wait()
     return C_local
+
+
+class PeerC:
+    """Root's column-major C (N columns, leading dimension ldc >= M) mapped into
+    the address space of every rank of `group` (created once, reused per step).
+
+    Root passes its C tensor; the other ranks pass None.  `share`/`open_` map a
+    tensor to a picklable token and back to an address; the defaults are the
+    library's CUDA IPC calls (qgemm_ipc_handle / qgemm_ipc_open), the CPU tests
+    inject shared-memory files."""
+
+    def __init__(self, C_full: torch.Tensor | None, group=None, root: int = 0,
+                 share: Callable | None = None, open_: Callable | None = None,
+                 close: Callable | None = None):
+        from .qgemm import ipc_close, ipc_handle, ipc_open
+        self.group, self.root = group, root
+        rank = dist.get_rank(group)
+        share = share or (lambda t: ipc_handle(t)[:2])
+        open_ = open_ or ipc_open
+        self._close = close or ipc_close
+        info = [None]
+        if rank == root:
+            assert C_full is not None and C_full.dim() == 3 and C_full.shape[2] == 4
+            assert C_full.is_contiguous()
+            info[0] = (share(C_full), int(C_full.shape[0]), int(C_full.shape[1]),
+                       str(C_full.dtype), C_full.element_size())
+        dist.broadcast_object_list(info, src=root, group=group)
+        token, self.ncols, self.ldc, self.dtype_name, self.elsize = info[0]
+        if rank == root:
+            self.addr, self.base, self.tensor = C_full.data_ptr(), None, C_full
+        else:
+            self.addr, self.base = open_(*token) if isinstance(token, tuple) else open_(token)
+            self.tensor = None
+
+    def row_addr(self, r0: int) -> int:
+        """Address of C(r0, 0) (column-major, 4 scalars per quaternion)."""
+        return self.addr + 4 * self.elsize * r0
+
+    def close(self):
+        if self.base is not None:
+            self._close(self.base)
+            self.base = None
+
+
+def qgemm_rowsharded_p2p(transA: str, transB: str, alpha, A_local: torch.Tensor, B: torch.Tensor,
+                         beta, peer: PeerC, M: int, N: int, K: int, group=None, root: int = 0,
+                         broadcast_b: bool = True, workspace: torch.Tensor | None = None,
+                         local_gemm_ptr: Callable | None = None, barrier: bool = True):
+    """Sharded QGEMM step with the collection fused into the epilogue:
+    broadcast B (NCCL) -> local QGEMM whose epilogue stores into root's C over
+    peer memory -> completion all_reduce.  A_local as qgemm_rowsharded; root's
+    C (PeerC) is read (beta != 0) and written in place; returns None."""
+    world = dist.get_world_size(group)
+    rank = dist.get_rank(group)
+    r0, r1 = rows_for_rank(M, world, rank)
+    m_loc = r1 - r0
+    assert peer.ncols == N and peer.ldc >= M
+    if broadcast_b:
+        dist.broadcast(B, src=root, group=group)
+    if m_loc > 0:
+        lda = A_local.shape[1]
+        if local_gemm_ptr is None:
+            from .qgemm import get_workspace, qgemm_ptr, workspace_bytes
+            dt = A_local.dtype
+            need = workspace_bytes(transA, transB, m_loc, N, K, dt)
+            ws = workspace
+            if ws is None or ws.numel() * ws.element_size() < need:
+                ws = get_workspace(need, A_local.device) if need else None
+            st = torch.cuda.current_stream(A_local.device).cuda_stream
+            qgemm_ptr(transA, transB, m_loc, N, K, alpha, A_local.data_ptr(), lda, B.data_ptr(),
+                      B.shape[1], beta, peer.row_addr(r0), peer.ldc,
+                      ws.data_ptr() if ws is not None else 0,
+                      ws.numel() * ws.element_size() if ws is not None else 0, st, dtype=dt)
+        else:
+            local_gemm_ptr(transA, transB, m_loc, N, K, alpha, A_local, lda, B, B.shape[1], beta,
+                           peer.row_addr(r0), peer.ldc)
+    if barrier:
+        flag = torch.zeros(1, dtype=torch.float32, device=A_local.device)
+        dist.all_reduce(flag, group=group)

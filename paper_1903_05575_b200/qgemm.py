@@ -164,6 +164,51 @@ def qgemm_host(transA: str, transB: str, alpha, A: torch.Tensor, B: torch.Tensor
                  nbytes, st)
 
 
+def qgemm_ptr(transA: str, transB: str, M: int, N: int, K: int, alpha, A: int, lda: int, B: int,
+              ldb: int, beta, C: int, ldc: int, workspace: int, workspace_bytes: int, stream: int,
+              dtype=torch.float64):
+    """qgemm / qgemm_f32 on raw device addresses (ints): for operands that are not
+    torch tensors of this process, e.g. root's C mapped with ipc_open()."""
+    lib = load()
+    fn = lib.qgemm if dtype == torch.float64 else lib.qgemm_f32
+    al, be = _q4(alpha, dtype), _q4(beta, dtype)
+    vp = ctypes.c_void_p
+    rc = fn(transA.encode(), transB.encode(), M, N, K, ctypes.cast(al, vp), vp(A or None), lda,
+            vp(B or None), ldb, ctypes.cast(be, vp), vp(C or None), ldc, vp(workspace or None),
+            workspace_bytes, vp(stream))
+    if rc != 0:
+        raise QgemmError("qgemm", rc)
+
+
+def ipc_handle(t: torch.Tensor) -> tuple[bytes, int, int]:
+    """(64-byte CUDA IPC handle of the allocation holding t, byte offset of
+    t.data_ptr() in it, allocation bytes)."""
+    h = ctypes.create_string_buffer(64)
+    off, size = ctypes.c_uint64(0), ctypes.c_uint64(0)
+    rc = load().qgemm_ipc_handle(ctypes.c_void_p(t.data_ptr()), h, ctypes.byref(off),
+                                 ctypes.byref(size))
+    if rc != 0:
+        raise QgemmError("qgemm_ipc_handle", rc)
+    return h.raw, int(off.value), int(size.value)
+
+
+def ipc_open(handle: bytes, offset: int) -> tuple[int, int]:
+    """Map another process's allocation: (address of the shared tensor, mapping base)."""
+    if len(handle) != 64:
+        raise ValueError("IPC handle must be 64 bytes")
+    p, b = ctypes.c_void_p(), ctypes.c_void_p()
+    rc = load().qgemm_ipc_open(handle, offset, ctypes.byref(p), ctypes.byref(b))
+    if rc != 0:
+        raise QgemmError("qgemm_ipc_open", rc)
+    return int(p.value), int(b.value)
+
+
+def ipc_close(base: int) -> None:
+    rc = load().qgemm_ipc_close(ctypes.c_void_p(base))
+    if rc != 0:
+        raise QgemmError("qgemm_ipc_close", rc)
+
+
 def qgemm_naive(transA: str, transB: str, alpha, A: torch.Tensor, B: torch.Tensor, beta,
                 C: torch.Tensor, M: int | None = None, N: int | None = None, K: int | None = None,
                 stream: torch.cuda.Stream | None = None):

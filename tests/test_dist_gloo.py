@@ -85,3 +85,73 @@ def test_rowsharded_gloo_world2(opA, opB, M):
         p.join(timeout=120)
     assert all(p.exitcode == 0 for p in procs), [p.exitcode for p in procs]
     assert q.get(timeout=5) is True
+
+
+# ---------------------------------------------------------------- fused collection (p2p)
+def _oracle_local_ptr(transA, transB, m_loc, N, K, alpha, A, lda, B, ldb, beta, c_addr, ldc):
+    """Local GEMM on a raw address of root's C (rows r0.. of a column-major
+    matrix with leading dimension ldc) -- the CPU stand-in for the epilogue
+    storing over peer memory."""
+    import ctypes
+    Cv = np.ctypeslib.as_array(ctypes.cast(c_addr, ctypes.POINTER(ctypes.c_double)),
+                               shape=(N, ldc, 4))  # only rows [0, m_loc) are touched
+    oracle.qgemm(transA, transB, m_loc, N, K, alpha, np.ascontiguousarray(A.numpy()),
+                 np.ascontiguousarray(B.numpy()), beta, Cv)
+
+
+def _p2p_worker(rank, world, port, opA, opB, M, N, K, path, q):
+    from paper_1903_05575_b200.dist import PeerC, qgemm_rowsharded_p2p
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        pr = make_problem(M, N, K, opA, opB, (0.5, 0.25, -1, 0.1), (1, -0.5, 0, 0.2), seed=5,
+                          ldc=M + 3)
+        r0, r1 = rows_for_rank(M, world, rank)
+        A_loc = (np.ascontiguousarray(pr.A[:, r0:r1, :]) if opA == "N"
+                 else np.ascontiguousarray(pr.A[r0:r1, :, :]))
+        B = torch.from_numpy(pr.B.copy()) if rank == 0 else torch.full(pr.B.shape, np.nan,
+                                                                        dtype=torch.float64)
+        n_el = pr.C.size
+        keep = []
+
+        def share(t):
+            return path
+
+        def open_(p):
+            t = torch.from_file(p, shared=True, size=n_el, dtype=torch.float64)
+            keep.append(t)
+            return t.data_ptr(), t
+
+        C_root = None
+        if rank == 0:  # root's C (ld = M + 3, padding sentinel) in a shared file
+            C_root = torch.from_file(path, shared=True, size=n_el, dtype=torch.float64)
+            C_root.copy_(torch.from_numpy(pr.C.reshape(-1)))
+            C_root = C_root.view(pr.C.shape)
+        peer = PeerC(C_root, share=share, open_=open_, close=lambda b: None)
+        assert peer.ldc == M + 3 and peer.ncols == N
+        qgemm_rowsharded_p2p(opA, opB, pr.alpha, torch.from_numpy(A_loc), B, pr.beta, peer, M, N,
+                             K, local_gemm_ptr=_oracle_local_ptr)
+        if rank == 0:
+            ref = pr.C.copy()
+            oracle.qgemm(opA, opB, M, N, K, pr.alpha, pr.A, pr.B, pr.beta, ref)
+            q.put(bool(np.array_equal(C_root.numpy(), ref)))  # incl. untouched ld padding
+        peer.close()
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("opA,opB,M", [("N", "H", 150), ("H", "T", 130)])
+def test_rowsharded_p2p_gloo_world2(opA, opB, M, tmp_path):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    N, K = 37, 29
+    path = str(tmp_path / "c_root.bin")
+    procs = [ctx.Process(target=_p2p_worker, args=(r, 2, port, opA, opB, M, N, K, path, q))
+             for r in range(2)]
+    for p in procs:
+        p.start()
+    for p in procs:
+        p.join(timeout=120)
+    assert all(p.exitcode == 0 for p in procs), [p.exitcode for p in procs]
+    assert q.get(timeout=5) is True
