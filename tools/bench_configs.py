@@ -61,8 +61,10 @@ def run(name, M, N, K, opA, opB, alpha, beta, dt=torch.float64, ld=None, ws_cap=
            "dtype": "f64" if dt == torch.float64 else "f32",
            "ms_min": tmin, "ms_med": tmed, "tflops_best": fl / tmin / 1e9,
            "tflops_med": fl / tmed / 1e9,
-           "launches_per_call": (kt["pack"][1] + kt["mainloop"][1] + kt["scale"][1]) // calls,
-           "pack_ms_per_call": kt["pack"][0] / calls, "main_ms_per_call": kt["mainloop"][0] / calls}
+           "launches_per_call": (kt["pack"][1] + kt["mainloop"][1] + kt["scale"][1]
+                                 + kt["small"][1]) // calls,
+           "pack_ms_per_call": kt["pack"][0] / calls,
+           "main_ms_per_call": (kt["mainloop"][0] + kt["small"][0]) / calls}
     if tmin < 5.0:
         # launch-bound sizes: the same call captured once in a CUDA graph and
         # replayed, so host-side Python/ctypes time is not on the device timeline
