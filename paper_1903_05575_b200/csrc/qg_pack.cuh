@@ -45,19 +45,37 @@ struct PlanarLayout {
   __device__ __forceinline__ static int offset(int r, int k, int c) { return (k * 4 + c) * kBR + r; }
 };
 
-// grid: RT*KT blocks (1-D), 256 threads.  Tile staged through shared memory so
-// both the global reads (along the stored contiguous axis) and the chunk
-// writes (linear) are coalesced.
+// One operand panel to pack: rows [0, R) x k in [k_begin, k_end) of op(X), as
+// RT*KT chunks (RT = ceil(R / tile rows)); `blocks` = RT*KT.
+template <typename T>
+struct PackJob {
+  const T *X;
+  int64_t ldx;
+  int row_contig, conj;
+  int64_t R, k_begin, k_end, KT;
+  T *out;
+  int64_t blocks;
+};
+
+// grid: ja.blocks + jb.blocks blocks (1-D), 256 threads: A and B are packed by
+// ONE launch (jb.blocks may be 0).  Tile staged through shared memory so both
+// the global reads (along the stored contiguous axis) and the chunk writes
+// (linear) are coalesced.
 template <typename T, class Layout>
-__global__ void __launch_bounds__(256) pack_kernel(const T *__restrict__ X, int64_t ldx, int row_contig,
-                                                   int conj, int64_t R, int64_t k_begin, int64_t k_end,
-                                                   int64_t KT, T *__restrict__ out) {
+__global__ void __launch_bounds__(256) pack_kernel(const PackJob<T> ja, const PackJob<T> jb) {
+  const bool second = int64_t(blockIdx.x) >= ja.blocks;
+  const PackJob<T> &j = second ? jb : ja;
+  const int64_t bid = second ? int64_t(blockIdx.x) - ja.blocks : int64_t(blockIdx.x);
+  const T *__restrict__ X = j.X;
+  const int64_t ldx = j.ldx, R = j.R, k_end = j.k_end, KT = j.KT;
+  const int row_contig = j.row_contig, conj = j.conj;
+  T *__restrict__ out = j.out;
   __shared__ __align__(16) T tile[kBK * kBR * 4 + 4 * kBK];  // [k][r][c], rows padded by 4 elems per k
   constexpr int kPitch = kBR * 4 + 4;
-  const int64_t rt = blockIdx.x / KT;
-  const int64_t kt = blockIdx.x % KT;
+  const int64_t rt = bid / KT;
+  const int64_t kt = bid % KT;
   const int64_t r0 = rt * kBR;
-  const int64_t k0 = k_begin + kt * kBK;
+  const int64_t k0 = j.k_begin + kt * kBK;
   const T sgn = conj ? T(-1) : T(1);
 
 #pragma unroll
@@ -77,7 +95,7 @@ __global__ void __launch_bounds__(256) pack_kernel(const T *__restrict__ X, int6
     d[0] = v[0]; d[1] = v[1]; d[2] = v[2]; d[3] = v[3];
   }
   __syncthreads();
-  T *o = out + blockIdx.x * (int64_t)kChunkElems;
+  T *o = out + bid * (int64_t)kChunkElems;
   // Walk the chunk linearly, 2 elements per step (16 B for double, 8 B for float).
   for (int w = threadIdx.x; w < kChunkElems / 2; w += 256) {
     // invert the layout for the element pair at offset 2w, 2w+1

@@ -30,6 +30,7 @@
 // tcgen05.ld, apply alpha/beta from the left and store whole quaternions.
 #pragma once
 #include "qg_common.cuh"
+#include "qg_pack.cuh"  // PackJob
 
 namespace qg {
 
@@ -58,13 +59,19 @@ __device__ __forceinline__ float tf32_rna(float x) {
 // Pack for the tensor-core path: rows r of op(X) (R of them) x k in
 // [k_begin, k_end), conj applied, split into tf32 hi/lo, one 32 KiB chunk per
 // (128-row tile, 8-k tile).  grid = RT * KT blocks of 256 threads.
-__global__ void __launch_bounds__(256) pack_tc32_kernel(const float *__restrict__ X, int64_t ldx, int row_contig,
-                                                        int conj, int64_t R, int64_t k_begin, int64_t k_end,
-                                                        int64_t KT, float *__restrict__ out) {
+// grid = ja.blocks + jb.blocks: A and B in one launch (as pack_kernel).
+__global__ void __launch_bounds__(256) pack_tc32_kernel(const PackJob<float> ja, const PackJob<float> jb) {
+  const bool second = int64_t(blockIdx.x) >= ja.blocks;
+  const PackJob<float> &j = second ? jb : ja;
+  const int64_t bid = second ? int64_t(blockIdx.x) - ja.blocks : int64_t(blockIdx.x);
+  const float *__restrict__ X = j.X;
+  const int64_t ldx = j.ldx, R = j.R, k_end = j.k_end, KT = j.KT;
+  const int row_contig = j.row_contig, conj = j.conj;
+  float *__restrict__ out = j.out;
   __shared__ __align__(16) float tile[kTcBK][kTcBM][4];
-  const int64_t rt = blockIdx.x / KT;
-  const int64_t kt = blockIdx.x % KT;
-  const int64_t r0 = rt * kTcBM, k0 = k_begin + kt * kTcBK;
+  const int64_t rt = bid / KT;
+  const int64_t kt = bid % KT;
+  const int64_t r0 = rt * kTcBM, k0 = j.k_begin + kt * kTcBK;
   const float sgn = conj ? -1.f : 1.f;
 #pragma unroll
   for (int it = 0; it < (kTcBM * kTcBK) / 256; ++it) {
@@ -81,7 +88,7 @@ __global__ void __launch_bounds__(256) pack_tc32_kernel(const float *__restrict_
     *reinterpret_cast<float4 *>(&tile[k][r][0]) = make_float4(v[0], v[1], v[2], v[3]);
   }
   __syncthreads();
-  float4 *o = reinterpret_cast<float4 *>(out + blockIdx.x * int64_t(kTcChunkFloats));
+  float4 *o = reinterpret_cast<float4 *>(out + bid * int64_t(kTcChunkFloats));
   for (int o4 = threadIdx.x; o4 < kTcChunkFloats / 4; o4 += 256) {
     const int plane = o4 >> 8, rem = o4 & 255;
     const int rg = rem >> 4, kh = (rem >> 3) & 1, r8 = rem & 7;

@@ -209,19 +209,29 @@ int launch_scale(T *C, int64_t ldc, int64_t M, int64_t N, const qg::Scalars<T> &
 }
 
 template <typename T>
-int launch_pack(const T *X, int64_t ldx, int row_contig, int conj, int64_t R, int64_t k_begin, int64_t k_end,
-                int64_t KT, T *out, cudaStream_t st) {
-  const int64_t blocks = cdiv(R, Geo<T>::rows) * KT;
+qg::PackJob<T> pack_job(const T *X, int64_t ldx, int row_contig, int conj, int64_t R, int64_t k_begin,
+                        int64_t k_end, int64_t KT, T *out) {
+  qg::PackJob<T> j;
+  j.X = X; j.ldx = ldx; j.row_contig = row_contig; j.conj = conj; j.R = R;
+  j.k_begin = k_begin; j.k_end = k_end; j.KT = KT; j.out = out;
+  j.blocks = cdiv(R, Geo<T>::rows) * KT;
+  return j;
+}
+
+// Pack both operands' panels (rows a2 and a3) in ONE launch.
+template <typename T>
+int launch_pack2(const qg::PackJob<T> &ja, const qg::PackJob<T> &jb, cudaStream_t st) {
+  const int64_t blocks = ja.blocks + jb.blocks;
+  if (blocks <= 0) return 0;
+  if (blocks > INT32_MAX) return int(cudaErrorInvalidConfiguration);
   int ti = tstart(kPack, st);
   if constexpr (sizeof(T) == 8)
-    qg::pack_kernel<T, qg::FragLayout><<<unsigned(blocks), 256, 0, st>>>(X, ldx, row_contig, conj, R, k_begin,
-                                                                        k_end, KT, out);
+    qg::pack_kernel<T, qg::FragLayout><<<unsigned(blocks), 256, 0, st>>>(ja, jb);
   else
 #if QG_F32_TC
-    qg::pack_tc32_kernel<<<unsigned(blocks), 256, 0, st>>>(X, ldx, row_contig, conj, R, k_begin, k_end, KT, out);
+    qg::pack_tc32_kernel<<<unsigned(blocks), 256, 0, st>>>(ja, jb);
 #else
-    qg::pack_kernel<T, qg::PlanarLayout><<<unsigned(blocks), 256, 0, st>>>(X, ldx, row_contig, conj, R,
-                                                                          k_begin, k_end, KT, out);
+    qg::pack_kernel<T, qg::PlanarLayout><<<unsigned(blocks), 256, 0, st>>>(ja, jb);
 #endif
   tstop(ti, st);
   ++g_last_launches;
@@ -461,9 +471,8 @@ int panel_loop(const PackSpec<T> &pa, const PackSpec<T> &pb, int64_t M, int64_t 
     const int64_t k_begin = kt0 * Geo<T>::kq;
     const int64_t k_end = std::min<int64_t>(K, (kt0 + KTp) * Geo<T>::kq);
     const int64_t ktn = cdiv(k_end - k_begin, Geo<T>::kq);
-    rc = launch_pack<T>(pa.X, pa.ldx, pa.row_contig, pa.conj, M, k_begin, k_end, ktn, Ap, st);
-    if (rc) return rc;
-    rc = launch_pack<T>(pb.X, pb.ldx, pb.row_contig, pb.conj, N, k_begin, k_end, ktn, Bp, st);
+    rc = launch_pack2<T>(pack_job<T>(pa.X, pa.ldx, pa.row_contig, pa.conj, M, k_begin, k_end, ktn, Ap),
+                         pack_job<T>(pb.X, pb.ldx, pb.row_contig, pb.conj, N, k_begin, k_end, ktn, Bp), st);
     if (rc) return rc;
     rc = launch_mainloop(Ap, Bp, C, ldc, M, N, ktn, kt0 == 0 ? sc : sc_acc, sk_scratch, st, tri);
     if (rc) return rc;
@@ -715,9 +724,9 @@ int qgemm_host_impl(char transA, char transB, int64_t M, int64_t N, int64_t K, c
     const int64_t ktn = cdiv(kc, Geo<T>::kq);
     T *pa = reinterpret_cast<T *>(ws + h.off_pa[sl]);
     T *pb = reinterpret_cast<T *>(ws + h.off_pb[sl]);
-    QH_TRY(launch_pack<T>(reinterpret_cast<const T *>(ws + h.off_sa[sl]), lda_s, a_rc, a_cj, M, 0, kc, ktn, pa, S));
-    QH_TRY(launch_pack<T>(reinterpret_cast<const T *>(ws + h.off_sb[sl]), ldb_s, b_rc, b_cj, N, 0, kc, ktn, pb, S));
-    launches += 2;
+    QH_TRY(launch_pack2<T>(pack_job<T>(reinterpret_cast<const T *>(ws + h.off_sa[sl]), lda_s, a_rc, a_cj, M, 0, kc, ktn, pa),
+                           pack_job<T>(reinterpret_cast<const T *>(ws + h.off_sb[sl]), ldb_s, b_rc, b_cj, N, 0, kc, ktn, pb), S));
+    launches += 1;
     packed[size_t(p)] = hs.ev();
     QH_TRY(int(cudaEventRecord(packed[size_t(p)], S)));
     const qg::Scalars<T> &scp = p == 0 ? sc : sc_acc;
