@@ -32,6 +32,25 @@ __global__ void qgemm_scale_kernel(T *C, int64_t ldc, int64_t M, int64_t N, Scal
   }
 }
 
+// Y <- Y + beta (x) X (left quaternion product): folds the caller's C into the
+// accumulated alpha op(A) op(B) of the host-streamed path (qgemm_host).  HBM-bound.
+template <typename T>
+__global__ void qgemm_axpby_kernel(T *Y, int64_t ldy, const T *X, int64_t ldx, int64_t M, int64_t N,
+                                   Scalars<T> sc) {
+  const int64_t total = M * N;
+  for (int64_t idx = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; idx < total;
+       idx += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t i = idx % M, j = idx / M;
+    T x[4], bx[4], y[4];
+    ldq(X + 4 * (i + j * ldx), x);
+    ldq_c(Y + 4 * (i + j * ldy), y);
+    left_scale(sc.beta, sc.beta_real, x, bx);
+#pragma unroll
+    for (int c = 0; c < 4; ++c) y[c] += bx[c];
+    stq(Y + 4 * (i + j * ldy), y);
+  }
+}
+
 template <typename T>
 __global__ void qgemm_naive_kernel(int opA, int opB, int64_t M, int64_t N, int64_t K, const T *A, int64_t lda,
                                    const T *B, int64_t ldb, T *C, int64_t ldc, Scalars<T> sc) {

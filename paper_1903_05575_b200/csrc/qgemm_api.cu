@@ -208,6 +208,20 @@ int launch_scale(T *C, int64_t ldc, int64_t M, int64_t N, const qg::Scalars<T> &
   return int(cudaGetLastError());
 }
 
+// Y <- Y + beta (x) X over an M x N block (beta from sc, left product); HBM-bound.
+template <typename T>
+int launch_axpby(T *Y, int64_t ldy, const T *X, int64_t ldx, int64_t M, int64_t N, const qg::Scalars<T> &sc,
+                 cudaStream_t st) {
+  const int64_t total = M * N;
+  const int threads = 256;
+  const int64_t blocks = std::min<int64_t>(cdiv(total, threads), 148 * 16);
+  { int ti = tstart(kScale, st);
+  qg::qgemm_axpby_kernel<T><<<unsigned(blocks), threads, 0, st>>>(Y, ldy, X, ldx, M, N, sc);
+  tstop(ti, st); }
+  ++g_last_launches;
+  return int(cudaGetLastError());
+}
+
 template <typename T>
 qg::PackJob<T> pack_job(const T *X, int64_t ldx, int row_contig, int conj, int64_t R, int64_t k_begin,
                         int64_t k_end, int64_t KT, T *out) {
@@ -549,9 +563,11 @@ size_t ws_bytes(char transA, char transB, int64_t M, int64_t N, int64_t K, bool 
 template <typename T>
 struct HostPlan {
   bool small = false;       // one-launch kernel on the whole problem (Q = P = 1)
-  int64_t Kc = 0, Q = 0;    // K chunk and chunk count
-  int64_t Nj = 0, P = 0;    // C column panel width and count
-  size_t off_sa[2], off_sb[2], off_pa[2], off_pb[2], off_sk = 0, total = 0;  // off_C = 0
+  int64_t Kc0 = 0, Kc = 0, Q = 0;  // first K chunk (short: compute starts early), later chunks, count
+  int64_t Nj = 0, P = 0;    // C column panel width and count (last chunk / downloads)
+  size_t off_cold = 0;      // device copy of the caller's C (beta != 0); off_C = 0
+  size_t off_sa[2], off_sb[2], off_pa[2], off_pb[2], off_sk = 0, total = 0;
+  int64_t k_begin(int64_t p) const { return p == 0 ? 0 : Kc0 + (p - 1) * Kc; }
 };
 
 template <typename T>
@@ -561,14 +577,20 @@ HostPlan<T> host_plan(int64_t M, int64_t N, int64_t K) {
   const int64_t kq = Geo<T>::kq, rows = 128;  // panel width: multiple of both tile sizes (64, 128)
   h.small = use_small<T>(M, N, K);
   if (h.small || K == 0) {
-    h.Kc = std::max<int64_t>(K, 1); h.Q = 1; h.Nj = N; h.P = 1;
+    h.Kc0 = h.Kc = std::max<int64_t>(K, 1); h.Q = 1; h.Nj = N; h.P = 1;
   } else {
+    // chunks of ~K/8 (256..2048); the first one a quarter of that, so the first
+    // mainloop waits only for a small upload
     h.Kc = std::min<int64_t>(cdiv(K, kq) * kq, std::max<int64_t>(256, std::min<int64_t>(2048, cdiv(cdiv(K, 8), kq) * kq)));
-    h.Q = cdiv(K, h.Kc);
-    h.Nj = std::min<int64_t>(cdiv(N, rows) * rows, std::max<int64_t>(256, cdiv(cdiv(N, 8), rows) * rows));
+    h.Kc0 = std::min<int64_t>(h.Kc, std::max<int64_t>(kq, cdiv(cdiv(h.Kc, 4), kq) * kq));
+    h.Q = K <= h.Kc0 ? 1 : 1 + cdiv(K - h.Kc0, h.Kc);
+    h.Nj = std::min<int64_t>(cdiv(N, rows) * rows, std::max<int64_t>(256, cdiv(cdiv(N, 16), rows) * rows));
     h.P = cdiv(N, h.Nj);
   }
-  size_t off = align256(size_t(M) * size_t(N) * qb);  // C, compact ld = M
+  const size_t csz = align256(size_t(M) * size_t(N) * qb);  // C, compact ld = M
+  size_t off = csz;
+  h.off_cold = off;
+  if (!h.small && K > 0) off += csz;  // the caller's C waits here until the axpby pass
   const size_t sa = align256(size_t(M) * size_t(h.Kc) * qb), sb = align256(size_t(N) * size_t(h.Kc) * qb);
   const int nbuf = (h.Q > 1) ? 2 : 1;
   for (int i = 0; i < 2; ++i) { h.off_sa[i] = off; if (i < nbuf) off += sa; }
@@ -668,9 +690,14 @@ int qgemm_host_impl(char transA, char transB, int64_t M, int64_t N, int64_t K, c
 
   // staged operand views (compact): chunk p of op(A) and op(B) over k in [k0, k1)
   const int a_rc = sh.oa == 0, a_cj = sh.oa == 2, b_rc = sh.ob != 0, b_cj = sh.ob == 2;
+  auto chunk = [&](int64_t p, int64_t &k0, int64_t &kc) {
+    k0 = h.k_begin(p);
+    kc = std::min<int64_t>(K, p == 0 ? h.Kc0 : k0 + h.Kc) - k0;
+  };
   auto stage = [&](int64_t p) -> int {  // on H
     const int sl = int(p & 1);
-    const int64_t k0 = p * h.Kc, kc = std::min<int64_t>(K, k0 + h.Kc) - k0;
+    int64_t k0, kc;
+    chunk(p, k0, kc);
     T *sa = reinterpret_cast<T *>(ws + h.off_sa[sl]);
     T *sb = reinterpret_cast<T *>(ws + h.off_sb[sl]);
     int r = a_rc ? copy2d(sa, M, A + 4 * (k0 * lda), lda, M, kc, hs.H)     // A(:, k0:k1), ld M
@@ -695,57 +722,73 @@ int qgemm_host_impl(char transA, char transB, int64_t M, int64_t N, int64_t K, c
     return int(hs.err);
   }
 
-  qg::Scalars<T> sc_acc = sc;  // chunks after the first accumulate onto C: beta = 1
-  for (int c = 0; c < 4; ++c) sc_acc.beta[c] = T(c == 0 ? 1 : 0);
-  sc_acc.beta_real = 1;
-  sc_acc.beta_zero = 0;
+  // Cd accumulates T = alpha sum_p op(A)_p op(B)_p from beta = 0 (the caller's C
+  // is not needed for that); the caller's C is uploaded behind the first two
+  // chunks into Cold and folded in with one axpby pass, Cd += beta Cold, before
+  // the last chunk (or per panel inside it when there are fewer than 3 chunks).
+  qg::Scalars<T> sc0 = sc, sc_acc = sc;
+  for (int c = 0; c < 4; ++c) {
+    sc0.beta[c] = T(0);
+    sc_acc.beta[c] = T(c == 0 ? 1 : 0);
+  }
+  sc0.beta_real = 1; sc0.beta_zero = 1;
+  sc_acc.beta_real = 1; sc_acc.beta_zero = 0;
+  T *Cold = reinterpret_cast<T *>(ws + h.off_cold);
   void *sk = ws + h.off_sk;
-  std::vector<cudaEvent_t> c_up(size_t(h.P), nullptr);
   std::vector<cudaEvent_t> packed(size_t(h.Q), nullptr);
+  cudaEvent_t c_up = nullptr;
+  bool folded = !need_c;
+  const int64_t p_fold = h.Q >= 3 ? h.Q - 2 : -1;  // fold after this chunk's mainloop
 
   for (int64_t p = 0; p < h.Q; ++p) {
     const int sl = int(p & 1);
-    // ---- H: staging slot sl is free once the packs of chunk p-2 have run
+    // ---- H: staging slot sl is free once the pack of chunk p-2 has run
     if (p >= 2) QH_TRY(int(cudaStreamWaitEvent(hs.H, packed[size_t(p - 2)], 0)));
     QH_TRY(stage(p));
     cudaEvent_t staged = hs.ev();
     QH_TRY(int(cudaEventRecord(staged, hs.H)));
-    if (p == 0 && need_c) {
-      for (int64_t j = 0; j < h.P; ++j) {
-        const int64_t n0 = j * h.Nj, nj = std::min<int64_t>(N, n0 + h.Nj) - n0;
-        QH_TRY(copy2d(Cd + 4 * (n0 * M), M, C + 4 * (n0 * ldc), ldc, M, nj, hs.H));
-        c_up[size_t(j)] = hs.ev();
-        QH_TRY(int(cudaEventRecord(c_up[size_t(j)], hs.H)));
-      }
+    if (need_c && p == std::min<int64_t>(1, h.Q - 1)) {  // the caller's C, behind chunks 0 and 1
+      QH_TRY(copy2d(Cold, M, C, ldc, M, N, hs.H));
+      c_up = hs.ev();
+      QH_TRY(int(cudaEventRecord(c_up, hs.H)));
     }
     // ---- S: pack chunk p, then its mainloop(s)
     QH_TRY(int(cudaStreamWaitEvent(S, staged, 0)));
-    const int64_t k0 = p * h.Kc, kc = std::min<int64_t>(K, k0 + h.Kc) - k0;
+    int64_t k0, kc;
+    chunk(p, k0, kc);
     const int64_t ktn = cdiv(kc, Geo<T>::kq);
     T *pa = reinterpret_cast<T *>(ws + h.off_pa[sl]);
     T *pb = reinterpret_cast<T *>(ws + h.off_pb[sl]);
     QH_TRY(launch_pack2<T>(pack_job<T>(reinterpret_cast<const T *>(ws + h.off_sa[sl]), lda_s, a_rc, a_cj, M, 0, kc, ktn, pa),
                            pack_job<T>(reinterpret_cast<const T *>(ws + h.off_sb[sl]), ldb_s, b_rc, b_cj, N, 0, kc, ktn, pb), S));
-    launches += 1;
+    ++launches;
     packed[size_t(p)] = hs.ev();
     QH_TRY(int(cudaEventRecord(packed[size_t(p)], S)));
-    const qg::Scalars<T> &scp = p == 0 ? sc : sc_acc;
-    const bool first = p == 0, last = p == h.Q - 1;
-    if (!first && !last) {
+    const qg::Scalars<T> &scp = p == 0 ? sc0 : sc_acc;
+    if (p != h.Q - 1) {
       QH_TRY(launch_mainloop(pa, pb, Cd, M, M, N, ktn, scp, sk, S));
       ++launches;
+      if (!folded && p == p_fold) {
+        QH_TRY(int(cudaStreamWaitEvent(S, c_up, 0)));
+        QH_TRY(launch_axpby(Cd, M, Cold, M, M, N, sc, S));
+        ++launches;
+        folded = true;
+      }
       continue;
     }
-    for (int64_t j = 0; j < h.P; ++j) {  // per column panel of C
+    if (!folded) QH_TRY(int(cudaStreamWaitEvent(S, c_up, 0)));
+    for (int64_t j = 0; j < h.P; ++j) {  // last chunk: per column panel, each downloaded at once
       const int64_t n0 = j * h.Nj, nj = std::min<int64_t>(N, n0 + h.Nj) - n0;
-      if (first && need_c) QH_TRY(int(cudaStreamWaitEvent(S, c_up[size_t(j)], 0)));
       const T *pbj = pb + size_t(n0 / Geo<T>::rows) * size_t(ktn) * (Geo<T>::chunk / sizeof(T));
-      QH_TRY(launch_mainloop(pa, pbj, Cd + 4 * (n0 * M), M, M, nj, ktn, scp, sk, S));
+      T *Cdj = Cd + 4 * (n0 * M);
+      QH_TRY(launch_mainloop(pa, pbj, Cdj, M, M, nj, ktn, scp, sk, S));
       ++launches;
-      if (last) {
-        hs.link(S, hs.D);
-        QH_TRY(copy2d(C + 4 * (n0 * ldc), ldc, Cd + 4 * (n0 * M), M, M, nj, hs.D));
+      if (!folded) {
+        QH_TRY(launch_axpby(Cdj, M, Cold + 4 * (n0 * M), M, M, nj, sc, S));
+        ++launches;
       }
+      hs.link(S, hs.D);
+      QH_TRY(copy2d(C + 4 * (n0 * ldc), ldc, Cdj, M, M, nj, hs.D));
     }
   }
   hs.link(hs.D, S);  // the call is complete when the caller's stream is
