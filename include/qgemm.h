@@ -185,7 +185,12 @@ int qgemm_naive(char transA, char transB, int64_t M, int64_t N, int64_t K,
                 double *C, int64_t ldc, void *stream);
 
 /* Path policy (process-wide): 0 = auto (default), 1 = always the packed
- * path (pack + persistent mainloop), 2 = always the one-launch small kernel.
+ * path (pack launch + persistent mainloop), 2 = always the one-launch small
+ * kernel, 3 = direct (FP64: the pack fused into the persistent mainloop's
+ * producer warpgroup, which de-interleaves op(A)/op(B) tiles straight into
+ * shared memory -- one launch, workspace = stream-K scratch only, ~3% slower
+ * than packed at c3; FP32 calls take the packed path).  Auto = small kernel
+ * below the crossover, else packed.
  * Returns the previous policy, or -1 (policy unchanged) for other values.
  * For tests and benchmarks; the result is correct under every policy. */
 int qgemm_set_path_policy(int policy);

@@ -23,6 +23,7 @@ from .qgemm import (  # noqa: F401
     PATH_AUTO,
     PATH_PACKED,
     PATH_SMALL,
+    PATH_DIRECT,
     timing_collect,
     timing_enable,
     version,

@@ -40,18 +40,11 @@ namespace qg {
 constexpr int kStages = 3;
 constexpr int kConsumerWarps = 8;
 constexpr int kConsumerThreads = kConsumerWarps * 32;
-#ifndef QG_PRODUCER_WG
-#define QG_PRODUCER_WG 1
-#endif
-#if QG_PRODUCER_WG
 // 8 consumer warps + a producer warpgroup; setmaxnreg moves registers from the
 // producer (40/thread) to the consumers (232/thread): 128*40 + 256*232 <= 64K.
 constexpr int kDmmaThreads = (kConsumerWarps + 4) * 32;
 constexpr int kProducerRegs = 40;
 constexpr int kConsumerRegs = 232;
-#else
-constexpr int kDmmaThreads = kConsumerWarps * 32;  // producer role lives in thread 0
-#endif
 constexpr int kGroupM = 8;  // rasterisation: 8 M-tiles share each B panel in flight
 constexpr size_t kDmmaSmemBytes = size_t(kStages) * 2 * kChunkElems * sizeof(double) + 2 * kStages * 8;
 constexpr int kAccPerThread = 64;                      // doubles
@@ -59,8 +52,13 @@ constexpr size_t kPartialBytes = size_t(kConsumerThreads) * kAccPerThread * size
 constexpr int kMaxPersistentCTAs = 256;
 
 struct DmmaArgs {
-  const double *Ap;  // packed A panel: MT x KT chunks
-  const double *Bp;  // packed B panel: NT x KT chunks
+  const double *Ap;  // packed path: packed A panel, MT x KT chunks
+  const double *Bp;  // packed path: packed B panel, NT x KT chunks
+  // direct path (pack fused into the producer): op(A) / op(B) read in place as
+  // R x K views -- X~(r, k) at X + 4(r + k ldx) (rc = 1) or X + 4(k + r ldx) (rc = 0)
+  const double *A, *B;
+  int64_t lda, ldb, K;
+  int a_rc, b_rc;
   double *C;
   int64_t ldc, M, N, MT, NT, KT;
   Scalars<double> sc;
@@ -163,6 +161,7 @@ __device__ __forceinline__ int ld_acquire(const int *p) {
 struct Producer {
   WorkIter it;
   int64_t kt, ke;
+  int64_t mt, nt;  // direct path: tile coordinates of the current unit
   const double *a_src, *b_src;
   int slot;
   uint32_t phase;
@@ -193,6 +192,72 @@ __device__ __forceinline__ bool produce_next(Producer &p, const DmmaArgs &args, 
   return true;
 }
 
+// ---- direct path: the pack (rows a2/a3) fused into the producer warpgroup ----
+// 16-byte cp.async (LDGSTS, no registers staged) global -> shared; src-size 0
+// zero-fills rows r >= R and k >= K (the zero padding of Alg. 2).
+__device__ __forceinline__ void cp_async16_zfill(void *smem, const void *gmem, bool valid) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(smem_u32(smem)), "l"(gmem),
+               "r"(valid ? 16 : 0)
+               : "memory");
+}
+// The mbarrier's next arrival by this thread fires when its prior cp.asyncs land.
+__device__ __forceinline__ void cp_async_mbar_arrive_noinc(uint64_t *bar) {
+  asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];\n" ::"r"(smem_u32(bar)) : "memory");
+}
+
+constexpr int kProducerThreads = 128;
+
+// One 64-row x 16-k tile of an interleaved operand view into a FragLayout chunk:
+// 2048 16-byte halves (components 0-1 | 2-3) of 1024 quaternions, 16 per
+// producer thread.  The 16-byte slot of (r, k, half) sits in bank group
+// ((r & 1) << 2 | (k & 3)) of the chunk, so a warp's 32 copies must span 2 row
+// parities x 4 k residues to be conflict-free (4 lanes per group = the minimum
+// 4 wavefronts); within that, lanes run along the stored contiguous axis:
+//   rows contiguous (rc): 4 k x 4 consecutive rows x 2 halves -> 4 runs of 128 B
+//   k contiguous:         2 rows x 8 consecutive k x 2 halves -> 2 runs of 256 B
+__device__ __forceinline__ void load_tile_direct(double *dst, const double *X, int64_t ldx, int rc, int64_t r0,
+                                                 int64_t R, int64_t k0, int64_t K, int ptid) {
+#pragma unroll 4
+  for (int it = 0; it < (kBR * kBK * 2) / kProducerThreads; ++it) {
+    const int q = ptid + kProducerThreads * it;
+    const int pp = q & 1;
+    int r, k;
+    if (rc) { k = ((q >> 9) << 2) | ((q >> 1) & 3); r = (((q >> 5) & 15) << 2) | ((q >> 3) & 3); }
+    else    { k = (((q >> 5) & 1) << 3) | ((q >> 1) & 7); r = ((q >> 6) << 1) | ((q >> 4) & 1); }
+    const int64_t gr = r0 + r, gk = k0 + k;
+    const bool valid = gr < R && gk < K;
+    const double *src = valid ? X + 4 * (rc ? gr + gk * ldx : gk + gr * ldx) + 2 * pp : X;
+    const int off = ((((k >> 2) * 8 + (r >> 3)) * 2 + pp) * 32 + (((r & 7) << 2) | (k & 3))) * 2;
+    cp_async16_zfill(dst + off, src, valid);
+  }
+}
+
+// Direct-path fill, executed by all 128 producer threads.
+__device__ __forceinline__ bool produce_next_direct(Producer &p, const DmmaArgs &args, double *sA, double *sB,
+                                                    uint64_t *full, uint64_t *empty, int ptid) {
+  while (p.kt >= p.ke) {
+    Unit u;
+    if (!p.it.next(args, u)) return false;
+    work_tile(args, u.t, p.mt, p.nt);
+    p.kt = u.kb;
+    p.ke = u.ke;
+  }
+  if (p.fills >= kStages) mbar_wait(&empty[p.slot], p.phase ^ 1u);
+  const int64_t k0 = p.kt * kBK;
+  load_tile_direct(sA + p.slot * kChunkElems, args.A, args.lda, args.a_rc, p.mt * kBR, args.M, k0, args.K, ptid);
+  load_tile_direct(sB + p.slot * kChunkElems, args.B, args.ldb, args.b_rc, p.nt * kBR, args.N, k0, args.K, ptid);
+  cp_async_mbar_arrive_noinc(&full[p.slot]);
+  if (++p.slot == kStages) { p.slot = 0; p.phase ^= 1u; }
+  ++p.kt;
+  ++p.fills;
+  return true;
+}
+
+// kDirect: operands read in place by the producer warpgroup (CA / CB: op H on
+// A / B, folded into the sign of each of the 16 products: conj flips the sign
+// of components 1-3); otherwise from packed chunks (conj applied by
+// the pack kernel; CA = CB = false).
+template <bool kDirect, bool CA, bool CB>
 __global__ void __launch_bounds__(kDmmaThreads, 1) qgemm_dmma_kernel(const DmmaArgs args) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   double *sA = reinterpret_cast<double *>(smem_raw);
@@ -209,19 +274,17 @@ __global__ void __launch_bounds__(kDmmaThreads, 1) qgemm_dmma_kernel(const DmmaA
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < kStages; ++s) {
-      mbar_init(&full[s], 1);
+      mbar_init(&full[s], kDirect ? kProducerThreads : 1);
       mbar_init(&empty[s], kConsumerWarps);
     }
     fence_mbar_init();
   }
   __syncthreads();
 
-  // ---------------- producer role (thread 0), kStages - 1 fills ahead ----------------
-  // Thread 0 streams the A/B chunks of the CTA's work list; it refills the slot
-  // of consumption f-1 at the start of consumption f (a one-step lag, so it
-  // rarely waits for the other warps).  Keeping the producer inside a compute
-  // warp (8 warps, 2 per SM sub-partition) leaves 255 registers per thread; a
-  // ninth warp would cap every thread at 168 (3 warps on one sub-partition).
+  // ---------------- producer warpgroup, kStages fills ahead ----------------
+  // Packed path: one lane streams packed chunks with bulk copies.  Direct path:
+  // all 128 threads de-interleave op(A)/op(B) tiles into the same chunk layout
+  // with cp.async.  setmaxnreg hands the warpgroup's registers to the consumers.
   Producer prod;
   prod.it = make_iter(args, sp);
   prod.kt = 0;
@@ -229,20 +292,20 @@ __global__ void __launch_bounds__(kDmmaThreads, 1) qgemm_dmma_kernel(const DmmaA
   prod.slot = 0;
   prod.phase = 0;
   prod.fills = 0;
-#if QG_PRODUCER_WG
   if (warp >= kConsumerWarps) {
-    // producer warpgroup: give registers back, one lane streams every fill
     asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;\n" ::"n"(kProducerRegs));
-    if (warp == kConsumerWarps && lane == 0)
-      while (produce_next(prod, args, sA, sB, full, empty)) {
+    if constexpr (kDirect) {
+      const int ptid = threadIdx.x - kConsumerThreads;
+      while (produce_next_direct(prod, args, sA, sB, full, empty, ptid)) {
       }
+    } else {
+      if (warp == kConsumerWarps && lane == 0)
+        while (produce_next(prod, args, sA, sB, full, empty)) {
+        }
+    }
     return;
   }
   asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;\n" ::"n"(kConsumerRegs));
-#else
-  if (threadIdx.x == 0)
-    for (int s = 0; s < kStages; ++s) produce_next(prod, args, sA, sB, full, empty);
-#endif
 
   // ---------------- consumers ----------------
   const int wm = warp & 1;   // 32-row half of the CTA tile
@@ -250,7 +313,6 @@ __global__ void __launch_bounds__(kDmmaThreads, 1) qgemm_dmma_kernel(const DmmaA
   const int tid = threadIdx.x;
   int slot = 0;
   uint32_t phase = 0;
-  [[maybe_unused]] bool first = true;
   WorkIter it = make_iter(args, sp);
   Unit u;
   while (it.next(args, u)) {
@@ -281,11 +343,6 @@ __global__ void __launch_bounds__(kDmmaThreads, 1) qgemm_dmma_kernel(const DmmaA
                 asm volatile("prefetch.global.L2 [%0];\n" ::"l"(args.C + 4 * (row + col * args.ldc)));
             }
       }
-      // refill the slot consumption f-1 used (fill f-1+kStages), then consume f
-#if !QG_PRODUCER_WG
-      if (tid == 0 && !first) produce_next(prod, args, sA, sB, full, empty);
-#endif
-      first = false;
       mbar_wait(&full[slot], phase);
       const double2 *a2 = reinterpret_cast<const double2 *>(sA + slot * kChunkElems);
       const double2 *b2 = reinterpret_cast<const double2 *>(sB + slot * kChunkElems);
@@ -323,7 +380,8 @@ __global__ void __launch_bounds__(kDmmaThreads, 1) qgemm_dmma_kernel(const DmmaA
 #pragma unroll
               for (int c = 0; c < 4; ++c) {
                 const int s = p ^ c;
-                dmma_8x8x4(acc[ii][jj][c], af[ii][p], hneg(p, s) ? bn[jj][s] : bf[jj][s]);
+                const bool neg = hneg(p, s) ^ (CA && p != 0) ^ (CB && s != 0);
+                dmma_8x8x4(acc[ii][jj][c], af[ii][p], neg ? bn[jj][s] : bf[jj][s]);
               }
       }
       __syncwarp();

@@ -261,8 +261,8 @@ int persistent_ctas() {
   if (cudaGetDevice(&dev) != cudaSuccess) return 0;
   if (dev < kMaxDev && cache[dev] > 0) return cache[dev];
   if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess) return 0;
-  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, qg::qgemm_dmma_kernel, qg::kDmmaThreads,
-                                                    qg::kDmmaSmemBytes) != cudaSuccess)
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, qg::qgemm_dmma_kernel<false, false, false>,
+                                                    qg::kDmmaThreads, qg::kDmmaSmemBytes) != cudaSuccess)
     return 0;
   const int r = std::min(qg::kMaxPersistentCTAs, sms * std::max(1, per_sm));
   if (dev < kMaxDev) cache[dev] = r;
@@ -286,21 +286,40 @@ void plan_schedule(qg::DmmaArgs &a, int resident) {
   a.grid = G;
 }
 
-int launch_mainloop(const double *Ap, const double *Bp, double *C, int64_t ldc, int64_t M, int64_t N,
-                    int64_t KT, const qg::Scalars<double> &sc, void *sk_scratch, cudaStream_t st, int tri = 0) {
-  static bool attr_set = false;
-  if (!attr_set) {
-    cudaError_t e = cudaFuncSetAttribute(qg::qgemm_dmma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         int(qg::kDmmaSmemBytes));
+using DmmaKernel = void (*)(const qg::DmmaArgs);
+
+// The five instantiations: packed, and direct x (conj A, conj B).
+DmmaKernel dmma_kernel(bool direct, bool ca, bool cb) {
+  if (!direct) return qg::qgemm_dmma_kernel<false, false, false>;
+  if (ca) return cb ? qg::qgemm_dmma_kernel<true, true, true> : qg::qgemm_dmma_kernel<true, true, false>;
+  return cb ? qg::qgemm_dmma_kernel<true, false, true> : qg::qgemm_dmma_kernel<true, false, false>;
+}
+
+int dmma_set_attributes() {
+  constexpr int kMaxDev = 64;
+  static bool done[kMaxDev] = {false};
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return int(e);
+  if (dev < kMaxDev && done[dev]) return 0;
+  const DmmaKernel ks[5] = {dmma_kernel(false, false, false), dmma_kernel(true, false, false),
+                            dmma_kernel(true, true, false), dmma_kernel(true, false, true),
+                            dmma_kernel(true, true, true)};
+  for (DmmaKernel k : ks) {
+    e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(qg::kDmmaSmemBytes));
     if (e != cudaSuccess) return int(e);
-    attr_set = true;
   }
+  if (dev < kMaxDev) done[dev] = true;
+  return 0;
+}
+
+// Schedule + stream-K scratch + launch of a filled-in DmmaArgs (operands set).
+int launch_dmma(qg::DmmaArgs &a, DmmaKernel kernel, void *sk_scratch, cudaStream_t st) {
+  int rc = dmma_set_attributes();
+  if (rc) return rc;
   const int resident = persistent_ctas();
   if (resident <= 0) return int(cudaErrorInvalidConfiguration);
-  qg::DmmaArgs a;
-  a.Ap = Ap; a.Bp = Bp; a.C = C; a.ldc = ldc; a.M = M; a.N = N;
-  a.MT = cdiv(M, qg::kBR); a.NT = cdiv(N, qg::kBR); a.KT = KT; a.sc = sc;
-  a.tri = tri;
+  a.MT = cdiv(a.M, qg::kBR); a.NT = cdiv(a.N, qg::kBR);
   plan_schedule(a, resident);
   // scratch layout: [2*kMaxPersistentCTAs arrival counters][grid partial slots]
   a.flags = reinterpret_cast<int *>(sk_scratch);
@@ -311,10 +330,29 @@ int launch_mainloop(const double *Ap, const double *Bp, double *C, int64_t ldc, 
     if (e != cudaSuccess) return int(e);
   }
   { int ti = tstart(kMain, st);
-  qg::qgemm_dmma_kernel<<<unsigned(a.grid), qg::kDmmaThreads, qg::kDmmaSmemBytes, st>>>(a);
+  kernel<<<unsigned(a.grid), qg::kDmmaThreads, qg::kDmmaSmemBytes, st>>>(a);
   tstop(ti, st); }
   ++g_last_launches;
   return int(cudaGetLastError());
+}
+
+// Packed path: operands from packed chunks (pack_kernel).
+int launch_mainloop(const double *Ap, const double *Bp, double *C, int64_t ldc, int64_t M, int64_t N,
+                    int64_t KT, const qg::Scalars<double> &sc, void *sk_scratch, cudaStream_t st, int tri = 0) {
+  qg::DmmaArgs a{};
+  a.Ap = Ap; a.Bp = Bp; a.C = C; a.ldc = ldc; a.M = M; a.N = N; a.KT = KT; a.sc = sc; a.tri = tri;
+  return launch_dmma(a, dmma_kernel(false, false, false), sk_scratch, st);
+}
+
+// Direct path: op(A), op(B) read in place by the producer warpgroup (no pack
+// launch, no packed workspace).  rc / cj as PackSpec (row_contig, conj).
+int launch_mainloop_direct(const double *A, int64_t lda, int a_rc, int a_cj, const double *B, int64_t ldb,
+                           int b_rc, int b_cj, double *C, int64_t ldc, int64_t M, int64_t N, int64_t K,
+                           const qg::Scalars<double> &sc, void *sk_scratch, cudaStream_t st, int tri = 0) {
+  qg::DmmaArgs a{};
+  a.A = A; a.B = B; a.lda = lda; a.ldb = ldb; a.K = K; a.a_rc = a_rc; a.b_rc = b_rc;
+  a.C = C; a.ldc = ldc; a.M = M; a.N = N; a.KT = cdiv(K, qg::kBK); a.sc = sc; a.tri = tri;
+  return launch_dmma(a, dmma_kernel(true, a_cj != 0, b_cj != 0), sk_scratch, st);
 }
 
 int launch_mainloop(const float *Ap, const float *Bp, float *C, int64_t ldc, int64_t M, int64_t N, int64_t KT,
@@ -354,10 +392,21 @@ int launch_mainloop(const float *Ap, const float *Bp, float *C, int64_t ldc, int
   return int(cudaGetLastError());
 }
 
-// ---- path choice: packed (pack + persistent mainloop) vs one-launch small kernel
-// 0 = auto, 1 = always packed, 2 = small kernel whenever the call reads A and B
-// (qgemm_set_path_policy; tests use 1/2 to cover both paths at every shape).
+// ---- path choice: packed (pack launch + persistent mainloop), direct (FP64:
+// the pack fused into the mainloop's producer warpgroup) or the one-launch
+// small kernel.  0 = auto, 1 = always packed, 2 = small kernel whenever the call
+// reads A and B, 3 = direct for FP64 (packed for FP32) -- qgemm_set_path_policy;
+// the tests run every shape under each.
 std::atomic<int> g_path_policy{0};
+
+// Direct path only on request: measured 3.3% slower than pack + mainloop at c3
+// (494.7 vs 478.9 ms) and c4 (255.1 vs 247.1 ms), equal at c2;
+// its merit is memory: the workspace is the stream-K scratch only.
+template <typename T>
+bool use_direct() {
+  if (sizeof(T) != 8) return false;
+  return g_path_policy.load(std::memory_order_relaxed) == 3;
+}
 // Auto policy (crossover measured on B200 with tools/small_sweep.py):
 //  * FP64: the small kernel up to 2^24 quaternion multiply-adds (256^3), where
 //    the packed path's persistent DMMA mainloop catches up;
@@ -373,7 +422,7 @@ int num_sms();
 template <typename T>
 bool use_small(int64_t M, int64_t N, int64_t K) {
   const int pol = g_path_policy.load(std::memory_order_relaxed);
-  if (pol == 1) return false;
+  if (pol == 1 || pol == 3) return false;
   if (pol == 2) return true;
   constexpr int64_t kCap = int64_t(1) << 28;
   if (M > kCap || N > kCap || K > kCap) return false;  // keeps M*N*K from overflowing below
@@ -452,6 +501,14 @@ int qgemm_impl(char transA, char transB, int64_t M, int64_t N, int64_t K, const 
   if (use_small<T>(M, N, K))  // one launch, no workspace (NEXT item 4)
     return launch_small<T>(A, lda, pa.row_contig, pa.conj, B, ldb, pb.row_contig, pb.conj, C, ldc, M, N, K,
                            alpha, beta, st);
+  if constexpr (sizeof(T) == 8) {
+    if (use_direct<T>()) {  // one launch; the workspace holds only the stream-K scratch
+      if (workspace == nullptr || (reinterpret_cast<uintptr_t>(workspace) & 255u)) return -14;
+      if (workspace_bytes < sk_reserve<T>(M, N, cdiv(K, Geo<T>::kq))) return -15;
+      return launch_mainloop_direct(A, lda, pa.row_contig, pa.conj, B, ldb, pb.row_contig, pb.conj, C, ldc, M,
+                                    N, K, sc, workspace, st);
+    }
+  }
   return panel_loop<T>(pa, pb, M, N, K, sc, C, ldc, workspace, workspace_bytes, st, 0);
 }
 
@@ -527,6 +584,12 @@ int qherk_impl(char uplo, char trans, int64_t N, int64_t K, double alpha, const 
   qg::Scalars<double> sc = make_scalars(al, be);
   if (!reads_a) return launch_scale(C, ldc, N, N, sc, st, tri);
   if (workspace == nullptr || (reinterpret_cast<uintptr_t>(workspace) & 255u)) return -11;
+  if (use_direct<double>()) {
+    if (workspace_bytes < sk_reserve<double>(N, N, cdiv(K, qg::kBK))) return -12;
+    // same operand views as the packed path below (conj folded into the signs)
+    return launch_mainloop_direct(A, lda, ot == 0 ? 1 : 0, ot == 0 ? 0 : 1, A, lda, ot == 0 ? 1 : 0,
+                                  ot == 0 ? 1 : 0, C, ldc, N, N, K, sc, workspace, st, tri);
+  }
   if (workspace_bytes < workspace_for<double>(N, N, K, 1)) return -12;
   // op(A) as the A operand; op(B) = op(A)^H as the B operand (same buffer):
   //   trans N: op(A)(n,k) = A(n,k) -> rows contiguous;  B~(k,n) = conj(A(n,k))
@@ -540,6 +603,7 @@ template <typename T>
 size_t ws_bytes(char transA, char transB, int64_t M, int64_t N, int64_t K, bool minimum) {
   if (op_code(transA) < 0 || op_code(transB) < 0 || M <= 0 || N <= 0 || K <= 0) return 0;
   if (use_small<T>(M, N, K)) return 0;  // the small kernel needs no workspace
+  if (use_direct<T>()) return sk_reserve<T>(M, N, cdiv(K, Geo<T>::kq));  // stream-K scratch only
   return workspace_for<T>(M, N, K, minimum ? 1 : cdiv(K, Geo<T>::kq));
 }
 
@@ -862,6 +926,7 @@ size_t qherk_workspace_bytes(char uplo, char trans, int64_t N, int64_t K) {
   const int ot = op_code(trans);
   if (!(uplo == 'L' || uplo == 'l' || uplo == 'U' || uplo == 'u') || (ot != 0 && ot != 2) || N <= 0 || K <= 0)
     return 0;
+  if (use_direct<double>()) return sk_reserve<double>(N, N, cdiv(K, qg::kBK));
   return workspace_for<double>(N, N, K, cdiv(K, qg::kBK));
 }
 
@@ -888,7 +953,7 @@ size_t qgemm_host_workspace_bytes(char transA, char transB, int64_t M, int64_t N
 int qgemm_last_launch_count(void) { return g_last_launches; }
 
 int qgemm_set_path_policy(int policy) {
-  if (policy < 0 || policy > 2) return -1;
+  if (policy < 0 || policy > 3) return -1;
   return g_path_policy.exchange(policy);
 }
 

@@ -146,8 +146,26 @@ def test_workspace_sizes(lib):
 def test_path_policy_setter(lib):
     assert lib.qgemm_set_path_policy(2) == 1
     assert lib.qgemm_set_path_policy(7) == -1  # rejected, unchanged
-    assert lib.qgemm_set_path_policy(0) == 2
+    assert lib.qgemm_set_path_policy(3) == 2
+    assert lib.qgemm_set_path_policy(0) == 3
     assert lib.qgemm_set_path_policy(1) == 0
+
+
+def test_direct_path_workspace_is_stream_k_scratch(lib):
+    """Policy 3 (direct): the pack is fused into the FP64 mainloop, so the
+    workspace is the stream-K scratch only (256 partial slots of 128 KiB + 512
+    arrival counters); FP32 keeps the packed sizes."""
+    sk = 256 * 131072 + 2048
+    for pol in (3,):
+        lib.qgemm_set_path_policy(pol)
+        assert lib.qgemm_workspace_bytes(b"N", b"H", 8192, 8192, 8192, 0) == sk
+        assert lib.qgemm_workspace_min_bytes(b"N", b"H", 8192, 8192, 8192, 0) == sk
+        assert lib.qgemm_workspace_bytes(b"N", b"H", 8192, 8192, 8192, 1) == 2 * 8192 * 8192 * 32
+        assert lib.qherk_workspace_bytes(b"L", b"N", 32768, 256) == sk
+    for pol in (0, 1):
+        lib.qgemm_set_path_policy(pol)
+        assert lib.qherk_workspace_bytes(b"L", b"N", 32768, 256) > sk
+        assert lib.qgemm_workspace_bytes(b"N", b"H", 8192, 8192, 8192, 0) > sk
 
 
 def test_small_path_needs_no_workspace(lib):

@@ -19,10 +19,11 @@ pytestmark = pytest.mark.gpu
 OPS = [(a, b) for a in "NTH" for b in "NTH"]
 QALPHA = (0.3, -1.2, 0.7, 0.25)
 QBETA = (-0.5, 0.1, -0.9, 0.4)
-PATHS = [qg.PATH_PACKED, qg.PATH_SMALL]  # pack + persistent mainloop | one-launch small kernel
+# pack launch + persistent mainloop | one-launch small kernel | pack fused into the mainloop
+PATHS = [qg.PATH_PACKED, qg.PATH_SMALL, qg.PATH_DIRECT]
 
 
-@pytest.fixture(params=PATHS, ids=["packed", "small"])
+@pytest.fixture(params=PATHS, ids=["packed", "small", "direct"])
 def path(request):
     with path_policy(request.param):
         yield request.param

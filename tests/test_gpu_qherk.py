@@ -15,6 +15,7 @@ import torch
 import oracle
 import paper_1903_05575_b200 as qg
 from synth import quat_matrix
+from tests.gpu_helpers import path_policy
 from tests.tolerance import tolerance
 
 pytestmark = pytest.mark.gpu
@@ -57,10 +58,15 @@ def test_qherk_ragged(uplo, trans, N, K):
     _case(N, K, uplo, trans, 0.75, -0.5, seed=N + K)
 
 
+@pytest.mark.parametrize("policy", [qg.PATH_PACKED, qg.PATH_DIRECT], ids=["packed", "direct"])
 @pytest.mark.parametrize("uplo", ["L", "U"])
 @pytest.mark.parametrize("trans", ["N", "H"])
-def test_qherk_exact_integer(uplo, trans):
-    _case(200, 70, uplo, trans, 2.0, 1.0, seed=3, dist="int8", exact=True)
+def test_qherk_exact_integer(uplo, trans, policy):
+    """Bitwise in exact-integer mode on both FP64 mainloop feeds (packed chunks,
+    and the direct path with conj(A) folded into the product signs)."""
+    with path_policy(policy):
+        _case(200, 70, uplo, trans, 2.0, 1.0, seed=3, dist="int8", exact=True)
+        _case(130, 256, uplo, trans, 0.75, -0.5, seed=4)
 
 
 def test_qherk_quick_returns_and_scale():

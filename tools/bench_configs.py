@@ -17,7 +17,9 @@ ap = argparse.ArgumentParser()
 ap.add_argument("--configs", default="c1,c2,c3,c3f32,c4")
 ap.add_argument("--reps", type=int, default=3)
 ap.add_argument("--c5-workspace-gb", type=float, default=16.0)
+ap.add_argument("--policy", type=int, default=0, help="qgemm_set_path_policy (0 auto, 1 packed, 2 small, 3 direct)")
 a = ap.parse_args()
+qg.set_path_policy(a.policy)
 dev = torch.device("cuda")
 g = torch.Generator(device="cuda").manual_seed(0)
 
@@ -57,7 +59,7 @@ def run(name, M, N, K, opA, opB, alpha, beta, dt=torch.float64, ld=None, ws_cap=
     qg.timing_enable(False)
     calls = reps + 1
     fl = 32.0 * M * N * K
-    out = {"config": name, "M": M, "N": N, "K": K, "ops": opA + opB,
+    out = {"config": name, "M": M, "N": N, "K": K, "ops": opA + opB, "policy": a.policy,
            "dtype": "f64" if dt == torch.float64 else "f32",
            "ms_min": tmin, "ms_med": tmed, "tflops_best": fl / tmin / 1e9,
            "tflops_med": fl / tmed / 1e9,
