@@ -39,6 +39,11 @@ FP32_NOMINAL_TFLOPS = 148 * 128 * 2 * 1.965e9 / 1e12  # 74.4 (FFMA pipe)
 # tools/microbench/tf32_peak.cu (M=128 N=256 K=8, smem-resident operands, ~1.8 s
 # back to back: 1117 TFLOP/s; profiles/r01_tf32_peak.txt) -- the nominal 1.1 PF
 TF32_PEAK_TFLOPS = 1117.0
+# cuBLAS TF32 GEMM (torch.matmul 8192^3, tools/microbench/tf32_cublas.py,
+# profiles/r01_tf32_cublas.json): burst 753.6, sustained 614.5 TFLOP/s at a
+# 1132 MHz median clock under sw_power_cap -- the library yardstick
+TF32_CUBLAS_BURST = 753.6
+TF32_CUBLAS_SUSTAINED = 614.5
 
 
 def parse():
@@ -231,6 +236,9 @@ def make_roofline(precision, achieved, main_ms, step_ms, pack_ms, steps):
             "peak": TF32_PEAK_TFLOPS, "unit": "TFLOP/s", "frac": (mma / TF32_PEAK_TFLOPS) if mma else None,
             "achieved_algorithmic": achieved,
             "frac_algorithmic": (achieved / TF32_PEAK_TFLOPS) if achieved else None,
+            "vs_cublas_tf32": {"burst": TF32_CUBLAS_BURST, "sustained": TF32_CUBLAS_SUSTAINED,
+                               "mma_rate_over_sustained": (mma / TF32_CUBLAS_SUSTAINED) if mma else None,
+                               "source": "profiles/r01_tf32_cublas.json"},
             "traffic": _traffic("f32_mainloop_bytes_per_launch"),
             "peak_source": "measured tcgen05.mma kind::tf32 loop on this pool's B200, "
                            "tools/microbench/tf32_peak.cu (profiles/r01_tf32_peak.txt); achieved "
