@@ -1,0 +1,454 @@
+// qg_runtime.cuh -- host-side runtime of libqgemm.so (internal; included once, by
+// qgemm_api.cu, inside its anonymous namespace -- one translation unit).
+//
+// SURVEY.md §8(a) row a1 "Plan / validate": per-thread launch counting and the
+// optional CUDA-event timing of every launch, BLAS-style argument validation,
+// packed-operand geometry and workspace sizing, the persistent-grid schedule,
+// the path policy (packed / direct / one-launch small kernel) and one launcher
+// per kernel.
+#pragma once
+
+thread_local int g_last_launches = 0;
+
+// ---- optional per-launch event timing (qgemm_timing_enable / _collect)
+struct TimingRec {
+  int kind;
+  cudaEvent_t e0, e1;
+};
+struct Timing {
+  bool on = false;
+  std::vector<TimingRec> recs;
+  std::vector<cudaEvent_t> pool;
+  cudaEvent_t get() {
+    if (!pool.empty()) {
+      cudaEvent_t e = pool.back();
+      pool.pop_back();
+      return e;
+    }
+    cudaEvent_t e = nullptr;
+    cudaEventCreate(&e);
+    return e;
+  }
+};
+thread_local Timing g_timing;
+
+enum Kind { kPack = 0, kMain = 1, kScale = 2, kNaive = 3, kSmall = 4, kKinds = 5 };
+
+// Bracket one launch: call before (returns the record index or -1) and after.
+int tstart(int kind, cudaStream_t st) {
+  if (!g_timing.on) return -1;
+  TimingRec r{kind, g_timing.get(), g_timing.get()};
+  cudaEventRecord(r.e0, st);
+  g_timing.recs.push_back(r);
+  return int(g_timing.recs.size()) - 1;
+}
+void tstop(int idx, cudaStream_t st) {
+  if (idx >= 0) cudaEventRecord(g_timing.recs[size_t(idx)].e1, st);
+}
+
+int op_code(char t) {
+  switch (t) {
+    case 'N': case 'n': return 0;
+    case 'T': case 't': return 1;
+    case 'H': case 'h': case 'C': case 'c': return 2;
+    default: return -1;
+  }
+}
+
+template <typename T>
+bool is_zero_q(const T *q) { return q[0] == T(0) && q[1] == T(0) && q[2] == T(0) && q[3] == T(0); }
+
+template <typename T>
+qg::Scalars<T> make_scalars(const T *alpha, const T *beta) {
+  qg::Scalars<T> s;
+  for (int c = 0; c < 4; ++c) { s.alpha[c] = alpha[c]; s.beta[c] = beta[c]; }
+  s.alpha_real = alpha[1] == T(0) && alpha[2] == T(0) && alpha[3] == T(0);
+  s.beta_real = beta[1] == T(0) && beta[2] == T(0) && beta[3] == T(0);
+  s.beta_zero = is_zero_q(beta);
+  return s;
+}
+
+int64_t cdiv(int64_t a, int64_t b) { return (a + b - 1) / b; }
+size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
+
+// Byte extent [lo, hi) touched by a stored rows x cols matrix with leading dim ld.
+template <typename T>
+void extent(const T *p, int64_t rows, int64_t cols, int64_t ld, uintptr_t &lo, uintptr_t &hi) {
+  lo = reinterpret_cast<uintptr_t>(p);
+  hi = lo + uintptr_t(4 * sizeof(T)) * uintptr_t((cols - 1) * ld + rows);
+}
+bool overlaps(uintptr_t a0, uintptr_t a1, uintptr_t b0, uintptr_t b1) { return a0 < b1 && b0 < a1; }
+
+struct Shape {
+  int oa, ob;
+  int64_t M, N, K;
+};
+
+// Packed-operand geometry per precision: rows per tile, k per tile, bytes per chunk.
+template <typename T>
+struct Geo;
+template <>
+struct Geo<double> {  // DMMA path (qg_dmma.cuh)
+  static constexpr int64_t rows = qg::kBR, kq = qg::kBK;
+  static constexpr size_t chunk = size_t(qg::kChunkElems) * sizeof(double);
+};
+#if QG_F32_TC
+template <>
+struct Geo<float> {  // tcgen05 3xTF32 path (qg_tc32.cuh): hi + lo planes
+  static constexpr int64_t rows = qg::kTcBM, kq = qg::kTcBK;
+  static constexpr size_t chunk = qg::kTcChunkBytes;
+};
+#else
+template <>
+struct Geo<float> {  // FFMA path (qg_simt_f32.cuh)
+  static constexpr int64_t rows = qg::kBR, kq = qg::kBK;
+  static constexpr size_t chunk = size_t(qg::kChunkElems) * sizeof(float);
+};
+#endif
+
+// Bytes of one K-tile column of packed panels (all MT + NT row tiles).
+template <typename T>
+size_t bytes_per_ktile(int64_t M, int64_t N) {
+  return size_t(cdiv(M, Geo<T>::rows) + cdiv(N, Geo<T>::rows)) * Geo<T>::chunk;
+}
+
+// Upper bound of the persistent grid for a panel of `ktiles` k-tiles: the
+// schedule (plan_schedule) never launches more CTAs than this.
+int64_t max_grid(int64_t tiles, int64_t ktiles) {
+  return std::max<int64_t>(1, std::min<int64_t>(qg::kMaxPersistentCTAs, std::max<int64_t>(tiles, tiles * ktiles / 2)));
+}
+
+// Stream-K scratch of the persistent FP64 mainloop: one partial-accumulator slot
+// per CTA + the arrival counters (at most 2 per CTA).
+template <typename T>
+size_t sk_slots_bytes(int64_t M, int64_t N, int64_t ktiles) {
+  const int64_t tiles = cdiv(M, qg::kBR) * cdiv(N, qg::kBR);
+  return align256(size_t(max_grid(tiles, ktiles)) * qg::kPartialBytes);
+}
+template <typename T>
+size_t sk_reserve(int64_t M, int64_t N, int64_t ktiles) {
+  if (sizeof(T) != 8) return 0;
+  return sk_slots_bytes<T>(M, N, ktiles) + align256(size_t(2 * qg::kMaxPersistentCTAs) * sizeof(int));
+}
+
+template <typename T>
+size_t workspace_for(int64_t M, int64_t N, int64_t K, int64_t ktiles) {
+  // the stream-K reserve is sized for the whole K (an upper bound for any panel),
+  // so the workspace grows linearly with the panel depth `ktiles`
+  const size_t a = size_t(cdiv(M, Geo<T>::rows)) * size_t(ktiles) * Geo<T>::chunk;
+  const size_t b = size_t(cdiv(N, Geo<T>::rows)) * size_t(ktiles) * Geo<T>::chunk;
+  return align256(a) + align256(b) + sk_reserve<T>(M, N, cdiv(K, Geo<T>::kq));
+}
+
+// Argument validation common to all entry points.  Returns 0 or -i.
+template <typename T>
+int validate(char transA, char transB, int64_t M, int64_t N, int64_t K, const T *alpha, const T *A,
+             int64_t lda, const T *B, int64_t ldb, const T *beta, const T *C, int64_t ldc, Shape &sh,
+             bool &reads_ab) {
+  sh.oa = op_code(transA);
+  sh.ob = op_code(transB);
+  if (sh.oa < 0) return -1;
+  if (sh.ob < 0) return -2;
+  if (M < 0) return -3;
+  if (N < 0) return -4;
+  if (K < 0) return -5;
+  if (alpha == nullptr) return -6;
+  const int64_t a_rows = sh.oa == 0 ? M : K, a_cols = sh.oa == 0 ? K : M;
+  const int64_t b_rows = sh.ob == 0 ? K : N, b_cols = sh.ob == 0 ? N : K;
+  if (lda < std::max<int64_t>(1, a_rows)) return -8;
+  if (ldb < std::max<int64_t>(1, b_rows)) return -10;
+  if (beta == nullptr) return -11;
+  if (ldc < std::max<int64_t>(1, M)) return -13;
+  sh.M = M; sh.N = N; sh.K = K;
+  reads_ab = false;
+  if (M == 0 || N == 0) return 0;
+  if (C == nullptr || (reinterpret_cast<uintptr_t>(C) & 15u)) return -12;
+  reads_ab = K > 0 && !is_zero_q(alpha);
+  if (reads_ab) {
+    if (A == nullptr || (reinterpret_cast<uintptr_t>(A) & 15u)) return -7;
+    if (B == nullptr || (reinterpret_cast<uintptr_t>(B) & 15u)) return -9;
+    uintptr_t c0, c1, a0, a1, b0, b1;
+    extent(C, M, N, ldc, c0, c1);
+    extent(A, a_rows, a_cols, lda, a0, a1);
+    extent(B, b_rows, b_cols, ldb, b0, b1);
+    if (overlaps(c0, c1, a0, a1) || overlaps(c0, c1, b0, b1)) return -12;
+  }
+  return 0;
+}
+
+template <typename T>
+int launch_scale(T *C, int64_t ldc, int64_t M, int64_t N, const qg::Scalars<T> &sc, cudaStream_t st,
+                 int tri = 0) {
+  const int64_t total = M * N;
+  const int threads = 256;
+  const int64_t blocks = std::min<int64_t>(cdiv(total, threads), 148 * 16);
+  { int ti = tstart(kScale, st);
+  qg::qgemm_scale_kernel<T><<<unsigned(blocks), threads, 0, st>>>(C, ldc, M, N, sc, tri);
+  tstop(ti, st); }
+  ++g_last_launches;
+  return int(cudaGetLastError());
+}
+
+// Y <- Y + beta (x) X over an M x N block (beta from sc, left product); HBM-bound.
+template <typename T>
+int launch_axpby(T *Y, int64_t ldy, const T *X, int64_t ldx, int64_t M, int64_t N, const qg::Scalars<T> &sc,
+                 cudaStream_t st) {
+  const int64_t total = M * N;
+  const int threads = 256;
+  const int64_t blocks = std::min<int64_t>(cdiv(total, threads), 148 * 16);
+  { int ti = tstart(kScale, st);
+  qg::qgemm_axpby_kernel<T><<<unsigned(blocks), threads, 0, st>>>(Y, ldy, X, ldx, M, N, sc);
+  tstop(ti, st); }
+  ++g_last_launches;
+  return int(cudaGetLastError());
+}
+
+template <typename T>
+qg::PackJob<T> pack_job(const T *X, int64_t ldx, int row_contig, int conj, int64_t R, int64_t k_begin,
+                        int64_t k_end, int64_t KT, T *out) {
+  qg::PackJob<T> j;
+  j.X = X; j.ldx = ldx; j.row_contig = row_contig; j.conj = conj; j.R = R;
+  j.k_begin = k_begin; j.k_end = k_end; j.KT = KT; j.out = out;
+  j.blocks = cdiv(R, Geo<T>::rows) * KT;
+  return j;
+}
+
+// Pack both operands' panels (rows a2 and a3) in ONE launch.
+template <typename T>
+int launch_pack2(const qg::PackJob<T> &ja, const qg::PackJob<T> &jb, cudaStream_t st) {
+  const int64_t blocks = ja.blocks + jb.blocks;
+  if (blocks <= 0) return 0;
+  if (blocks > INT32_MAX) return int(cudaErrorInvalidConfiguration);
+  int ti = tstart(kPack, st);
+  if constexpr (sizeof(T) == 8)
+    qg::pack_kernel<T, qg::FragLayout><<<unsigned(blocks), 256, 0, st>>>(ja, jb);
+  else
+#if QG_F32_TC
+    qg::pack_tc32_kernel<<<unsigned(blocks), 256, 0, st>>>(ja, jb);
+#else
+    qg::pack_kernel<T, qg::PlanarLayout><<<unsigned(blocks), 256, 0, st>>>(ja, jb);
+#endif
+  tstop(ti, st);
+  ++g_last_launches;
+  return int(cudaGetLastError());
+}
+
+// Resident CTAs of the persistent FP64 mainloop on the current device.
+// (cached per device: the query costs microseconds, which matter at c1 sizes)
+int persistent_ctas() {
+  constexpr int kMaxDev = 64;
+  static int cache[kMaxDev] = {0};
+  int dev = 0, sms = 0, per_sm = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return 0;
+  if (dev < kMaxDev && cache[dev] > 0) return cache[dev];
+  if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess) return 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, qg::qgemm_dmma_kernel<false, false, false>,
+                                                    qg::kDmmaThreads, qg::kDmmaSmemBytes) != cudaSuccess)
+    return 0;
+  const int r = std::min(qg::kMaxPersistentCTAs, sms * std::max(1, per_sm));
+  if (dev < kMaxDev) cache[dev] = r;
+  return r;
+}
+
+// Persistent "data-parallel + stream-K" schedule (see qg_dmma.cuh).
+void plan_schedule(qg::DmmaArgs &a, int resident) {
+  a.T = a.tri ? a.MT * (a.MT + 1) / 2 : a.MT * a.NT;
+  // fewer tiles than SMs: split k too, but keep >= 2 k-tiles per CTA
+  const int64_t G = std::max<int64_t>(1, std::min<int64_t>(resident, std::max<int64_t>(a.T, (a.T * a.KT) / 2)));
+  const int64_t waves = a.T / G, rem = a.T % G;
+  if (rem == 0) {
+    a.dp_tiles = a.T;
+  } else if (waves >= 2) {
+    a.dp_tiles = (waves - 1) * G;  // last full wave + remainder go stream-K
+  } else {
+    a.dp_tiles = 0;
+  }
+  a.sk_iters = (a.T - a.dp_tiles) * a.KT;
+  a.grid = G;
+}
+
+using DmmaKernel = void (*)(const qg::DmmaArgs);
+
+// The five instantiations: packed, and direct x (conj A, conj B).
+DmmaKernel dmma_kernel(bool direct, bool ca, bool cb) {
+  if (!direct) return qg::qgemm_dmma_kernel<false, false, false>;
+  if (ca) return cb ? qg::qgemm_dmma_kernel<true, true, true> : qg::qgemm_dmma_kernel<true, true, false>;
+  return cb ? qg::qgemm_dmma_kernel<true, false, true> : qg::qgemm_dmma_kernel<true, false, false>;
+}
+
+int dmma_set_attributes() {
+  constexpr int kMaxDev = 64;
+  static bool done[kMaxDev] = {false};
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return int(e);
+  if (dev < kMaxDev && done[dev]) return 0;
+  const DmmaKernel ks[5] = {dmma_kernel(false, false, false), dmma_kernel(true, false, false),
+                            dmma_kernel(true, true, false), dmma_kernel(true, false, true),
+                            dmma_kernel(true, true, true)};
+  for (DmmaKernel k : ks) {
+    e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(qg::kDmmaSmemBytes));
+    if (e != cudaSuccess) return int(e);
+  }
+  if (dev < kMaxDev) done[dev] = true;
+  return 0;
+}
+
+// Schedule + stream-K scratch + launch of a filled-in DmmaArgs (operands set).
+int launch_dmma(qg::DmmaArgs &a, DmmaKernel kernel, void *sk_scratch, cudaStream_t st) {
+  int rc = dmma_set_attributes();
+  if (rc) return rc;
+  const int resident = persistent_ctas();
+  if (resident <= 0) return int(cudaErrorInvalidConfiguration);
+  a.MT = cdiv(a.M, qg::kBR); a.NT = cdiv(a.N, qg::kBR);
+  plan_schedule(a, resident);
+  // scratch layout: [2*kMaxPersistentCTAs arrival counters][grid partial slots]
+  a.flags = reinterpret_cast<int *>(sk_scratch);
+  a.partials = reinterpret_cast<double *>(reinterpret_cast<char *>(sk_scratch) +
+                                          align256(size_t(2 * qg::kMaxPersistentCTAs) * sizeof(int)));
+  if (a.sk_iters) {
+    cudaError_t e = cudaMemsetAsync(a.flags, 0, size_t(a.T - a.dp_tiles) * sizeof(int), st);
+    if (e != cudaSuccess) return int(e);
+  }
+  { int ti = tstart(kMain, st);
+  kernel<<<unsigned(a.grid), qg::kDmmaThreads, qg::kDmmaSmemBytes, st>>>(a);
+  tstop(ti, st); }
+  ++g_last_launches;
+  return int(cudaGetLastError());
+}
+
+// Packed path: operands from packed chunks (pack_kernel).
+int launch_mainloop(const double *Ap, const double *Bp, double *C, int64_t ldc, int64_t M, int64_t N,
+                    int64_t KT, const qg::Scalars<double> &sc, void *sk_scratch, cudaStream_t st, int tri = 0) {
+  qg::DmmaArgs a{};
+  a.Ap = Ap; a.Bp = Bp; a.C = C; a.ldc = ldc; a.M = M; a.N = N; a.KT = KT; a.sc = sc; a.tri = tri;
+  return launch_dmma(a, dmma_kernel(false, false, false), sk_scratch, st);
+}
+
+// Direct path: op(A), op(B) read in place by the producer warpgroup (no pack
+// launch, no packed workspace).  rc / cj as PackSpec (row_contig, conj).
+int launch_mainloop_direct(const double *A, int64_t lda, int a_rc, int a_cj, const double *B, int64_t ldb,
+                           int b_rc, int b_cj, double *C, int64_t ldc, int64_t M, int64_t N, int64_t K,
+                           const qg::Scalars<double> &sc, void *sk_scratch, cudaStream_t st, int tri = 0) {
+  qg::DmmaArgs a{};
+  a.A = A; a.B = B; a.lda = lda; a.ldb = ldb; a.K = K; a.a_rc = a_rc; a.b_rc = b_rc;
+  a.C = C; a.ldc = ldc; a.M = M; a.N = N; a.KT = cdiv(K, qg::kBK); a.sc = sc; a.tri = tri;
+  return launch_dmma(a, dmma_kernel(true, a_cj != 0, b_cj != 0), sk_scratch, st);
+}
+
+int launch_mainloop(const float *Ap, const float *Bp, float *C, int64_t ldc, int64_t M, int64_t N, int64_t KT,
+                    const qg::Scalars<float> &sc, void * /*sk_scratch*/, cudaStream_t st,
+                    int /*tri: FP64 only*/ = 0) {
+#if QG_F32_TC
+  static bool tc_attr_set = false;
+  if (!tc_attr_set) {
+    cudaError_t e = cudaFuncSetAttribute(qg::qgemm_tc32_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         int(qg::kTcSmemBytes));
+    if (e != cudaSuccess) return int(e);
+    tc_attr_set = true;
+  }
+  qg::Tc32Args t;
+  t.Ap = Ap; t.Bp = Bp; t.C = C; t.ldc = ldc; t.M = M; t.N = N;
+  t.MT = cdiv(M, qg::kTcBM); t.NT = cdiv(N, qg::kTcBN); t.KT = KT; t.sc = sc;
+  { int ti = tstart(kMain, st);
+  qg::qgemm_tc32_kernel<<<unsigned(t.MT * t.NT), qg::kTcThreads, qg::kTcSmemBytes, st>>>(t);
+  tstop(ti, st); }
+  ++g_last_launches;
+  return int(cudaGetLastError());
+#endif
+  static bool attr_set = false;
+  if (!attr_set) {
+    cudaError_t e = cudaFuncSetAttribute(qg::qgemm_simt_f32_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         int(qg::kF32SmemBytes));
+    if (e != cudaSuccess) return int(e);
+    attr_set = true;
+  }
+  qg::F32Args a;
+  a.Ap = Ap; a.Bp = Bp; a.C = C; a.ldc = ldc; a.M = M; a.N = N;
+  a.MT = cdiv(M, qg::kBR); a.NT = cdiv(N, qg::kBR); a.KT = KT; a.sc = sc;
+  { int ti = tstart(kMain, st);
+  qg::qgemm_simt_f32_kernel<<<unsigned(a.MT * a.NT), qg::kF32Threads, qg::kF32SmemBytes, st>>>(a);
+  tstop(ti, st); }
+  ++g_last_launches;
+  return int(cudaGetLastError());
+}
+
+// ---- path choice: packed (pack launch + persistent mainloop), direct (FP64:
+// the pack fused into the mainloop's producer warpgroup) or the one-launch
+// small kernel.  0 = auto, 1 = always packed, 2 = small kernel whenever the call
+// reads A and B, 3 = direct for FP64 (packed for FP32) -- qgemm_set_path_policy;
+// the tests run every shape under each.
+std::atomic<int> g_path_policy{0};
+
+// Direct path only on request: measured 3.3% slower than pack + mainloop at c3
+// (494.7 vs 478.9 ms) and c4 (255.1 vs 247.1 ms), equal at c2;
+// its merit is memory: the workspace is the stream-K scratch only.
+template <typename T>
+bool use_direct() {
+  if (sizeof(T) != 8) return false;
+  return g_path_policy.load(std::memory_order_relaxed) == 3;
+}
+// Auto policy (crossover measured on B200 with tools/small_sweep.py):
+//  * FP64: the small kernel up to 2^24 quaternion multiply-adds (256^3), where
+//    the packed path's persistent DMMA mainloop catches up;
+//  * FP32: up to 2^25 (the tcgen05 path has a 128x128 tile and no split-K), and
+//    up to 2^28 when that path would launch fewer than 1/4 as many CTAs as
+//    there are SMs and K >= 4 max(M, N) (small M x N, long K);
+//    but not for K <= 16 with M*N >= 2^20: there the FP32 call is C-traffic
+//    bound and the packed tcgen05 epilogue streams C better.
+constexpr int64_t kSmallMaxMacs = int64_t(1) << 24;
+
+int num_sms();
+
+template <typename T>
+bool use_small(int64_t M, int64_t N, int64_t K) {
+  const int pol = g_path_policy.load(std::memory_order_relaxed);
+  if (pol == 1 || pol == 3) return false;
+  if (pol == 2) return true;
+  constexpr int64_t kCap = int64_t(1) << 28;
+  if (M > kCap || N > kCap || K > kCap) return false;  // keeps M*N*K from overflowing below
+  const double macs = double(M) * double(N) * double(K);
+  if (macs > double(kCap)) return false;
+  if (sizeof(T) == 8) return macs <= double(kSmallMaxMacs);
+  if (K <= 16 && double(M) * double(N) >= double(1 << 20)) return false;
+  if (macs <= double(2 * kSmallMaxMacs)) return true;
+  const int64_t tc_ctas = cdiv(M, 128) * cdiv(N, 128);
+  return 4 * tc_ctas < num_sms() && K >= 4 * std::max(M, N);
+}
+
+int num_sms() {
+  static int sms = 0;
+  if (sms > 0) return sms;
+  int dev = 0, v = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess ||
+      cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || v <= 0)
+    return 148;
+  sms = v;
+  return sms;
+}
+
+template <typename T>
+int launch_small(const T *A, int64_t lda, int a_rc, int a_cj, const T *B, int64_t ldb, int b_rc, int b_cj, T *C,
+                 int64_t ldc, int64_t M, int64_t N, int64_t K, const T *alpha, const T *beta, cudaStream_t st) {
+  qg::SmallArgs a;
+  a.A = A; a.B = B; a.C = C; a.lda = lda; a.ldb = ldb; a.ldc = ldc; a.M = M; a.N = N; a.K = K;
+  a.a_rc = a_rc; a.a_cj = a_cj; a.b_rc = b_rc; a.b_cj = b_cj;
+  double al[4], be[4];
+  for (int c = 0; c < 4; ++c) { al[c] = double(alpha[c]); be[c] = double(beta[c]); }
+  a.sc = make_scalars<double>(al, be);
+  // split K over more warps until the grid covers the SMs (keeping >= 2 k4 steps per warp)
+  const int64_t tm = cdiv(M, 8), tn = cdiv(N, 8), steps = cdiv(K, 4);
+  const int64_t sms = num_sms();
+  int S = 1;
+  while (S < 4 && cdiv(tm, 4 / S) * tn < sms && steps >= 4 * S) S *= 2;
+  a.S = S;
+  a.m_blocks = cdiv(tm, 4 / S);
+  const int64_t blocks = a.m_blocks * tn;
+  if (blocks > INT32_MAX) return int(cudaErrorInvalidConfiguration);
+  { int ti = tstart(kSmall, st);
+  qg::qgemm_small_kernel<T><<<unsigned(blocks), qg::kSmallThreads, 0, st>>>(a);
+  tstop(ti, st); }
+  ++g_last_launches;
+  return int(cudaGetLastError());
+}
+
