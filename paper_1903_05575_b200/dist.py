@@ -163,9 +163,10 @@ def qgemm_rowsharded_p2p(transA: str, transB: str, alpha, A_local: torch.Tensor,
             dt = A_local.dtype
             need = workspace_bytes(transA, transB, m_loc, N, K, dt)
             ws = workspace
+            cur = torch.cuda.current_stream(A_local.device)
             if ws is None or ws.numel() * ws.element_size() < need:
-                ws = get_workspace(need, A_local.device) if need else None
-            st = torch.cuda.current_stream(A_local.device).cuda_stream
+                ws = get_workspace(need, A_local.device, cur) if need else None
+            st = cur.cuda_stream
             qgemm_ptr(transA, transB, m_loc, N, K, alpha, A_local.data_ptr(), lda, B.data_ptr(),
                       B.shape[1], beta, peer.row_addr(r0), peer.ldc,
                       ws.data_ptr() if ws is not None else 0,

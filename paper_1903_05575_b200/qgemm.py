@@ -15,7 +15,9 @@ import torch
 
 from ._lib import QgemmError, load
 
-_workspaces: dict[int, torch.Tensor] = {}
+# library-managed workspaces, one per (device, stream): calls on different
+# streams may run concurrently and must not share scratch memory
+_workspaces: dict[tuple[int, int], torch.Tensor] = {}
 
 
 def _q4(x, dtype) -> ctypes.Array:
@@ -60,13 +62,21 @@ def workspace_min_bytes(transA: str, transB: str, M: int, N: int, K: int, dtype=
                                                 0 if dtype == torch.float64 else 1))
 
 
-def get_workspace(nbytes: int, device) -> torch.Tensor:
-    dev = torch.device(device).index or 0
-    ws = _workspaces.get(dev)
+def get_workspace(nbytes: int, device, stream: torch.cuda.Stream | None = None) -> torch.Tensor:
+    """Cached workspace of at least `nbytes` for calls on `stream` (default: the
+    device's current stream).  It is allocated on that stream, so the caching
+    allocator only recycles a replaced buffer after the stream's earlier work."""
+    dev = torch.device(device)
+    if dev.index is None:
+        dev = torch.device("cuda", torch.cuda.current_device())
+    st = stream or torch.cuda.current_stream(dev)
+    key = (dev.index, st.cuda_stream)
+    ws = _workspaces.get(key)
     if ws is None or ws.numel() < nbytes:
-        _workspaces.pop(dev, None)
-        ws = torch.empty(max(nbytes, 256), dtype=torch.uint8, device=device)
-        _workspaces[dev] = ws
+        _workspaces.pop(key, None)
+        with torch.cuda.stream(st):
+            ws = torch.empty(max(nbytes, 256), dtype=torch.uint8, device=dev)
+        _workspaces[key] = ws
     return ws
 
 
@@ -112,10 +122,11 @@ def _qgemm_typed(fn, name, dtype, transA, transB, alpha, A, B, beta, C, M, N, K,
     M = m0 if M is None else M
     N = n0 if N is None else N
     K = k0 if K is None else K
-    st = (stream or torch.cuda.current_stream(C.device)).cuda_stream
+    stream = stream or torch.cuda.current_stream(C.device)
+    st = stream.cuda_stream
     need = workspace_bytes(transA, transB, M, N, K, dtype)
     if workspace is None:
-        workspace = get_workspace(need, C.device) if need else None
+        workspace = get_workspace(need, C.device, stream) if need else None
     nbytes = workspace.numel() * workspace.element_size() if workspace is not None else 0
     return _call(fn, name, transA, transB, M, N, K, alpha, A, B, beta, C, dtype, workspace, nbytes,
                  st)
@@ -152,10 +163,11 @@ def qgemm_host(transA: str, transB: str, alpha, A: torch.Tensor, B: torch.Tensor
     K = k0 if K is None else K
     dev = torch.device(device) if device is not None else torch.device("cuda",
                                                                        torch.cuda.current_device())
-    st = (stream or torch.cuda.current_stream(dev)).cuda_stream
+    stream = stream or torch.cuda.current_stream(dev)
+    st = stream.cuda_stream
     need = host_workspace_bytes(transA, transB, M, N, K, dtype)
     if workspace is None:
-        workspace = get_workspace(need, dev) if need else None
+        workspace = get_workspace(need, dev, stream) if need else None
     elif not workspace.is_cuda:
         raise TypeError("workspace: must be device memory")
     nbytes = workspace.numel() * workspace.element_size() if workspace is not None else 0
@@ -241,11 +253,12 @@ def qherk(uplo: str, trans: str, alpha: float, A: torch.Tensor, beta: float, C: 
     N = C.shape[0] if N is None else N
     if K is None:
         K = A.shape[0] if trans.upper() == "N" else A.shape[1]
-    st = (stream or torch.cuda.current_stream(C.device)).cuda_stream
+    stream = stream or torch.cuda.current_stream(C.device)
+    st = stream.cuda_stream
     lib = load()
     need = int(lib.qherk_workspace_bytes(uplo.encode(), trans.encode(), N, K))
     if workspace is None:
-        workspace = get_workspace(need, C.device) if need else None
+        workspace = get_workspace(need, C.device, stream) if need else None
     nbytes = workspace.numel() * workspace.element_size() if workspace is not None else 0
     rc = lib.qherk(uplo.encode(), trans.encode(), N, K, float(alpha), _ptr(A), A.shape[1],
                    float(beta), _ptr(C), C.shape[1], _ptr(workspace), nbytes, ctypes.c_void_p(st))

@@ -225,3 +225,23 @@ def test_small_kernel_split_and_edges(M, N, K, precision):
         got = run_gpu(pr, precision)
         assert qg.last_launch_count() == 1
     assert_parity(pr, got, oracle_full(pr), precision=precision)
+
+
+def test_concurrent_streams_do_not_share_workspace():
+    """Two calls in flight on two streams with library-managed workspaces: each
+    stream gets its own scratch (a shared one would let the second call's pack
+    overwrite the first call's packed operands)."""
+    prs = [make_problem(700, 650, 900, "N", "H", QALPHA, QBETA, seed=30 + i) for i in range(2)]
+    streams = [torch.cuda.Stream(), torch.cuda.Stream()]
+    outs = []
+    for pr, s in zip(prs, streams):
+        A, B, C = to_dev(pr.A), to_dev(pr.B), to_dev(pr.C)
+        torch.cuda.synchronize()
+        with torch.cuda.stream(s):
+            qg.qgemm(pr.transA, pr.transB, pr.alpha, A, B, pr.beta, C, M=pr.M, N=pr.N, K=pr.K)
+        outs.append((A, B, C))
+    torch.cuda.synchronize()
+    ws = {id(qg.get_workspace(1, "cuda", s)) for s in streams}
+    assert len(ws) == 2
+    for pr, (_, _, C) in zip(prs, outs):
+        assert_parity(pr, C.cpu().numpy(), oracle_full(pr))
