@@ -33,6 +33,7 @@
 // producer warp walks the same work list, so the ring keeps streaming across
 // tile boundaries while the consumers run an epilogue.
 #pragma once
+#include <cuda.h>  // CUtensorMap (the TMA feed)
 #include "qg_pack.cuh"
 
 namespace qg {
@@ -46,16 +47,27 @@ constexpr int kDmmaThreads = (kConsumerWarps + 4) * 32;
 constexpr int kProducerRegs = 40;
 constexpr int kConsumerRegs = 232;
 constexpr int kGroupM = 8;  // rasterisation: 8 M-tiles share each B panel in flight
-constexpr size_t kDmmaSmemBytes = size_t(kStages) * 2 * kChunkElems * sizeof(double) + 2 * kStages * 8;
+// ring + barriers + 1 KB so the ring can start on a 1024-byte boundary
+constexpr size_t kDmmaSmemBytes = size_t(kStages) * 2 * kChunkElems * sizeof(double) + 2 * kStages * 8 + 1024;
+// (the 32-byte swizzle repeats every 256 bytes; the ring starts 1024-aligned)
+
+// How the ring is fed (kernel template parameter).
+// (a third feed -- all 128 producer threads de-interleaving with 16-byte
+// cp.async -- was measured 3% slower than packed at c3 and removed)
+enum Feed : int {
+  kFeedPacked = 0,  // bulk copies of pre-packed chunks (pack_kernel)
+  kFeedTma = 2,     // TMA tensor-map tiles of the interleaved storage, 32-byte swizzle
+};
 constexpr int kAccPerThread = 64;                      // doubles
 constexpr size_t kPartialBytes = size_t(kConsumerThreads) * kAccPerThread * sizeof(double);  // 128 KiB
 constexpr int kMaxPersistentCTAs = 256;
 
-struct DmmaArgs {
+struct alignas(64) DmmaArgs {
+  CUtensorMap tmA, tmB;  // TMA feed: 3-D maps (component, view row, k) or (component, k, view row)
   const double *Ap;  // packed path: packed A panel, MT x KT chunks
   const double *Bp;  // packed path: packed B panel, NT x KT chunks
-  // direct path (pack fused into the producer): op(A) / op(B) read in place as
-  // R x K views -- X~(r, k) at X + 4(r + k ldx) (rc = 1) or X + 4(k + r ldx) (rc = 0)
+  // TMA feed: op(A) / op(B) read in place as R x K views -- X~(r, k) at
+  // X + 4(r + k ldx) (rc = 1) or X + 4(k + r ldx) (rc = 0)
   const double *A, *B;
   int64_t lda, ldb, K;
   int a_rc, b_rc;
@@ -161,7 +173,7 @@ __device__ __forceinline__ int ld_acquire(const int *p) {
 struct Producer {
   WorkIter it;
   int64_t kt, ke;
-  int64_t mt, nt;  // direct path: tile coordinates of the current unit
+  int64_t mt, nt;  // TMA feed: tile coordinates of the current unit
   const double *a_src, *b_src;
   int slot;
   uint32_t phase;
@@ -192,49 +204,30 @@ __device__ __forceinline__ bool produce_next(Producer &p, const DmmaArgs &args, 
   return true;
 }
 
-// ---- direct path: the pack (rows a2/a3) fused into the producer warpgroup ----
-// 16-byte cp.async (LDGSTS, no registers staged) global -> shared; src-size 0
-// zero-fills rows r >= R and k >= K (the zero padding of Alg. 2).
-__device__ __forceinline__ void cp_async16_zfill(void *smem, const void *gmem, bool valid) {
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(smem_u32(smem)), "l"(gmem),
-               "r"(valid ? 16 : 0)
-               : "memory");
-}
-// The mbarrier's next arrival by this thread fires when its prior cp.asyncs land.
-__device__ __forceinline__ void cp_async_mbar_arrive_noinc(uint64_t *bar) {
-  asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];\n" ::"r"(smem_u32(bar)) : "memory");
-}
-
-constexpr int kProducerThreads = 128;
-
-// One 64-row x 16-k tile of an interleaved operand view into a FragLayout chunk:
-// 2048 16-byte halves (components 0-1 | 2-3) of 1024 quaternions, 16 per
-// producer thread.  The 16-byte slot of (r, k, half) sits in bank group
-// ((r & 1) << 2 | (k & 3)) of the chunk, so a warp's 32 copies must span 2 row
-// parities x 4 k residues to be conflict-free (4 lanes per group = the minimum
-// 4 wavefronts); within that, lanes run along the stored contiguous axis:
-//   rows contiguous (rc): 4 k x 4 consecutive rows x 2 halves -> 4 runs of 128 B
-//   k contiguous:         2 rows x 8 consecutive k x 2 halves -> 2 runs of 256 B
-__device__ __forceinline__ void load_tile_direct(double *dst, const double *X, int64_t ldx, int rc, int64_t r0,
-                                                 int64_t R, int64_t k0, int64_t K, int ptid) {
-#pragma unroll 4
-  for (int it = 0; it < (kBR * kBK * 2) / kProducerThreads; ++it) {
-    const int q = ptid + kProducerThreads * it;
-    const int pp = q & 1;
-    int r, k;
-    if (rc) { k = ((q >> 9) << 2) | ((q >> 1) & 3); r = (((q >> 5) & 15) << 2) | ((q >> 3) & 3); }
-    else    { k = (((q >> 5) & 1) << 3) | ((q >> 1) & 7); r = ((q >> 6) << 1) | ((q >> 4) & 1); }
-    const int64_t gr = r0 + r, gk = k0 + k;
-    const bool valid = gr < R && gk < K;
-    const double *src = valid ? X + 4 * (rc ? gr + gk * ldx : gk + gr * ldx) + 2 * pp : X;
-    const int off = ((((k >> 2) * 8 + (r >> 3)) * 2 + pp) * 32 + (((r & 7) << 2) | (k & 3))) * 2;
-    cp_async16_zfill(dst + off, src, valid);
-  }
+// ---- TMA feed: one lane loads each operand tile straight from the user's
+// interleaved storage with a 3-D tensor map (component, row, k) or (component,
+// k, row); out-of-range rows / k are zero-filled by the TMA unit (the padding
+// of Alg. 2).  The tile lands in smem in storage order, 32-byte
+// swizzled (one quaternion = one 32-byte swizzle row; the 128-byte mode would
+// pad every 32-byte row to 128 bytes): element (r, k, c) of the 64 x 16 tile at
+//   lin = ((k*64 + r)*4 + c)*8   (rows contiguous)   or   ((r*16 + k)*4 + c)*8
+//   swz = lin ^ (((lin >> 7) & 1) << 4)   (16-byte half swapped on odd 128 B)
+// so the de-interleave into DMMA fragments is done by the consumers' addresses.
+// Rows contiguous: a warp's fragment loads (8 rows x 4 k) hit every bank group
+// exactly 4 times (conflict-free); k contiguous: 2-way conflicts.  Verified
+// element by element by tools/microbench/tma_probe.cu.
+__device__ __forceinline__ void tma_load_3d(void *dst, const CUtensorMap *tm, int c0, int c1, int c2,
+                                            uint64_t *bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], "
+      "[%5];\n" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(tm)), "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(bar))
+      : "memory");
 }
 
-// Direct-path fill, executed by all 128 producer threads.
-__device__ __forceinline__ bool produce_next_direct(Producer &p, const DmmaArgs &args, double *sA, double *sB,
-                                                    uint64_t *full, uint64_t *empty, int ptid) {
+__device__ __forceinline__ bool produce_next_tma(Producer &p, const DmmaArgs &args, double *sA, double *sB,
+                                                 uint64_t *full, uint64_t *empty) {
+  constexpr uint32_t kBytes = kChunkElems * sizeof(double);
   while (p.kt >= p.ke) {
     Unit u;
     if (!p.it.next(args, u)) return false;
@@ -243,23 +236,60 @@ __device__ __forceinline__ bool produce_next_direct(Producer &p, const DmmaArgs 
     p.ke = u.ke;
   }
   if (p.fills >= kStages) mbar_wait(&empty[p.slot], p.phase ^ 1u);
-  const int64_t k0 = p.kt * kBK;
-  load_tile_direct(sA + p.slot * kChunkElems, args.A, args.lda, args.a_rc, p.mt * kBR, args.M, k0, args.K, ptid);
-  load_tile_direct(sB + p.slot * kChunkElems, args.B, args.ldb, args.b_rc, p.nt * kBR, args.N, k0, args.K, ptid);
-  cp_async_mbar_arrive_noinc(&full[p.slot]);
+  mbar_arrive_expect_tx(&full[p.slot], 2 * kBytes);
+  const int k0 = int(p.kt * kBK), ra = int(p.mt * kBR), rb = int(p.nt * kBR);
+  if (args.a_rc) tma_load_3d(sA + p.slot * kChunkElems, &args.tmA, 0, ra, k0, &full[p.slot]);
+  else           tma_load_3d(sA + p.slot * kChunkElems, &args.tmA, 0, k0, ra, &full[p.slot]);
+  if (args.b_rc) tma_load_3d(sB + p.slot * kChunkElems, &args.tmB, 0, rb, k0, &full[p.slot]);
+  else           tma_load_3d(sB + p.slot * kChunkElems, &args.tmB, 0, k0, rb, &full[p.slot]);
   if (++p.slot == kStages) { p.slot = 0; p.phase ^= 1u; }
   ++p.kt;
   ++p.fills;
   return true;
 }
 
-// kDirect: operands read in place by the producer warpgroup (CA / CB: op H on
+// Byte offset of the 16-byte pair (components 2pp, 2pp+1) of (r, k) in a TMA tile.
+__device__ __forceinline__ uint32_t tma_tile_off(int rc, int r, int k, int pp) {
+  const uint32_t lin = rc ? uint32_t(((k * kBR + r) * 4 + 2 * pp) * 8) : uint32_t(((r * kBK + k) * 4 + 2 * pp) * 8);
+  return lin ^ (((lin >> 7) & 1u) << 4);
+}
+
+// Per-lane part of the fragment offsets in a TMA tile.  A lane reads rows
+// r0 + 8i (r0 = its first row) at k = 4ks + kl.  Rows contiguous: the swizzle
+// bit (address bit 7) is bit 2 of the row, the same for every i, so
+//   off = r0*32 + kl*2048 + ks*8192 + i*256 + ((16 pp) ^ x),   x = 16 * bit2(r0);
+// k contiguous: the swizzle bit is bit 2 of k = bit 0 of ks, so
+//   off = r0*512 + kl*32 + i*4096 + ks*128 + 16 (pp ^ (ks & 1)).
+// Everything but `base` / `x` is a compile-time constant of the unrolled loops.
+struct TmaLane {
+  uint32_t base, x;
+  int rc;
+};
+__device__ __forceinline__ TmaLane tma_lane(int rc, int r0, int kl) {
+  TmaLane t;
+  t.rc = rc;
+  t.base = rc ? uint32_t(r0 * 32 + kl * 2048) : uint32_t(r0 * 512 + kl * 32);
+  t.x = rc ? uint32_t(((r0 >> 2) & 1) << 4) : 0u;
+  return t;
+}
+__device__ __forceinline__ uint32_t tma_frag_off(const TmaLane &t, int ks, int i, int pp) {
+  return t.rc ? t.base + uint32_t(ks * 8192 + i * 256) + (uint32_t(pp << 4) ^ t.x)
+              : t.base + uint32_t(i * 4096 + ks * 128 + ((pp ^ (ks & 1)) << 4));
+}
+
+// kFeed: kFeedPacked (conj applied by the pack kernel; CA = CB = false), or a
+// direct feed reading op(A)/op(B) in place (CA / CB: op H on
 // A / B, folded into the sign of each of the 16 products: conj flips the sign
 // of components 1-3); otherwise from packed chunks (conj applied by
 // the pack kernel; CA = CB = false).
-template <bool kDirect, bool CA, bool CB>
-__global__ void __launch_bounds__(kDmmaThreads, 1) qgemm_dmma_kernel(const DmmaArgs args) {
-  extern __shared__ __align__(128) unsigned char smem_raw[];
+// kRC (TMA feed only): bit 0 = op(A) rows contiguous, bit 1 = op(B) rows
+// contiguous -- compile-time, so the fragment offsets fold into immediates.
+template <int kFeed, bool CA, bool CB, int kRC = 0>
+__global__ void __launch_bounds__(kDmmaThreads, 1) qgemm_dmma_kernel(const __grid_constant__ DmmaArgs args) {
+  extern __shared__ __align__(128) unsigned char smem_dyn[];
+  // (offset arithmetic on the shared array, not an integer round trip, so the
+  // compiler keeps shared-space loads: LDS, not generic LD)
+  unsigned char *smem_raw = smem_dyn + ((1024u - (smem_u32(smem_dyn) & 1023u)) & 1023u);
   double *sA = reinterpret_cast<double *>(smem_raw);
   double *sB = sA + kStages * kChunkElems;
   uint64_t *full = reinterpret_cast<uint64_t *>(sB + kStages * kChunkElems);
@@ -274,7 +304,7 @@ __global__ void __launch_bounds__(kDmmaThreads, 1) qgemm_dmma_kernel(const DmmaA
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < kStages; ++s) {
-      mbar_init(&full[s], kDirect ? kProducerThreads : 1);
+      mbar_init(&full[s], 1);
       mbar_init(&empty[s], kConsumerWarps);
     }
     fence_mbar_init();
@@ -282,9 +312,8 @@ __global__ void __launch_bounds__(kDmmaThreads, 1) qgemm_dmma_kernel(const DmmaA
   __syncthreads();
 
   // ---------------- producer warpgroup, kStages fills ahead ----------------
-  // Packed path: one lane streams packed chunks with bulk copies.  Direct path:
-  // all 128 threads de-interleave op(A)/op(B) tiles into the same chunk layout
-  // with cp.async.  setmaxnreg hands the warpgroup's registers to the consumers.
+  // One lane streams packed chunks (bulk copies) or interleaved tiles (TMA);
+  // setmaxnreg hands the warpgroup's registers to the consumers.
   Producer prod;
   prod.it = make_iter(args, sp);
   prod.kt = 0;
@@ -294,10 +323,10 @@ __global__ void __launch_bounds__(kDmmaThreads, 1) qgemm_dmma_kernel(const DmmaA
   prod.fills = 0;
   if (warp >= kConsumerWarps) {
     asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;\n" ::"n"(kProducerRegs));
-    if constexpr (kDirect) {
-      const int ptid = threadIdx.x - kConsumerThreads;
-      while (produce_next_direct(prod, args, sA, sB, full, empty, ptid)) {
-      }
+    if constexpr (kFeed == kFeedTma) {
+      if (warp == kConsumerWarps && lane == 0)
+        while (produce_next_tma(prod, args, sA, sB, full, empty)) {
+        }
     } else {
       if (warp == kConsumerWarps && lane == 0)
         while (produce_next(prod, args, sA, sB, full, empty)) {
@@ -310,6 +339,8 @@ __global__ void __launch_bounds__(kDmmaThreads, 1) qgemm_dmma_kernel(const DmmaA
   // ---------------- consumers ----------------
   const int wm = warp & 1;   // 32-row half of the CTA tile
   const int wn = warp >> 1;  // 16-column quarter
+  [[maybe_unused]] const TmaLane ta = tma_lane(kRC & 1, wm * 32 + (lane >> 2), lane & 3);
+  [[maybe_unused]] const TmaLane tb = tma_lane((kRC >> 1) & 1, wn * 16 + (lane >> 2), lane & 3);
   const int tid = threadIdx.x;
   int slot = 0;
   uint32_t phase = 0;
@@ -346,6 +377,8 @@ __global__ void __launch_bounds__(kDmmaThreads, 1) qgemm_dmma_kernel(const DmmaA
       mbar_wait(&full[slot], phase);
       const double2 *a2 = reinterpret_cast<const double2 *>(sA + slot * kChunkElems);
       const double2 *b2 = reinterpret_cast<const double2 *>(sB + slot * kChunkElems);
+      [[maybe_unused]] const unsigned char *a8 = reinterpret_cast<const unsigned char *>(a2);
+      [[maybe_unused]] const unsigned char *b8 = reinterpret_cast<const unsigned char *>(b2);
 #pragma unroll
       for (int ks = 0; ks < kBK / 4; ++ks) {
         double af[4][4], bf[2][4], bn[2][4];
@@ -353,7 +386,11 @@ __global__ void __launch_bounds__(kDmmaThreads, 1) qgemm_dmma_kernel(const DmmaA
         for (int ii = 0; ii < 4; ++ii)
 #pragma unroll
           for (int pp = 0; pp < 2; ++pp) {
-            double2 v = a2[((ks * 8 + wm * 4 + ii) * 2 + pp) * 32 + lane];
+            double2 v;
+            if constexpr (kFeed == kFeedTma)
+              v = *reinterpret_cast<const double2 *>(a8 + tma_frag_off(ta, ks, ii, pp));
+            else
+              v = a2[((ks * 8 + wm * 4 + ii) * 2 + pp) * 32 + lane];
             af[ii][2 * pp] = v.x;
             af[ii][2 * pp + 1] = v.y;
           }
@@ -361,7 +398,11 @@ __global__ void __launch_bounds__(kDmmaThreads, 1) qgemm_dmma_kernel(const DmmaA
         for (int jj = 0; jj < 2; ++jj)
 #pragma unroll
           for (int pp = 0; pp < 2; ++pp) {
-            double2 v = b2[((ks * 8 + wn * 2 + jj) * 2 + pp) * 32 + lane];
+            double2 v;
+            if constexpr (kFeed == kFeedTma)
+              v = *reinterpret_cast<const double2 *>(b8 + tma_frag_off(tb, ks, jj, pp));
+            else
+              v = b2[((ks * 8 + wn * 2 + jj) * 2 + pp) * 32 + lane];
             bf[jj][2 * pp] = v.x;
             bf[jj][2 * pp + 1] = v.y;
           }

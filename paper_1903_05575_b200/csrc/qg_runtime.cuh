@@ -242,7 +242,7 @@ int persistent_ctas() {
   if (cudaGetDevice(&dev) != cudaSuccess) return 0;
   if (dev < kMaxDev && cache[dev] > 0) return cache[dev];
   if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess) return 0;
-  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, qg::qgemm_dmma_kernel<false, false, false>,
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, qg::qgemm_dmma_kernel<qg::kFeedPacked, false, false>,
                                                     qg::kDmmaThreads, qg::kDmmaSmemBytes) != cudaSuccess)
     return 0;
   const int r = std::min(qg::kMaxPersistentCTAs, sms * std::max(1, per_sm));
@@ -267,13 +267,27 @@ void plan_schedule(qg::DmmaArgs &a, int resident) {
   a.grid = G;
 }
 
-using DmmaKernel = void (*)(const qg::DmmaArgs);
+using DmmaKernel = void (*)(const qg::DmmaArgs);  // (__grid_constant__ is not part of the type)
 
-// The five instantiations: packed, and direct x (conj A, conj B).
-DmmaKernel dmma_kernel(bool direct, bool ca, bool cb) {
-  if (!direct) return qg::qgemm_dmma_kernel<false, false, false>;
-  if (ca) return cb ? qg::qgemm_dmma_kernel<true, true, true> : qg::qgemm_dmma_kernel<true, true, false>;
-  return cb ? qg::qgemm_dmma_kernel<true, false, true> : qg::qgemm_dmma_kernel<true, false, false>;
+// Instantiations: packed; TMA x the op pairs (rows-contiguous and conj flags of
+// A and B are compile-time there).
+template <bool CA, bool CB>
+DmmaKernel tma_kernel(int arc, int brc) {
+  using namespace qg;
+  switch (arc | (brc << 1)) {
+    case 0: return qgemm_dmma_kernel<kFeedTma, CA, CB, 0>;
+    case 1: return qgemm_dmma_kernel<kFeedTma, CA, CB, 1>;
+    case 2: return qgemm_dmma_kernel<kFeedTma, CA, CB, 2>;
+    default: return qgemm_dmma_kernel<kFeedTma, CA, CB, 3>;
+  }
+}
+DmmaKernel dmma_kernel(int feed, bool ca, bool cb, int arc = 0, int brc = 0) {
+  using namespace qg;
+  if (feed == kFeedPacked) return qgemm_dmma_kernel<kFeedPacked, false, false>;
+  // op H implies k-contiguous storage for A (rows of op(A) = columns of A) and
+  // rows-contiguous for B, so conj A => arc = 0 and conj B => brc = 1
+  if (ca) return cb ? tma_kernel<true, true>(0, 1) : tma_kernel<true, false>(0, brc);
+  return cb ? tma_kernel<false, true>(arc, 1) : tma_kernel<false, false>(arc, brc);
 }
 
 int dmma_set_attributes() {
@@ -283,15 +297,51 @@ int dmma_set_attributes() {
   cudaError_t e = cudaGetDevice(&dev);
   if (e != cudaSuccess) return int(e);
   if (dev < kMaxDev && done[dev]) return 0;
-  const DmmaKernel ks[5] = {dmma_kernel(false, false, false), dmma_kernel(true, false, false),
-                            dmma_kernel(true, true, false), dmma_kernel(true, false, true),
-                            dmma_kernel(true, true, true)};
-  for (DmmaKernel k : ks) {
-    e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(qg::kDmmaSmemBytes));
-    if (e != cudaSuccess) return int(e);
-  }
+  for (int feed : {int(qg::kFeedPacked), int(qg::kFeedTma)})
+    for (int c = 0; c < 16; ++c) {
+      const bool ca = c & 1, cb = c & 2;
+      const int arc = (c >> 2) & 1, brc = (c >> 3) & 1;
+      if (feed == qg::kFeedPacked && c) continue;
+      if ((ca && arc) || (cb && !brc)) continue;  // no such op
+      e = cudaFuncSetAttribute(dmma_kernel(feed, ca, cb, arc, brc), cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               int(qg::kDmmaSmemBytes));
+      if (e != cudaSuccess) return int(e);
+    }
   if (dev < kMaxDev) done[dev] = true;
   return 0;
+}
+
+// cuTensorMapEncodeTiled through the runtime's driver entry point (the library
+// does not link libcuda).
+using EncodeTiledFn = CUresult (*)(CUtensorMap *, CUtensorMapDataType, cuuint32_t, void *, const cuuint64_t *,
+                                   const cuuint64_t *, const cuuint32_t *, const cuuint32_t *, CUtensorMapInterleave,
+                                   CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+EncodeTiledFn encode_tiled() {
+  static EncodeTiledFn fn = nullptr;
+  if (fn) return fn;
+  void *p = nullptr;
+  cudaDriverEntryPointQueryResult q;
+  if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) != cudaSuccess ||
+      q != cudaDriverEntryPointSuccess)
+    return nullptr;
+  fn = reinterpret_cast<EncodeTiledFn>(p);
+  return fn;
+}
+
+// 3-D map of an R x K operand view over interleaved FP64 storage (ld in
+// quaternions): (component, row, k) when rows are contiguous, else
+// (component, k, row); box = one 64-row x 16-k tile, 32-byte swizzle.
+int encode_view(CUtensorMap *tm, const double *X, int64_t ldx, int rc, int64_t R, int64_t K) {
+  EncodeTiledFn fn = encode_tiled();
+  if (!fn) return int(cudaErrorNotSupported);
+  const cuuint64_t dims[3] = {4, cuuint64_t(rc ? R : K), cuuint64_t(rc ? K : R)};
+  const cuuint64_t strides[2] = {32, cuuint64_t(32) * cuuint64_t(ldx)};
+  const cuuint32_t box[3] = {4, cuuint32_t(rc ? qg::kBR : qg::kBK), cuuint32_t(rc ? qg::kBK : qg::kBR)};
+  const cuuint32_t estr[3] = {1, 1, 1};
+  const CUresult r = fn(tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, const_cast<double *>(X), dims, strides, box, estr,
+                        CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_32B,
+                        CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS ? 0 : int(cudaErrorInvalidValue);
 }
 
 // Schedule + stream-K scratch + launch of a filled-in DmmaArgs (operands set).
@@ -322,18 +372,24 @@ int launch_mainloop(const double *Ap, const double *Bp, double *C, int64_t ldc, 
                     int64_t KT, const qg::Scalars<double> &sc, void *sk_scratch, cudaStream_t st, int tri = 0) {
   qg::DmmaArgs a{};
   a.Ap = Ap; a.Bp = Bp; a.C = C; a.ldc = ldc; a.M = M; a.N = N; a.KT = KT; a.sc = sc; a.tri = tri;
-  return launch_dmma(a, dmma_kernel(false, false, false), sk_scratch, st);
+  return launch_dmma(a, dmma_kernel(qg::kFeedPacked, false, false), sk_scratch, st);
 }
 
 // Direct path: op(A), op(B) read in place by the producer warpgroup (no pack
 // launch, no packed workspace).  rc / cj as PackSpec (row_contig, conj).
-int launch_mainloop_direct(const double *A, int64_t lda, int a_rc, int a_cj, const double *B, int64_t ldb,
-                           int b_rc, int b_cj, double *C, int64_t ldc, int64_t M, int64_t N, int64_t K,
-                           const qg::Scalars<double> &sc, void *sk_scratch, cudaStream_t st, int tri = 0) {
+int launch_mainloop_direct(int feed, const double *A, int64_t lda, int a_rc, int a_cj, const double *B,
+                           int64_t ldb, int b_rc, int b_cj, double *C, int64_t ldc, int64_t M, int64_t N,
+                           int64_t K, const qg::Scalars<double> &sc, void *sk_scratch, cudaStream_t st,
+                           int tri = 0) {
   qg::DmmaArgs a{};
   a.A = A; a.B = B; a.lda = lda; a.ldb = ldb; a.K = K; a.a_rc = a_rc; a.b_rc = b_rc;
   a.C = C; a.ldc = ldc; a.M = M; a.N = N; a.KT = cdiv(K, qg::kBK); a.sc = sc; a.tri = tri;
-  return launch_dmma(a, dmma_kernel(true, a_cj != 0, b_cj != 0), sk_scratch, st);
+  if (feed == qg::kFeedTma) {
+    int rc = encode_view(&a.tmA, A, lda, a_rc, M, K);
+    if (!rc) rc = encode_view(&a.tmB, B, ldb, b_rc, N, K);
+    if (rc) return rc;
+  }
+  return launch_dmma(a, dmma_kernel(feed, a_cj != 0, b_cj != 0, a_rc, b_rc), sk_scratch, st);
 }
 
 int launch_mainloop(const float *Ap, const float *Bp, float *C, int64_t ldc, int64_t M, int64_t N, int64_t KT,
@@ -374,20 +430,30 @@ int launch_mainloop(const float *Ap, const float *Bp, float *C, int64_t ldc, int
 }
 
 // ---- path choice: packed (pack launch + persistent mainloop), direct (FP64:
-// the pack fused into the mainloop's producer warpgroup) or the one-launch
-// small kernel.  0 = auto, 1 = always packed, 2 = small kernel whenever the call
-// reads A and B, 3 = direct for FP64 (packed for FP32) -- qgemm_set_path_policy;
-// the tests run every shape under each.
+// the persistent mainloop fed by TMA from the interleaved storage, no pack) or
+// the one-launch small kernel.  0 = auto, 1 = always packed, 2 = small kernel
+// whenever the call reads A and B, 3 = direct for FP64 (packed for FP32) --
+// qgemm_set_path_policy; the tests run every shape under each.
 std::atomic<int> g_path_policy{0};
 
-// Direct path only on request: measured 3.3% slower than pack + mainloop at c3
-// (494.7 vs 478.9 ms) and c4 (255.1 vs 247.1 ms), equal at c2;
-// its merit is memory: the workspace is the stream-K scratch only.
+// Direct (TMA-fed) FP64 mainloop vs pack launch + mainloop, from the sweep in
+// profiles/r01i_feed_sweep.jsonl (tools/feed_sweep.py): the TMA tile lands in
+// storage order, so op(A) = A (rows contiguous) costs 4-way shared-memory bank
+// conflicts on the A fragments (2-way when k is contiguous) -- the pack it
+// saves is worth more than that only for small problems.  Auto: direct when
+// op(A) is T/H, or when M*N*K <= 2^30; packed for K < 512 (c4: K = 256) and
+// large op(A) = N problems (c3, c5).
 template <typename T>
-bool use_direct() {
-  if (sizeof(T) != 8) return false;
-  return g_path_policy.load(std::memory_order_relaxed) == 3;
+int direct_feed(int opA, int64_t M, int64_t N, int64_t K) {
+  if (sizeof(T) != 8) return 0;
+  const int pol = g_path_policy.load(std::memory_order_relaxed);
+  if (pol == 3) return qg::kFeedTma;
+  if (pol != 0) return 0;
+  if (K < 512) return 0;
+  if (opA != 0) return qg::kFeedTma;
+  return double(M) * double(N) * double(K) <= double(int64_t(1) << 30) ? qg::kFeedTma : 0;
 }
+
 // Auto policy (crossover measured on B200 with tools/small_sweep.py):
 //  * FP64: the small kernel up to 2^24 quaternion multiply-adds (256^3), where
 //    the packed path's persistent DMMA mainloop catches up;

@@ -277,8 +277,8 @@ PATH_AUTO, PATH_PACKED, PATH_SMALL, PATH_DIRECT = 0, 1, 2, 3
 
 def set_path_policy(policy: int) -> int:
     """0 auto, 1 always packed (pack launch + mainloop), 2 always the one-launch
-    small kernel, 3 direct (FP64: pack fused into the mainloop producer; FP32
-    packed); returns the old one."""
+    small kernel, 3 direct (FP64: persistent mainloop fed by TMA straight from
+    the interleaved storage, no pack; FP32 packed); returns the old one."""
     old = int(load().qgemm_set_path_policy(int(policy)))
     if old < 0:
         raise ValueError(f"invalid path policy {policy}")

@@ -146,6 +146,7 @@ def test_workspace_sizes(lib):
 def test_path_policy_setter(lib):
     assert lib.qgemm_set_path_policy(2) == 1
     assert lib.qgemm_set_path_policy(7) == -1  # rejected, unchanged
+    assert lib.qgemm_set_path_policy(4) == -1
     assert lib.qgemm_set_path_policy(3) == 2
     assert lib.qgemm_set_path_policy(0) == 3
     assert lib.qgemm_set_path_policy(1) == 0
@@ -162,10 +163,13 @@ def test_direct_path_workspace_is_stream_k_scratch(lib):
         assert lib.qgemm_workspace_min_bytes(b"N", b"H", 8192, 8192, 8192, 0) == sk
         assert lib.qgemm_workspace_bytes(b"N", b"H", 8192, 8192, 8192, 1) == 2 * 8192 * 8192 * 32
         assert lib.qherk_workspace_bytes(b"L", b"N", 32768, 256) == sk
-    for pol in (0, 1):
+    for pol in (0, 1):  # auto: packed for c4's K = 256 and for c3 (op(A) = N, large)
         lib.qgemm_set_path_policy(pol)
         assert lib.qherk_workspace_bytes(b"L", b"N", 32768, 256) > sk
         assert lib.qgemm_workspace_bytes(b"N", b"H", 8192, 8192, 8192, 0) > sk
+    lib.qgemm_set_path_policy(0)  # auto: direct for op(A) = T/H, and for N up to 1024^3
+    assert lib.qgemm_workspace_bytes(b"T", b"N", 8192, 8192, 8192, 0) == sk
+    assert lib.qgemm_workspace_bytes(b"N", b"N", 1024, 1024, 1024, 0) == sk
 
 
 def test_small_path_needs_no_workspace(lib):

@@ -19,7 +19,7 @@ pytestmark = pytest.mark.gpu
 OPS = [(a, b) for a in "NTH" for b in "NTH"]
 QALPHA = (0.3, -1.2, 0.7, 0.25)
 QBETA = (-0.5, 0.1, -0.9, 0.4)
-# pack launch + persistent mainloop | one-launch small kernel | pack fused into the mainloop
+# pack launch + persistent mainloop | one-launch small kernel | TMA-fed mainloop (no pack)
 PATHS = [qg.PATH_PACKED, qg.PATH_SMALL, qg.PATH_DIRECT]
 
 

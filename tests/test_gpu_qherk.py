@@ -63,7 +63,7 @@ def test_qherk_ragged(uplo, trans, N, K):
 @pytest.mark.parametrize("trans", ["N", "H"])
 def test_qherk_exact_integer(uplo, trans, policy):
     """Bitwise in exact-integer mode on both FP64 mainloop feeds (packed chunks,
-    and the direct path with conj(A) folded into the product signs)."""
+    and TMA tiles of the interleaved A with conj folded into the product signs)."""
     with path_policy(policy):
         _case(200, 70, uplo, trans, 2.0, 1.0, seed=3, dist="int8", exact=True)
         _case(130, 256, uplo, trans, 0.75, -0.5, seed=4)
