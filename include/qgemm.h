@@ -186,11 +186,11 @@ int qgemm_naive(char transA, char transB, int64_t M, int64_t N, int64_t K,
 
 /* Path policy (process-wide): 0 = auto (default), 1 = always the packed
  * path (pack launch + persistent mainloop), 2 = always the one-launch small
- * kernel, 3 = direct (FP64: the pack fused into the persistent mainloop's
- * producer warpgroup, which de-interleaves op(A)/op(B) tiles straight into
- * shared memory -- one launch, workspace = stream-K scratch only, ~3% slower
- * than packed at c3; FP32 calls take the packed path).  Auto = small kernel
- * below the crossover, else packed.
+ * kernel, 3 = direct (FP64: the persistent mainloop fed by TMA straight from
+ * the interleaved storage -- one launch, no pack, workspace = stream-K scratch
+ * only; FP32 calls take the packed path).  Auto = small kernel below the
+ * crossover; above it FP64 takes the direct path when op(A) is T/H or
+ * M*N*K <= 2^30 (with K >= 512), else packed; FP32 packed.
  * Returns the previous policy, or -1 (policy unchanged) for other values.
  * For tests and benchmarks; the result is correct under every policy. */
 int qgemm_set_path_policy(int policy);
