@@ -212,10 +212,12 @@ __device__ __forceinline__ bool produce_next(Producer &p, const DmmaArgs &args, 
 // pad every 32-byte row to 128 bytes): element (r, k, c) of the 64 x 16 tile at
 //   lin = ((k*64 + r)*4 + c)*8   (rows contiguous)   or   ((r*16 + k)*4 + c)*8
 //   swz = lin ^ (((lin >> 7) & 1) << 4)   (16-byte half swapped on odd 128 B)
-// so the de-interleave into DMMA fragments is done by the consumers' addresses.
-// Rows contiguous: a warp's fragment loads (8 rows x 4 k) hit every bank group
-// exactly 4 times (conflict-free); k contiguous: 2-way conflicts.  Verified
-// element by element by tools/microbench/tma_probe.cu.
+// so the de-interleave into DMMA fragments is done by the consumers' addresses
+// (layout verified element by element by tools/microbench/tma_probe.cu).  A
+// 128-bit shared load is served a quarter-warp (8 lanes = 2 rows x 4 k) at a
+// time, and those 8 lanes hit only 2 bank groups when rows are contiguous
+// (4-way conflicts; ncu) or 4 when k is contiguous (2-way) -- the price of not
+// packing, which auto pays only where the sweep shows it wins.
 __device__ __forceinline__ void tma_load_3d(void *dst, const CUtensorMap *tm, int c0, int c1, int c2,
                                             uint64_t *bar) {
   asm volatile(
