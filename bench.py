@@ -198,7 +198,7 @@ def run_reference(args):
             "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": tot_t / args.steps * 1e3, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": "c3: QGEMM M=N=K=8192 opA=N opB=H alpha=beta=1 N(0,1) (sampled)",
+            "config": {"workload": f"c3: QGEMM M=N=K={n} opA=N opB=H alpha=beta=1 N(0,1) (sampled)",
                        "parallelism": "cpu"},
             "cpu_baseline": {"value": value, "unit": "TFLOP/s", "cores": oracle.max_threads(),
                              "kind": "oracle", "sample": sample},
