@@ -37,7 +37,8 @@ def build(force: bool = False, verbose: bool = False) -> str:
     if not force and not needs_build():
         return SO
     tmp = SO + f".tmp{os.getpid()}"
-    cmd = [NVCC, *ARCH, *FLAGS, "-o", tmp, *sources()]
+    extra = os.environ.get("QG_NVCC_EXTRA", "").split()  # tuning experiments only
+    cmd = [NVCC, *ARCH, *FLAGS, *extra, "-o", tmp, *sources()]
     res = subprocess.run(cmd, capture_output=True, text=True)
     if res.returncode != 0:
         sys.stderr.write(res.stdout + res.stderr)

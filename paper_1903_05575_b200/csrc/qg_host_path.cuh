@@ -1,6 +1,19 @@
 // qg_host_path.cuh -- qgemm_host / qgemm_host_f32 (internal; included once, by
 // qgemm_api.cu, inside its anonymous namespace, after qg_runtime.cuh).
 #pragma once
+
+// Chunking of the host-streamed path (tuned on c3): K chunks of
+// ~K/QG_HOST_KC_DIV, the first one QG_HOST_KC0_DIV times shorter; the last
+// chunk in QG_HOST_PANELS column panels.
+#ifndef QG_HOST_KC_DIV
+#define QG_HOST_KC_DIV 8
+#endif
+#ifndef QG_HOST_KC0_DIV
+#define QG_HOST_KC0_DIV 4
+#endif
+#ifndef QG_HOST_PANELS
+#define QG_HOST_PANELS 16
+#endif
 // ---------------------------------------------------------------------------
 // Host-resident operands (qgemm_host / qgemm_host_f32): the end-to-end call.
 //
@@ -39,10 +52,11 @@ HostPlan<T> host_plan(int64_t M, int64_t N, int64_t K) {
   } else {
     // chunks of ~K/8 (256..2048); the first one a quarter of that, so the first
     // mainloop waits only for a small upload
-    h.Kc = std::min<int64_t>(cdiv(K, kq) * kq, std::max<int64_t>(256, std::min<int64_t>(2048, cdiv(cdiv(K, 8), kq) * kq)));
-    h.Kc0 = std::min<int64_t>(h.Kc, std::max<int64_t>(kq, cdiv(cdiv(h.Kc, 4), kq) * kq));
+    h.Kc = std::min<int64_t>(cdiv(K, kq) * kq,
+                             std::max<int64_t>(256, std::min<int64_t>(2048, cdiv(cdiv(K, QG_HOST_KC_DIV), kq) * kq)));
+    h.Kc0 = std::min<int64_t>(h.Kc, std::max<int64_t>(kq, cdiv(cdiv(h.Kc, QG_HOST_KC0_DIV), kq) * kq));
     h.Q = K <= h.Kc0 ? 1 : 1 + cdiv(K - h.Kc0, h.Kc);
-    h.Nj = std::min<int64_t>(cdiv(N, rows) * rows, std::max<int64_t>(256, cdiv(cdiv(N, 16), rows) * rows));
+    h.Nj = std::min<int64_t>(cdiv(N, rows) * rows, std::max<int64_t>(256, cdiv(cdiv(N, QG_HOST_PANELS), rows) * rows));
     h.P = cdiv(N, h.Nj);
   }
   const size_t csz = align256(size_t(M) * size_t(N) * qb);  // C, compact ld = M
