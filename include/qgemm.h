@@ -58,14 +58,17 @@
  * size of a single K-panel (qgemm_workspace_min_bytes); the call then loops over
  * K-panels (Alg. 2 kappa loop), applying beta on the first panel and
  * accumulating onto C afterwards.  Smaller -> -15.
- * The workspace must be 256-byte aligned (-14 otherwise).
+ * The workspace must be 256-byte aligned (-14 otherwise).  When an FP64 call
+ * takes the direct path (no pack; see the path policy below), both functions
+ * return the stream-K scratch size only (~33 MB) and no K-panel loop runs.
  *
  * Small problems: below the library's measured
  * crossover (FP64: M*N*K <= 2^24 quaternion multiply-adds; FP32: <= 2^25, or
  * small M x N with long K), qgemm/qgemm_f32 run ONE kernel that reads
  * op(A)/op(B) in place (no pack, no workspace);
  * qgemm_workspace_bytes() then returns 0 and `workspace` may be NULL.  The
- * choice is a pure function of (M, N, K) and the path policy below.
+ * path is a pure function of (transA, M, N, K), the precision and the path
+ * policy below, so qgemm_workspace_bytes() with the same arguments sizes it.
  */
 #ifndef QGEMM_B200_H
 #define QGEMM_B200_H
@@ -109,12 +112,15 @@ size_t qgemm_workspace_min_bytes(char transA, char transB, int64_t M, int64_t N,
  *             but serialises) or device memory: every access is a
  *             cudaMemcpy2DAsync with cudaMemcpyDefault;
  *   workspace DEVICE memory of at least qgemm_host_workspace_bytes() bytes,
- *             256-byte aligned; it holds the device copy of C plus
- *             double-buffered staging and packed chunks of op(A)/op(B).
+ *             256-byte aligned; it holds the device accumulator of C, a device
+ *             copy of the caller's C, and double-buffered staging and packed
+ *             chunks of op(A)/op(B).
  * The call streams K in chunks (Alg. 2's kappa loop) host->device
  * on a private upload stream while `stream` packs and multiplies the previous
- * chunk; the first and last chunks run per column panel of C so that C's
- * upload and download overlap the mainloop too.  It returns
+ * chunk.  The accumulator starts from beta = 0, the caller's C is uploaded
+ * behind the first chunks and folded in (C += beta (x) C_old) before the last
+ * chunk, which runs per column panel so each finished panel downloads while
+ * the next computes.  It returns
  * after enqueueing; the result is in the caller's C once `stream` has
  * synchronised (host buffers must stay valid until then).  The library creates
  * two streams and a few events per call and releases them once their work
