@@ -245,3 +245,30 @@ def test_concurrent_streams_do_not_share_workspace():
     assert len(ws) == 2
     for pr, (_, _, C) in zip(prs, outs):
         assert_parity(pr, C.cpu().numpy(), oracle_full(pr))
+
+
+# ---------------------------------------------------------------- randomized sweep
+def _random_cases(n, seed=2026):
+    rng = np.random.default_rng(seed)
+    sizes = [1, 3, 8, 16, 31, 64, 65, 100, 128, 129, 200, 257, 300, 513]
+    for _ in range(n):
+        M, N, K = (int(rng.choice(sizes)) for _ in range(3))
+        opA, opB = str(rng.choice(list("NTH"))), str(rng.choice(list("NTH")))
+        pads = rng.integers(0, 4, 3)
+        alpha = tuple(rng.uniform(-1, 1, 4)) if rng.random() < 0.5 else (float(rng.uniform(-2, 2)),)
+        beta = (0.0,) if rng.random() < 0.2 else tuple(rng.uniform(-1, 1, 4))
+        yield M, N, K, opA, opB, pads, alpha, beta
+
+
+@pytest.mark.parametrize("case", list(_random_cases(24)))
+@pytest.mark.parametrize("precision", ["f64", "f32"])
+def test_randomized_shapes_ops_scalars(case, precision, path):
+    """Random shapes (ragged, skinny, K = 1), op pairs, ld padding, real or
+    quaternion alpha and beta (beta = 0 with a NaN C) under every path policy."""
+    M, N, K, opA, opB, pads, alpha, beta = case
+    lda = (M if opA == "N" else K) + int(pads[0])
+    ldb = (K if opB == "N" else N) + int(pads[1])
+    pr = make_problem(M, N, K, opA, opB, alpha, beta, seed=M * 7 + N * 3 + K, dist="normal",
+                      lda=lda, ldb=ldb, ldc=M + int(pads[2]),
+                      c_init="nan" if beta == (0.0,) else "random")
+    assert_parity(pr, run_gpu(pr, precision), oracle_full(pr), precision=precision)
