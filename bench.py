@@ -65,6 +65,7 @@ def parse():
                          "memory (p2p, fused) or gathered with NCCL send/recv after compute")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-f32", action="store_true", help="skip the FP32 (tcgen05) variant")
+    ap.add_argument("--no-configs", action="store_true", help="skip the c1/c2/c4 context lines")
     return ap.parse_args()
 
 
@@ -282,6 +283,80 @@ def measure_f32_variant(A, B, C, n, warmup, steps):
                                                       steps), "clocks": clocks}
 
 
+def measure_other_configs(warmup):
+    """BASELINE.json configs 1, 2 and 4 at their own sizes (context lines next to
+    the c3 headline; c5's 103 GB single-GPU run takes ~31 s per call and is left
+    to tools/bench_configs.py).  Device-resident inputs, CUDA events; c1 and c2
+    are also replayed from a CUDA graph (host ctypes time off the timeline)."""
+    import torch
+    import paper_1903_05575_b200 as qg
+    dev = torch.device("cuda")
+    g = torch.Generator(device="cuda").manual_seed(0)
+
+    def rnd(cols, ld):
+        return 2 * torch.rand((cols, ld, 4), dtype=torch.float64, device=dev, generator=g) - 1
+
+    def timed(fn, reps):
+        for _ in range(max(1, warmup)):
+            fn()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(reps):
+            fn()
+        e1.record()
+        torch.cuda.synchronize()
+        return e0.elapsed_time(e1) / reps
+
+    def graphed(fn, reps=200):
+        s = torch.cuda.Stream()
+        s.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(s):
+            fn()
+            gr = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(gr, stream=s):
+                fn()
+        torch.cuda.current_stream().wait_stream(s)
+        torch.cuda.synchronize()
+        return timed(gr.replay, reps)
+
+    out = {}
+    A, B, C = rnd(64, 64), rnd(64, 64), rnd(64, 64)
+    qg.qgemm("N", "N", 1.0, A, B, 0.0, C)
+    launches = qg.last_launch_count()
+    ms = graphed(lambda: qg.qgemm("N", "N", 1.0, A, B, 0.0, C))
+    out["c1"] = {"workload": "c1: 64^3 N/N alpha=1 beta=0", "us_per_call": ms * 1e3,
+                 "tflops": 32.0 * 64 ** 3 / (ms * 1e-3) / 1e12, "launches_per_call": launches,
+                 "timing": "CUDA-graph replay"}
+    n, ld = 1024, 1040
+    per_op = {}
+    for oa in "NTH":
+        for ob in "NTH":
+            A, B, C = rnd(n, ld), rnd(n, ld), rnd(n, ld)
+            call = (lambda oa=oa, ob=ob, A=A, B=B, C=C:
+                    qg.qgemm(oa, ob, 0.75, A, B, -0.5, C, M=n, N=n, K=n))
+            ms = timed(call, 10)
+            per_op[oa + ob] = {"ms": ms, "tflops": 32.0 * n ** 3 / (ms * 1e-3) / 1e12,
+                               "graph_ms": graphed(call, 20)}
+    out["c2"] = {"workload": "c2: 1024^3, all 9 (opA, opB), alpha=0.75 beta=-0.5, ld=1040",
+                 "per_op": per_op,
+                 "tflops_min": min(v["tflops"] for v in per_op.values()),
+                 "tflops_max": max(v["tflops"] for v in per_op.values())}
+    del A, B, C
+    n, K = 32768, 256
+    A = rnd(K, n)
+    C = rnd(n, n)
+    ms = timed(lambda: qg.qgemm("N", "H", 1.0, A, A, 1.0, C, M=n, N=n, K=K), 2)
+    ms_herk = timed(lambda: qg.qherk("L", "N", 1.0, A, 1.0, C), 2)
+    fl = 32.0 * n * n * K
+    out["c4"] = {"workload": "c4: M=N=32768 K=256, C <- A A^H + C (B == A)", "qgemm_ms": ms,
+                 "qgemm_tflops": fl / (ms * 1e-3) / 1e12, "qherk_lower_ms": ms_herk,
+                 "qherk_speedup": ms / ms_herk}
+    del A, C
+    torch.cuda.empty_cache()
+    return out
+
+
 # ------------------------------------------------------------------ our arm
 def run_ours(args):
     import torch
@@ -436,6 +511,9 @@ def run_ours(args):
     variants = None
     if world == 1 and args.precision == "f64" and not args.no_f32:
         variants = {"c3_fp32": measure_f32_variant(A, B, C, n, args.warmup, args.steps)}
+    if world == 1 and args.precision == "f64" and not args.no_configs and n == 8192:
+        variants = dict(variants or {})
+        variants["other_configs"] = measure_other_configs(args.warmup)
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
