@@ -360,9 +360,29 @@ int launch_dmma(qg::DmmaArgs &a, DmmaKernel kernel, void *sk_scratch, cudaStream
     cudaError_t e = cudaMemsetAsync(a.flags, 0, size_t(a.T - a.dp_tiles) * sizeof(int), st);
     if (e != cudaSuccess) return int(e);
   }
+  // Stream-K owners wait for the CTAs holding the rest of their tile, which is
+  // only safe if the whole grid is resident at once.  A cooperative launch
+  // guarantees that even when other kernels share the GPU (e.g. qgemm calls on
+  // two streams at once, each with a persistent grid that fills every SM);
+  // data-parallel-only schedules have no inter-CTA waits and launch plainly.
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(unsigned(a.grid));
+  cfg.blockDim = dim3(qg::kDmmaThreads);
+  cfg.dynamicSmemBytes = qg::kDmmaSmemBytes;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeCooperative;
+  attr[0].val.cooperative = 1;
+  cfg.attrs = attr;
+#ifndef QG_COOP
+#define QG_COOP 1  // (0: plain launch, for the regression check in DESIGN.md §6)
+#endif
+  cfg.numAttrs = (QG_COOP && a.sk_iters) ? 1 : 0;
+  cudaError_t le;
   { int ti = tstart(kMain, st);
-  kernel<<<unsigned(a.grid), qg::kDmmaThreads, qg::kDmmaSmemBytes, st>>>(a);
+  le = cudaLaunchKernelEx(&cfg, kernel, a);
   tstop(ti, st); }
+  if (le != cudaSuccess) return int(le);
   ++g_last_launches;
   return int(cudaGetLastError());
 }

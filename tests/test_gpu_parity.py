@@ -272,3 +272,48 @@ def test_randomized_shapes_ops_scalars(case, precision, path):
                       lda=lda, ldb=ldb, ldc=M + int(pads[2]),
                       c_init="nan" if beta == (0.0,) else "random")
     assert_parity(pr, run_gpu(pr, precision), oracle_full(pr), precision=precision)
+
+
+_CONCURRENT = r"""
+import sys, torch
+sys.path.insert(0, {root!r})
+import paper_1903_05575_b200 as qg
+torch.manual_seed(0)
+n = 1024  # 256 tiles on 148 SMs: an all-stream-K schedule (owners wait for contributors)
+streams = [torch.cuda.Stream() for _ in range(3)]
+ops = [("N", "N"), ("T", "H"), ("H", "N")]
+data = []
+for (oa, ob), s in zip(ops, streams):
+    A = torch.randn(n, n, 4, dtype=torch.float64, device="cuda")
+    B = torch.randn(n, n, 4, dtype=torch.float64, device="cuda")
+    C = torch.zeros(n, n, 4, dtype=torch.float64, device="cuda")
+    data.append((oa, ob, A, B, C, s))
+torch.cuda.synchronize()
+ref = []
+for oa, ob, A, B, C, s in data:  # serial reference run
+    C.zero_()
+    qg.qgemm(oa, ob, 1.0, A, B, 0.0, C)
+    ref.append(C.clone())
+torch.cuda.synchronize()
+for it in range(20):  # the three persistent grids in flight together
+    for oa, ob, A, B, C, s in data:
+        with torch.cuda.stream(s):
+            qg.qgemm(oa, ob, 1.0, A, B, 0.0, C)
+torch.cuda.synchronize()
+for (oa, ob, A, B, C, s), r in zip(data, ref):
+    assert torch.equal(C, r), (oa, ob)  # same tile config -> bitwise
+print("OK")
+"""
+
+
+def test_concurrent_persistent_grids_no_deadlock():
+    """Three stream-K grids that each want every SM, in flight at once on three
+    streams: the cooperative launch keeps each grid co-resident, so stream-K
+    owners never wait for a contributor that cannot be scheduled (run in a
+    subprocess with a timeout so a regression fails instead of hanging)."""
+    import subprocess
+    import sys as _sys
+    root = __import__("os").path.dirname(__import__("os").path.dirname(__import__("os").path.abspath(__file__)))
+    res = subprocess.run([_sys.executable, "-c", _CONCURRENT.format(root=root)], capture_output=True, text=True,
+                         timeout=180)
+    assert res.returncode == 0 and "OK" in res.stdout, res.stdout + res.stderr[-3000:]
