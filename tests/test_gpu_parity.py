@@ -317,3 +317,28 @@ def test_concurrent_persistent_grids_no_deadlock():
     res = subprocess.run([_sys.executable, "-c", _CONCURRENT.format(root=root)], capture_output=True, text=True,
                          timeout=180)
     assert res.returncode == 0 and "OK" in res.stdout, res.stdout + res.stderr[-3000:]
+
+
+@pytest.mark.parametrize("M,N,K,opA,opB", [(64, 64, 64, "N", "N"), (700, 650, 900, "N", "H"),
+                                           (1024, 1024, 1024, "T", "N"), (300, 200, 100, "H", "T")])
+def test_cuda_graph_capture_and_replay(M, N, K, opA, opB, path):
+    """Every path (small kernel, pack + persistent mainloop with its flag memset
+    and cooperative stream-K launch, TMA-fed direct) can be captured once and
+    replayed: the replays reproduce the eager result bitwise."""
+    pr = make_problem(M, N, K, opA, opB, QALPHA, 0.0, seed=40, c_init="zero")
+    A, B = to_dev(pr.A), to_dev(pr.B)
+    C_eager, C_graph = to_dev(pr.C), to_dev(pr.C)
+    ws = torch.empty(max(256, qg.workspace_bytes(opA, opB, M, N, K)), dtype=torch.uint8, device="cuda")
+    qg.qgemm(opA, opB, QALPHA, A, B, 0.0, C_eager, M=M, N=N, K=K, workspace=ws)
+    torch.cuda.synchronize()
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g, stream=s):
+        qg.qgemm(opA, opB, QALPHA, A, B, 0.0, C_graph, M=M, N=N, K=K, workspace=ws, stream=s)
+    for _ in range(3):
+        C_graph.fill_(float("nan"))
+        g.replay()
+        torch.cuda.synchronize()
+        assert torch.equal(C_graph, C_eager)
+    assert_parity(pr, C_eager.cpu().numpy(), oracle_full(pr))
