@@ -38,7 +38,8 @@
  *
  * Quick returns (BLAS convention; reading R4):
  *     M == 0 or N == 0      -> returns 0, enqueues nothing;
- *     alpha == 0 or K == 0  -> C <- beta * C (one elementwise kernel);
+ *     alpha == 0 or K == 0  -> C <- beta * C (one elementwise kernel; nothing
+ *                              is enqueued when beta == 1);
  *     beta == 0             -> C is overwritten and never read (NaN in C does
  *                              not propagate; reading R3).
  *

@@ -55,7 +55,10 @@ int qgemm_impl(char transA, char transB, int64_t M, int64_t N, int64_t K, const 
   if (M == 0 || N == 0) return 0;
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   qg::Scalars<T> sc = make_scalars(alpha, beta);
-  if (!reads_ab) return launch_scale(C, ldc, M, N, sc, st);
+  if (!reads_ab) {  // C <- beta C; nothing to do for beta = 1 (BLAS quick return)
+    if (sc.beta_real && sc.beta[0] == T(1)) return 0;
+    return launch_scale(C, ldc, M, N, sc, st);
+  }
   PackSpec<T> pa{A, lda, sh.oa == 0 ? 1 : 0, sh.oa == 2 ? 1 : 0};
   PackSpec<T> pb{B, ldb, sh.ob == 0 ? 0 : 1, sh.ob == 2 ? 1 : 0};
   if (use_small<T>(M, N, K))  // one launch, no workspace (NEXT item 4)

@@ -125,8 +125,9 @@ def test_quick_returns_and_beta_paths(path):
     assert qg.last_launch_count() == 0
     qg.qgemm("N", "N", 1, A, B, 1, C, M=5, N=0, K=3)
     assert torch.equal(C, C0)
-    # alpha = 0, beta = 1 -> bitwise unchanged
+    # alpha = 0, beta = 1 -> bitwise unchanged, nothing enqueued
     qg.qgemm("N", "N", 0, A, B, 1, C, M=5, N=4, K=3)
+    assert qg.last_launch_count() == 0
     torch.cuda.synchronize()
     assert torch.equal(C, C0)
     # K = 0 -> beta C (quaternion beta, left)
