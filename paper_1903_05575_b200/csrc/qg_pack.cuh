@@ -23,7 +23,7 @@
 //       value = X~(8i + lane/4, 4ks + lane%4) component 2pp+e; a lane's 16-byte
 //       word holds its A (or B) fragments of two components, for both operands
 //       (the m8n8k4 A fragment is A[lane/4][lane%4], B fragment B[lane%4][lane/4]).
-//   PlanarLayout (FP32 SIMT): [k 16][c 4][r 64]: component planes, r fastest.
+// (the FP32 tcgen05 path has its own pack, qg_tc32.cuh pack_tc32_kernel)
 #pragma once
 #include <type_traits>
 #include "qg_common.cuh"
@@ -40,9 +40,6 @@ struct FragLayout {
     int ks = k >> 2, i = r >> 3, lane = ((r & 7) << 2) | (k & 3), pp = c >> 1, e = c & 1;
     return ((((ks * 8 + i) * 2 + pp) * 32 + lane) << 1) | e;
   }
-};
-struct PlanarLayout {
-  __device__ __forceinline__ static int offset(int r, int k, int c) { return (k * 4 + c) * kBR + r; }
 };
 
 // One operand panel to pack: rows [0, R) x k in [k_begin, k_end) of op(X), as
@@ -103,12 +100,9 @@ __global__ void __launch_bounds__(256) pack_kernel(const PackJob<T> ja, const Pa
 #pragma unroll
     for (int e = 0; e < 2; ++e) {
       int off = 2 * w + e, r, k, c;
-      if constexpr (std::is_same<Layout, FragLayout>::value) {
-        int ee = off & 1, lane = (off >> 1) & 31, pp = (off >> 6) & 1, i = (off >> 7) & 7, ks = off >> 10;
-        r = i * 8 + (lane >> 2); k = ks * 4 + (lane & 3); c = pp * 2 + ee;
-      } else {
-        r = off % kBR; c = (off / kBR) & 3; k = off / (kBR * 4);
-      }
+      static_assert(std::is_same<Layout, FragLayout>::value, "FP64 packs use the fragment layout");
+      int ee = off & 1, lane = (off >> 1) & 31, pp = (off >> 6) & 1, i = (off >> 7) & 7, ks = off >> 10;
+      r = i * 8 + (lane >> 2); k = ks * 4 + (lane & 3); c = pp * 2 + ee;
       pair[e] = tile[k * kPitch + r * 4 + c];
     }
     if constexpr (sizeof(T) == 8) {

@@ -92,19 +92,11 @@ struct Geo<double> {  // DMMA path (qg_dmma.cuh)
   static constexpr int64_t rows = qg::kBR, kq = qg::kBK;
   static constexpr size_t chunk = size_t(qg::kChunkElems) * sizeof(double);
 };
-#if QG_F32_TC
 template <>
 struct Geo<float> {  // tcgen05 3xTF32 path (qg_tc32.cuh): hi + lo planes
   static constexpr int64_t rows = qg::kTcBM, kq = qg::kTcBK;
   static constexpr size_t chunk = qg::kTcChunkBytes;
 };
-#else
-template <>
-struct Geo<float> {  // FFMA path (qg_simt_f32.cuh)
-  static constexpr int64_t rows = qg::kBR, kq = qg::kBK;
-  static constexpr size_t chunk = size_t(qg::kChunkElems) * sizeof(float);
-};
-#endif
 
 // Bytes of one K-tile column of packed panels (all MT + NT row tiles).
 template <typename T>
@@ -223,11 +215,7 @@ int launch_pack2(const qg::PackJob<T> &ja, const qg::PackJob<T> &jb, cudaStream_
   if constexpr (sizeof(T) == 8)
     qg::pack_kernel<T, qg::FragLayout><<<unsigned(blocks), 256, 0, st>>>(ja, jb);
   else
-#if QG_F32_TC
     qg::pack_tc32_kernel<<<unsigned(blocks), 256, 0, st>>>(ja, jb);
-#else
-    qg::pack_kernel<T, qg::PlanarLayout><<<unsigned(blocks), 256, 0, st>>>(ja, jb);
-#endif
   tstop(ti, st);
   ++g_last_launches;
   return int(cudaGetLastError());
@@ -415,35 +403,21 @@ int launch_mainloop_direct(int feed, const double *A, int64_t lda, int a_rc, int
 int launch_mainloop(const float *Ap, const float *Bp, float *C, int64_t ldc, int64_t M, int64_t N, int64_t KT,
                     const qg::Scalars<float> &sc, void * /*sk_scratch*/, cudaStream_t st,
                     int /*tri: FP64 only*/ = 0) {
-#if QG_F32_TC
-  static bool tc_attr_set = false;
-  if (!tc_attr_set) {
+  constexpr int kMaxDev = 64;
+  static bool attr_set[kMaxDev] = {false};
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return int(cudaErrorInvalidDevice);
+  if (dev >= kMaxDev || !attr_set[dev]) {
     cudaError_t e = cudaFuncSetAttribute(qg::qgemm_tc32_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          int(qg::kTcSmemBytes));
     if (e != cudaSuccess) return int(e);
-    tc_attr_set = true;
+    if (dev < kMaxDev) attr_set[dev] = true;
   }
   qg::Tc32Args t;
   t.Ap = Ap; t.Bp = Bp; t.C = C; t.ldc = ldc; t.M = M; t.N = N;
   t.MT = cdiv(M, qg::kTcBM); t.NT = cdiv(N, qg::kTcBN); t.KT = KT; t.sc = sc;
   { int ti = tstart(kMain, st);
   qg::qgemm_tc32_kernel<<<unsigned(t.MT * t.NT), qg::kTcThreads, qg::kTcSmemBytes, st>>>(t);
-  tstop(ti, st); }
-  ++g_last_launches;
-  return int(cudaGetLastError());
-#endif
-  static bool attr_set = false;
-  if (!attr_set) {
-    cudaError_t e = cudaFuncSetAttribute(qg::qgemm_simt_f32_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         int(qg::kF32SmemBytes));
-    if (e != cudaSuccess) return int(e);
-    attr_set = true;
-  }
-  qg::F32Args a;
-  a.Ap = Ap; a.Bp = Bp; a.C = C; a.ldc = ldc; a.M = M; a.N = N;
-  a.MT = cdiv(M, qg::kBR); a.NT = cdiv(N, qg::kBR); a.KT = KT; a.sc = sc;
-  { int ti = tstart(kMain, st);
-  qg::qgemm_simt_f32_kernel<<<unsigned(a.MT * a.NT), qg::kF32Threads, qg::kF32SmemBytes, st>>>(a);
   tstop(ti, st); }
   ++g_last_launches;
   return int(cudaGetLastError());

@@ -19,13 +19,8 @@
 #include "qg_pack.cuh"
 #include "qg_simple.cuh"
 #include "qg_small.cuh"
-#include "qg_simt_f32.cuh"
 #include "qg_tc32.cuh"
 
-// FP32 mainloop: 1 = tcgen05 3xTF32 (qg_tc32.cuh), 0 = FFMA (qg_simt_f32.cuh)
-#ifndef QG_F32_TC
-#define QG_F32_TC 1
-#endif
 
 namespace {
 
@@ -283,11 +278,8 @@ int qgemm_timing_collect(double ms[5], int counts[5]) {
 }
 
 const char *qgemm_version(void) {
-#if QG_F32_TC
-  return "qgemm-b200 0.2 (sm_100a; FP64 DMMA.8x8x4 persistent stream-K; FP32 tcgen05 3xTF32)";
-#else
-  return "qgemm-b200 0.2 (sm_100a; FP64 DMMA.8x8x4 persistent stream-K; FP32 FFMA)";
-#endif
+  return "qgemm-b200 0.3 (sm_100a; FP64 DMMA.8x8x4 persistent stream-K, packed or TMA-fed; "
+         "FP32 tcgen05 3xTF32; one-launch small kernel)";
 }
 
 }  // extern "C"
