@@ -34,7 +34,6 @@ METRIC = "QGEMM FP64 TFLOP/s (32 flops/quat-MAC) and % of FP64 peak at 1/2/4/8 G
 # tools/microbench/fp64_pipes.cu (profiles/r01_fp64_pipes.txt), clocks at 1965 MHz.
 FP64_DMMA_PEAK_TFLOPS = 37.0
 FP64_NOMINAL_TFLOPS = 148 * 64 * 2 * 1.965e9 / 1e12  # 37.22
-FP32_NOMINAL_TFLOPS = 148 * 128 * 2 * 1.965e9 / 1e12  # 74.4 (FFMA pipe)
 # tcgen05.mma kind::tf32 peak MEASURED on this pool's B200 with the MMA loop of
 # tools/microbench/tf32_peak.cu (M=128 N=256 K=8, smem-resident operands, ~1.8 s
 # back to back: 1117 TFLOP/s; profiles/r01_tf32_peak.txt) -- the nominal 1.1 PF
