@@ -46,7 +46,10 @@ constexpr int kConsumerThreads = kConsumerWarps * 32;
 constexpr int kDmmaThreads = (kConsumerWarps + 4) * 32;
 constexpr int kProducerRegs = 40;
 constexpr int kConsumerRegs = 232;
-constexpr int kGroupM = 8;  // rasterisation: 8 M-tiles share each B panel in flight
+#ifndef QG_GROUP_M
+#define QG_GROUP_M 8
+#endif
+constexpr int kGroupM = QG_GROUP_M;  // rasterisation: M-tiles per group (L2 reuse of panels)
 // ring + barriers + 1 KB so the ring can start on a 1024-byte boundary
 constexpr size_t kDmmaSmemBytes = size_t(kStages) * 2 * kChunkElems * sizeof(double) + 2 * kStages * 8 + 1024;
 // (the 32-byte swizzle repeats every 256 bytes; the ring starts 1024-aligned)
