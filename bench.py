@@ -394,7 +394,20 @@ def run_ours(args):
         if rank == 0:
             for r in range(world):
                 C_full[:, r * n:(r + 1) * n, :].copy_(C)
-        peer = PeerC(C_full)
+        # every rank must agree: if any rank cannot map root's C (no P2P / IPC
+        # between these GPUs), all of them take the NCCL-gather collection
+        ok = 1
+        try:
+            peer = PeerC(C_full)
+        except Exception as exc:  # noqa: BLE001 -- reported, then the collective decision below
+            print(f"[rank {rank}] peer mapping of root's C failed ({exc}); using the NCCL gather",
+                  file=sys.stderr)
+            peer, ok = None, 0
+        flag = torch.tensor([ok], dtype=torch.int32, device=dev)
+        dist.all_reduce(flag, op=dist.ReduceOp.MIN)
+        if int(flag.item()) == 0 and peer is not None:
+            peer.close()
+            peer = None
     ws = qg.get_workspace(qg.workspace_bytes("N", "H", n, n, n, dt), dev)
     stream = torch.cuda.current_stream(dev)
 
