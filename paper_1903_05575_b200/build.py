@@ -49,5 +49,16 @@ def build(force: bool = False, verbose: bool = False) -> str:
     return SO
 
 
+def build_variant(out: str, extra_flags: list[str]) -> str:
+    """Build the same sources with extra nvcc flags into `out` (tests only:
+    e.g. the negative-control library, -DQG_NEGATIVE_CONTROL)."""
+    cmd = [NVCC, *ARCH, *FLAGS, *extra_flags, "-o", out, *sources()]
+    res = subprocess.run(cmd, capture_output=True, text=True)
+    if res.returncode != 0:
+        sys.stderr.write(res.stdout + res.stderr)
+        raise RuntimeError(f"nvcc failed building {out}")
+    return out
+
+
 if __name__ == "__main__":
     print(build(force="--force" in sys.argv, verbose=True))

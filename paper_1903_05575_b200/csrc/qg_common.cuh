@@ -15,7 +15,13 @@
 namespace qg {
 
 // bit (4p+s) set <=> eps(p,s) = -1
-constexpr unsigned kNegMask = (1u << 5) | (1u << 7) | (1u << 9) | (1u << 10) | (1u << 14) | (1u << 15);
+constexpr unsigned kNegMask = (1u << 5) | (1u << 7) | (1u << 9) | (1u << 10) | (1u << 14) | (1u << 15)
+#ifdef QG_NEGATIVE_CONTROL
+    // test-suite sensitivity check only: eps(1,2) flipped, so
+    // every kernel computes a wrong Hamilton product; never in libqgemm.so
+    ^ (1u << 6)
+#endif
+    ;
 
 __host__ __device__ constexpr bool hneg(int p, int s) { return (kNegMask >> (4 * p + s)) & 1u; }
 

@@ -343,3 +343,20 @@ def test_cuda_graph_capture_and_replay(M, N, K, opA, opB, path):
         torch.cuda.synchronize()
         assert torch.equal(C_graph, C_eager)
     assert_parity(pr, C_eager.cpu().numpy(), oracle_full(pr))
+
+
+@pytest.mark.parametrize("n", [2048, 4096])
+def test_metamorphic_conjugate_transpose_identity(n):
+    """(AB)^H = B^H A^H, checked on the GPU alone at sizes
+    the oracle would take minutes for: qgemm('N','N', A, B) vs qgemm('H','H', B, A)."""
+    g = torch.Generator(device="cuda").manual_seed(n)
+    A = torch.randn((n, n, 4), dtype=torch.float64, device="cuda", generator=g)
+    B = torch.randn((n, n, 4), dtype=torch.float64, device="cuda", generator=g)
+    C1 = torch.zeros((n, n, 4), dtype=torch.float64, device="cuda")
+    C2 = torch.zeros_like(C1)
+    qg.qgemm("N", "N", 1.0, A, B, 0.0, C1)
+    qg.qgemm("H", "H", 1.0, B, A, 0.0, C2)
+    torch.cuda.synchronize()
+    conjT = C1.transpose(0, 1) * torch.tensor([1.0, -1.0, -1.0, -1.0], dtype=torch.float64, device="cuda")
+    tol = 2e-12 * n * float(A.abs().max()) * float(B.abs().max())
+    assert float((C2 - conjT).abs().max()) <= tol
