@@ -17,11 +17,13 @@
 //
 // CTA: 64x64 output quaternions, 8 consumer warps (2 in m x 4 in n, each a
 // 32x16 warp tile = 4x2 m8n8 tiles x 4 components = 64 f64 accumulators per
-// lane) + 1 producer warp that streams packed chunks (qg_pack.cuh FragLayout)
-// through a 3-stage shared-memory ring with 1-D bulk copies (cp.async.bulk,
-// SASS UBLKCP) completing on mbarriers.  Epilogue: alpha (x) acc + beta (x) C,
-// left products, masked at the M/N edges, C re-interleaved in
-// registers (each lane owns whole quaternions).
+// lane) + a producer warpgroup, one lane of which fills a 3-stage shared-memory
+// ring completing on mbarriers -- with 1-D bulk copies of packed chunks
+// (qg_pack.cuh FragLayout; SASS UBLKCP), or (the direct path, kFeedTma) with
+// TMA tensor-map loads of the user's interleaved tiles, de-interleaved by the
+// consumers' fragment addresses.  Epilogue: alpha (x) acc + beta (x) C, left
+// products, masked at the M/N edges, C re-interleaved in registers
+// (each lane owns whole quaternions).
 //
 // Schedule: persistent (one CTA per SM), "data-parallel + stream-K" hybrid.
 // Whole tiles are dealt round-robin while at least two full waves remain; the
@@ -29,9 +31,10 @@
 // no SM idles in a partial last wave (c2: 256 tiles on 148 SMs).  A tile split
 // across CTAs is finished by the CTA holding its k = 0 segment (the "owner"):
 // the others park their partial accumulators in the workspace and bump the
-// tile's arrival counter; the owner adds them and runs the epilogue.  The
-// producer warp walks the same work list, so the ring keeps streaming across
-// tile boundaries while the consumers run an epilogue.
+// tile's arrival counter; the owner adds them and runs the epilogue (the host
+// launches such grids cooperatively, so every CTA is resident).  The producer
+// walks the same work list, so the ring keeps streaming across tile boundaries
+// while the consumers run an epilogue.
 #pragma once
 #include <cuda.h>  // CUtensorMap (the TMA feed)
 #include "qg_pack.cuh"
@@ -52,7 +55,6 @@ constexpr int kConsumerRegs = 232;
 constexpr int kGroupM = QG_GROUP_M;  // rasterisation: M-tiles per group (L2 reuse of panels)
 // ring + barriers + 1 KB so the ring can start on a 1024-byte boundary
 constexpr size_t kDmmaSmemBytes = size_t(kStages) * 2 * kChunkElems * sizeof(double) + 2 * kStages * 8 + 1024;
-// (the 32-byte swizzle repeats every 256 bytes; the ring starts 1024-aligned)
 
 // How the ring is fed (kernel template parameter).
 // (a third feed -- all 128 producer threads de-interleaving with 16-byte
