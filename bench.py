@@ -275,11 +275,18 @@ def measure_f32_variant(A, B, C, n, warmup, steps):
     achieved = fl / (main_ms / max(1, main_cnt) / 1e3) / 1e12 if main_cnt else None
     del A32, B32, C32
     torch.cuda.empty_cache()
+    roof = make_roofline("f32", achieved, main_ms, ms, kt["pack"][0], steps)
+    # the MMA-loop peak is at 1965 MHz; under this kernel's power draw the SM
+    # clock drops (sw_power_cap), so also report the fraction of the peak at the
+    # clock sampled during the timed region
+    mhz = (clocks or {}).get("sm_mhz")
+    if mhz and roof.get("achieved"):
+        roof["peak_at_observed_clock"] = TF32_PEAK_TFLOPS * mhz / 1965.0
+        roof["frac_at_observed_clock"] = roof["achieved"] / roof["peak_at_observed_clock"]
     return {"workload": "c3 FP32: M=N=K=8192 opA=N opB=H alpha=beta=1 (inputs = FP64 draws "
                         "rounded to FP32)", "dtype": "f32 (3xTF32 on tcgen05, FP32 accumulate)",
             "value": fl * steps / (ms / 1e3) / 1e12, "unit": "TFLOP/s", "ms_per_step": ms / steps,
-            "steps": steps, "roofline": make_roofline("f32", achieved, main_ms, ms, kt["pack"][0],
-                                                      steps), "clocks": clocks}
+            "steps": steps, "roofline": roof, "clocks": clocks}
 
 
 def measure_other_configs(warmup):
