@@ -64,7 +64,7 @@
  * return the stream-K scratch size only (~33 MB) and no K-panel loop runs.
  *
  * Small problems: below the library's measured
- * crossover (FP64: M*N*K <= 2^24 quaternion multiply-adds; FP32: <= 2^25, or
+ * crossover (FP64: M*N*K < 2^24 quaternion multiply-adds; FP32: <= 2^25, or
  * small M x N with long K), qgemm/qgemm_f32 run ONE kernel that reads
  * op(A)/op(B) in place (no pack, no workspace);
  * qgemm_workspace_bytes() then returns 0 and `workspace` may be NULL.  The
@@ -197,7 +197,8 @@ int qgemm_naive(char transA, char transB, int64_t M, int64_t N, int64_t K,
  * the interleaved storage -- one launch, no pack, workspace = stream-K scratch
  * only; FP32 calls take the packed path).  Auto = small kernel below the
  * crossover; above it FP64 takes the direct path when op(A) is T/H or
- * M*N*K <= 2^30 (with K >= 512), else packed; FP32 packed.
+ * M*N*K <= 2^30, except for K < 512 with M*N >= 2^22 (packed), else packed;
+ * FP32 packed.
  * Returns the previous policy, or -1 (policy unchanged) for other values.
  * For tests and benchmarks; the result is correct under every policy. */
 int qgemm_set_path_policy(int policy);

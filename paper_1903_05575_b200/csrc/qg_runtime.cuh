@@ -435,22 +435,23 @@ std::atomic<int> g_path_policy{0};
 // storage order, so op(A) = A (rows contiguous) costs 4-way shared-memory bank
 // conflicts on the A fragments (2-way when k is contiguous) -- the pack it
 // saves is worth more than that only for small problems.  Auto: direct when
-// op(A) is T/H, or when M*N*K <= 2^30; packed for K < 512 (c4: K = 256) and
-// large op(A) = N problems (c3, c5).
+// op(A) is T/H, or when M*N*K <= 2^30; packed for K < 512 with M*N >= 2^22
+// (c4: K = 256) and for large op(A) = N problems (c3, c5).
 template <typename T>
 int direct_feed(int opA, int64_t M, int64_t N, int64_t K) {
   if (sizeof(T) != 8) return 0;
   const int pol = g_path_policy.load(std::memory_order_relaxed);
   if (pol == 3) return qg::kFeedTma;
   if (pol != 0) return 0;
-  if (K < 512) return 0;
+  const double mn = double(M) * double(N);
+  if (K < 512 && mn >= double(int64_t(1) << 22)) return 0;  // c4-like: short K, big C
   if (opA != 0) return qg::kFeedTma;
-  return double(M) * double(N) * double(K) <= double(int64_t(1) << 30) ? qg::kFeedTma : 0;
+  return mn * double(K) <= double(int64_t(1) << 30) ? qg::kFeedTma : 0;
 }
 
 // Auto policy (crossover measured on B200 with tools/small_sweep.py):
-//  * FP64: the small kernel up to 2^24 quaternion multiply-adds (256^3), where
-//    the packed path's persistent DMMA mainloop catches up;
+//  * FP64: the small kernel below 2^24 quaternion multiply-adds (256^3), where
+//    the persistent DMMA mainloop (TMA-fed) catches up;
 //  * FP32: up to 2^25 (the tcgen05 path has a 128x128 tile and no split-K), and
 //    up to 2^28 when that path would launch fewer than 1/4 as many CTAs as
 //    there are SMs and K >= 4 max(M, N) (small M x N, long K);
@@ -469,7 +470,7 @@ bool use_small(int64_t M, int64_t N, int64_t K) {
   if (M > kCap || N > kCap || K > kCap) return false;  // keeps M*N*K from overflowing below
   const double macs = double(M) * double(N) * double(K);
   if (macs > double(kCap)) return false;
-  if (sizeof(T) == 8) return macs <= double(kSmallMaxMacs);
+  if (sizeof(T) == 8) return macs < double(kSmallMaxMacs);  // 256^3 itself: direct (45 vs 49 us)
   if (K <= 16 && double(M) * double(N) >= double(1 << 20)) return false;
   if (macs <= double(2 * kSmallMaxMacs)) return true;
   const int64_t tc_ctas = cdiv(M, 128) * cdiv(N, 128);

@@ -16,10 +16,13 @@ import paper_1903_05575_b200 as qg  # noqa: E402
 
 ap = argparse.ArgumentParser()
 ap.add_argument("--out", default=None)
+ap.add_argument("--small-shapes", action="store_true", help="the small/direct/packed crossover region")
 a = ap.parse_args()
 g = torch.Generator(device="cuda").manual_seed(0)
 SHAPES = [(n, n, n, ops) for n in (384, 512, 768, 1024, 1536, 2048, 3072, 4096) for ops in ("NN", "NH", "TN")]
 SHAPES += [(8192, 8192, 256, "NH"), (4096, 4096, 256, "NH"), (2048, 2048, 8192, "NH"), (4096, 4096, 1024, "NH")]
+if a.small_shapes:
+    SHAPES = [(n, n, n, ops) for n in (128, 192, 256, 320, 384, 448, 512) for ops in ("NN", "TN")]
 
 
 def graph_time(call):
@@ -59,7 +62,10 @@ for M, N, K, ops in SHAPES:
     B = torch.randn((bc, br, 4), dtype=torch.float64, device="cuda", generator=g)
     C = torch.randn((N, M, 4), dtype=torch.float64, device="cuda", generator=g)
     row = {"M": M, "N": N, "K": K, "ops": ops}
-    for name, pol in (("packed", qg.PATH_PACKED), ("tma", qg.PATH_DIRECT)):
+    pols = (("packed", qg.PATH_PACKED), ("tma", qg.PATH_DIRECT))
+    if a.small_shapes:
+        pols += (("small", qg.PATH_SMALL),)
+    for name, pol in pols:
         old = qg.set_path_policy(pol)
         ws = torch.empty(max(256, qg.workspace_bytes(ops[0], ops[1], M, N, K)), dtype=torch.uint8, device="cuda")
         t = graph_time(lambda: qg.qgemm(ops[0], ops[1], 1.0, A, B, 1.0, C, M=M, N=N, K=K, workspace=ws))
