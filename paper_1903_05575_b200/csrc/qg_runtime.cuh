@@ -450,8 +450,8 @@ int direct_feed(int opA, int64_t M, int64_t N, int64_t K) {
 }
 
 // Auto policy (crossover measured on B200 with tools/small_sweep.py):
-//  * FP64: the small kernel below 2^24 quaternion multiply-adds (256^3), where
-//    the persistent DMMA mainloop (TMA-fed) catches up;
+//  * FP64: the small kernel up to 2^24 quaternion multiply-adds (256^3); the
+//    persistent DMMA mainloop (TMA-fed) wins from 320^3;
 //  * FP32: up to 2^25 (the tcgen05 path has a 128x128 tile and no split-K), and
 //    up to 2^28 when that path would launch fewer than 1/4 as many CTAs as
 //    there are SMs and K >= 4 max(M, N) (small M x N, long K);
@@ -470,7 +470,7 @@ bool use_small(int64_t M, int64_t N, int64_t K) {
   if (M > kCap || N > kCap || K > kCap) return false;  // keeps M*N*K from overflowing below
   const double macs = double(M) * double(N) * double(K);
   if (macs > double(kCap)) return false;
-  if (sizeof(T) == 8) return macs < double(kSmallMaxMacs);  // 256^3 itself: direct (45 vs 49 us)
+  if (sizeof(T) == 8) return macs <= double(kSmallMaxMacs);  // 256^3: small 36.9 us vs direct 45
   if (K <= 16 && double(M) * double(N) >= double(1 << 20)) return false;
   if (macs <= double(2 * kSmallMaxMacs)) return true;
   const int64_t tc_ctas = cdiv(M, 128) * cdiv(N, 128);
@@ -488,6 +488,10 @@ int num_sms() {
   return sms;
 }
 
+#ifndef QG_SMALL_CTAS_PER_SM
+#define QG_SMALL_CTAS_PER_SM 4
+#endif
+
 template <typename T>
 int launch_small(const T *A, int64_t lda, int a_rc, int a_cj, const T *B, int64_t ldb, int b_rc, int b_cj, T *C,
                  int64_t ldc, int64_t M, int64_t N, int64_t K, const T *alpha, const T *beta, cudaStream_t st) {
@@ -500,8 +504,11 @@ int launch_small(const T *A, int64_t lda, int a_rc, int a_cj, const T *B, int64_
   // split K over more warps until the grid covers the SMs (keeping >= 2 k4 steps per warp)
   const int64_t tm = cdiv(M, 8), tn = cdiv(N, 8), steps = cdiv(K, 4);
   const int64_t sms = num_sms();
+  // split K over more warps while the grid still fits one wave of resident
+  // CTAs (4 per SM at <= 128 registers) and each warp keeps >= 2 k4 steps:
+  // shorter per-warp load->DMMA chains, same number of waves
   int S = 1;
-  while (S < 4 && cdiv(tm, 4 / S) * tn < sms && steps >= 4 * S) S *= 2;
+  while (S < 4 && cdiv(tm, 4 / (2 * S)) * tn <= QG_SMALL_CTAS_PER_SM * sms && steps >= 4 * S) S *= 2;
   a.S = S;
   a.m_blocks = cdiv(tm, 4 / S);
   const int64_t blocks = a.m_blocks * tn;

@@ -19,7 +19,8 @@
 // FP32 storage: quaternions are widened to double on load and the FP64 result
 // is rounded once on store -- more accurate than the FP32 tolerance requires.
 //
-// CTA = 4 warps.  With split factor S in {1, 2, 4}, warp w computes the 8x8 tile
+// CTA = 4 warps.  With split factor S in {1, 2, 4} (host: as large as keeps the
+// grid within one wave of resident CTAs), warp w computes the 8x8 tile
 // (w / S) of the CTA's (4/S) M-stacked tiles over the (w % S)-th of S equal
 // ranges of k4 steps; partials are summed in a fixed order through shared
 // memory (deterministic), then lane l applies the alpha/beta epilogue (left

@@ -178,8 +178,8 @@ def test_small_path_needs_no_workspace(lib):
     lib.qgemm_set_path_policy(0)
     assert lib.qgemm_workspace_bytes(b"N", b"N", 64, 64, 64, 0) == 0
     assert lib.qgemm_workspace_bytes(b"T", b"H", 256, 256, 256, 1) == 0   # FP32: <= 2^25
-    assert lib.qgemm_workspace_bytes(b"N", b"N", 255, 256, 256, 0) == 0   # FP64: < 2^24
-    assert lib.qgemm_workspace_bytes(b"N", b"N", 256, 256, 256, 0) > 0    # FP64 2^24: direct
+    assert lib.qgemm_workspace_bytes(b"N", b"N", 256, 256, 256, 0) == 0   # FP64: <= 2^24
+    assert lib.qgemm_workspace_bytes(b"N", b"N", 257, 256, 256, 0) > 0    # FP64 above: direct
     assert lib.qgemm_workspace_bytes(b"N", b"H", 8192, 8192, 8192, 0) > 0
     # huge single factors must not overflow M*N*K into the small path
     assert lib.qgemm_workspace_bytes(b"N", b"N", 1 << 40, 1 << 40, 1, 0) > 0
