@@ -69,7 +69,7 @@ HostPlan<T> host_plan(int64_t M, int64_t N, int64_t K) {
   for (int i = 0; i < 2; ++i) { h.off_sb[i] = off; if (i < nbuf) off += sb; }
   if (!h.small && K > 0) {
     const int64_t ktc = cdiv(h.Kc, kq);
-    const size_t pa = align256(size_t(cdiv(M, Geo<T>::rows)) * size_t(ktc) * Geo<T>::chunk);
+    const size_t pa = align256(size_t(Geo<T>::a_tiles(M)) * size_t(ktc) * Geo<T>::chunk);
     const size_t pb = align256(size_t(cdiv(N, Geo<T>::rows)) * size_t(ktc) * Geo<T>::chunk);
     for (int i = 0; i < 2; ++i) { h.off_pa[i] = off; if (i < nbuf) off += pa; }
     for (int i = 0; i < 2; ++i) { h.off_pb[i] = off; if (i < nbuf) off += pb; }
@@ -231,8 +231,8 @@ int qgemm_host_impl(char transA, char transB, int64_t M, int64_t N, int64_t K, c
     const int64_t ktn = cdiv(kc, Geo<T>::kq);
     T *pa = reinterpret_cast<T *>(ws + h.off_pa[sl]);
     T *pb = reinterpret_cast<T *>(ws + h.off_pb[sl]);
-    QH_TRY(launch_pack2<T>(pack_job<T>(reinterpret_cast<const T *>(ws + h.off_sa[sl]), lda_s, a_rc, a_cj, M, 0, kc, ktn, pa),
-                           pack_job<T>(reinterpret_cast<const T *>(ws + h.off_sb[sl]), ldb_s, b_rc, b_cj, N, 0, kc, ktn, pb), S));
+    QH_TRY(launch_pack2<T>(pack_job<T>(reinterpret_cast<const T *>(ws + h.off_sa[sl]), lda_s, a_rc, a_cj, M, 0, kc, ktn, pa, true),
+                           pack_job<T>(reinterpret_cast<const T *>(ws + h.off_sb[sl]), ldb_s, b_rc, b_cj, N, 0, kc, ktn, pb, false), S));
     ++launches;
     packed[size_t(p)] = hs.ev();
     QH_TRY(int(cudaEventRecord(packed[size_t(p)], S)));

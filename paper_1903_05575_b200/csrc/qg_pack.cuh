@@ -52,6 +52,7 @@ struct PackJob {
   int64_t R, k_begin, k_end, KT;
   T *out;
   int64_t blocks;
+  int split_halves;  // FP32 tcgen05 pack only: each 64-row half of a chunk contiguous (2-CTA B operand)
 };
 
 // grid: ja.blocks + jb.blocks blocks (1-D), 256 threads: A and B are packed by

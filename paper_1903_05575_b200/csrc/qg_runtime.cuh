@@ -87,21 +87,32 @@ struct Shape {
 // Packed-operand geometry per precision: rows per tile, k per tile, bytes per chunk.
 template <typename T>
 struct Geo;
+// a_tiles: row tiles of packed A (FP32 with CTA pairs: an even count, the
+// pair's second tile zero-filled past M); B is packed with split halves then.
+#ifndef QG_TC32_2CTA
+#define QG_TC32_2CTA 1  // FP32 mainloop on CTA pairs (qg_tc32_2cta.cuh); 0: one CTA per tile
+#endif
 template <>
 struct Geo<double> {  // DMMA path (qg_dmma.cuh)
   static constexpr int64_t rows = qg::kBR, kq = qg::kBK;
   static constexpr size_t chunk = size_t(qg::kChunkElems) * sizeof(double);
+  static int64_t a_tiles(int64_t M) { return cdiv(M, rows); }
+  static constexpr int split_b = 0;
+  static constexpr int64_t pack_sub = 1;  // chunks per pack block
 };
 template <>
 struct Geo<float> {  // tcgen05 3xTF32 path (qg_tc32.cuh): hi + lo planes
   static constexpr int64_t rows = qg::kTcBM, kq = qg::kTcBK;
   static constexpr size_t chunk = qg::kTcChunkBytes;
+  static int64_t a_tiles(int64_t M) { return QG_TC32_2CTA ? 2 * cdiv(M, 2 * rows) : cdiv(M, rows); }
+  static constexpr int split_b = QG_TC32_2CTA;
+  static constexpr int64_t pack_sub = qg::kTcPackSub;
 };
 
 // Bytes of one K-tile column of packed panels (all MT + NT row tiles).
 template <typename T>
 size_t bytes_per_ktile(int64_t M, int64_t N) {
-  return size_t(cdiv(M, Geo<T>::rows) + cdiv(N, Geo<T>::rows)) * Geo<T>::chunk;
+  return size_t(Geo<T>::a_tiles(M) + cdiv(N, Geo<T>::rows)) * Geo<T>::chunk;
 }
 
 // Upper bound of the persistent grid for a panel of `ktiles` k-tiles: the
@@ -127,7 +138,7 @@ template <typename T>
 size_t workspace_for(int64_t M, int64_t N, int64_t K, int64_t ktiles) {
   // the stream-K reserve is sized for the whole K (an upper bound for any panel),
   // so the workspace grows linearly with the panel depth `ktiles`
-  const size_t a = size_t(cdiv(M, Geo<T>::rows)) * size_t(ktiles) * Geo<T>::chunk;
+  const size_t a = size_t(Geo<T>::a_tiles(M)) * size_t(ktiles) * Geo<T>::chunk;
   const size_t b = size_t(cdiv(N, Geo<T>::rows)) * size_t(ktiles) * Geo<T>::chunk;
   return align256(a) + align256(b) + sk_reserve<T>(M, N, cdiv(K, Geo<T>::kq));
 }
@@ -195,13 +206,15 @@ int launch_axpby(T *Y, int64_t ldy, const T *X, int64_t ldx, int64_t M, int64_t 
   return int(cudaGetLastError());
 }
 
+// is_a: the A operand (row tiles per Geo::a_tiles); B takes Geo::split_b.
 template <typename T>
 qg::PackJob<T> pack_job(const T *X, int64_t ldx, int row_contig, int conj, int64_t R, int64_t k_begin,
-                        int64_t k_end, int64_t KT, T *out) {
+                        int64_t k_end, int64_t KT, T *out, bool is_a) {
   qg::PackJob<T> j;
   j.X = X; j.ldx = ldx; j.row_contig = row_contig; j.conj = conj; j.R = R;
   j.k_begin = k_begin; j.k_end = k_end; j.KT = KT; j.out = out;
-  j.blocks = cdiv(R, Geo<T>::rows) * KT;
+  j.blocks = (is_a ? Geo<T>::a_tiles(R) : cdiv(R, Geo<T>::rows)) * cdiv(KT, Geo<T>::pack_sub);
+  j.split_halves = is_a ? 0 : Geo<T>::split_b;
   return j;
 }
 
@@ -400,6 +413,21 @@ int launch_mainloop_direct(int feed, const double *A, int64_t lda, int a_rc, int
   return launch_dmma(a, dmma_kernel(feed, a_cj != 0, b_cj != 0, a_rc, b_rc), sk_scratch, st);
 }
 
+// 2-D view of a packed FP32 chunk array for the pair kernel's TMA: rows of
+// 256 floats (1 KB); a chunk = 32 rows, a split B half = 16 rows.
+int encode_packed_2d(CUtensorMap *tm, const float *base, int64_t chunks, int box_rows) {
+  EncodeTiledFn fn = encode_tiled();
+  if (!fn) return int(cudaErrorNotSupported);
+  const cuuint64_t dims[2] = {256, cuuint64_t(chunks) * 32};
+  const cuuint64_t strides[1] = {1024};
+  const cuuint32_t box[2] = {256, cuuint32_t(box_rows)};
+  const cuuint32_t estr[2] = {1, 1};
+  const CUresult r = fn(tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float *>(base), dims, strides, box,
+                        estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                        CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS ? 0 : int(cudaErrorInvalidValue);
+}
+
 int launch_mainloop(const float *Ap, const float *Bp, float *C, int64_t ldc, int64_t M, int64_t N, int64_t KT,
                     const qg::Scalars<float> &sc, void * /*sk_scratch*/, cudaStream_t st,
                     int /*tri: FP64 only*/ = 0) {
@@ -410,8 +438,26 @@ int launch_mainloop(const float *Ap, const float *Bp, float *C, int64_t ldc, int
   if (dev >= kMaxDev || !attr_set[dev]) {
     cudaError_t e = cudaFuncSetAttribute(qg::qgemm_tc32_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          int(qg::kTcSmemBytes));
+    if (e == cudaSuccess)
+      e = cudaFuncSetAttribute(qg::qgemm_tc32_2cta_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               int(qg::kTc2SmemBytes));
     if (e != cudaSuccess) return int(e);
     if (dev < kMaxDev) attr_set[dev] = true;
+  }
+  if (QG_TC32_2CTA) {
+    qg::Tc2Args t{};
+    t.C = C; t.ldc = ldc; t.M = M; t.N = N; t.KT = KT; t.sc = sc;
+    t.MT2 = cdiv(M, 2 * qg::kTcBM); t.NT = cdiv(N, qg::kTcBN);
+    int rc = encode_packed_2d(&t.tmA, Ap, 2 * t.MT2 * KT, 32);
+    if (!rc) rc = encode_packed_2d(&t.tmB, Bp, t.NT * KT, 16);
+    if (rc) return rc;
+    const int64_t grid = 2 * t.MT2 * t.NT;
+    if (grid > INT32_MAX) return int(cudaErrorInvalidConfiguration);
+    { int ti = tstart(kMain, st);
+    qg::qgemm_tc32_2cta_kernel<<<unsigned(grid), qg::kTcThreads, qg::kTc2SmemBytes, st>>>(t);
+    tstop(ti, st); }
+    ++g_last_launches;
+    return int(cudaGetLastError());
   }
   qg::Tc32Args t;
   t.Ap = Ap; t.Bp = Bp; t.C = C; t.ldc = ldc; t.M = M; t.N = N;

@@ -42,6 +42,7 @@ constexpr int kTcPlaneFloats = 128 * kTcBK;            // one 128 x 8 plane
 constexpr int kTcChunkFloats = 8 * kTcPlaneFloats;     // planes [p 4][hi, lo]
 constexpr uint32_t kTcChunkBytes = kTcChunkFloats * 4; // 32 KiB
 constexpr int kTcStages = 3;
+constexpr int kTcPackSub = 4;  // chunks packed per block
 constexpr int kTcThreads = 256;
 constexpr size_t kTcSmemBytes = size_t(kTcStages) * 2 * kTcChunkBytes + 256;
 
@@ -58,7 +59,8 @@ __device__ __forceinline__ float tf32_rna(float x) {
 
 // Pack for the tensor-core path: rows r of op(X) (R of them) x k in
 // [k_begin, k_end), conj applied, split into tf32 hi/lo, one 32 KiB chunk per
-// (128-row tile, 8-k tile).  grid = RT * KT blocks of 256 threads.
+// (128-row tile, 8-k tile).  A block packs kTcPackSub consecutive chunks of one
+// row tile: grid = RT * ceil(KT / kTcPackSub) blocks of 256 threads.
 // grid = ja.blocks + jb.blocks: A and B in one launch (as pack_kernel).
 __global__ void __launch_bounds__(256) pack_tc32_kernel(const PackJob<float> ja, const PackJob<float> jb) {
   const bool second = int64_t(blockIdx.x) >= ja.blocks;
@@ -68,39 +70,51 @@ __global__ void __launch_bounds__(256) pack_tc32_kernel(const PackJob<float> ja,
   const int64_t ldx = j.ldx, R = j.R, k_end = j.k_end, KT = j.KT;
   const int row_contig = j.row_contig, conj = j.conj;
   float *__restrict__ out = j.out;
-  __shared__ __align__(16) float tile[kTcBK][kTcBM][4];
-  const int64_t rt = bid / KT;
-  const int64_t kt = bid % KT;
-  const int64_t r0 = rt * kTcBM, k0 = j.k_begin + kt * kTcBK;
+  // [k][component][row], rows padded to 129: conflict-free for both the
+  // staging writes (consecutive rows, or consecutive k) and the per-plane reads
+  constexpr int kPitch = kTcBM + 1;
+  __shared__ float tile[kTcBK][4][kPitch];
+  const int64_t KTS = (KT + kTcPackSub - 1) / kTcPackSub;  // blocks per row tile
+  const int64_t rt = bid / KTS;
+  const int64_t r0 = rt * kTcBM;
   const float sgn = conj ? -1.f : 1.f;
+  for (int sub = 0; sub < kTcPackSub; ++sub) {
+    const int64_t kt = (bid % KTS) * kTcPackSub + sub;
+    if (kt >= KT) break;
+    const int64_t k0 = j.k_begin + kt * kTcBK;
+    if (sub) __syncthreads();  // the previous chunk's reads of `tile` are done
 #pragma unroll
-  for (int it = 0; it < (kTcBM * kTcBK) / 256; ++it) {
-    const int q = threadIdx.x + 256 * it;
-    int r, k;
-    if (row_contig) { r = q % kTcBM; k = q / kTcBM; }
-    else            { k = q % kTcBK; r = q / kTcBK; }
-    const int64_t rg = r0 + r, kg = k0 + k;
-    float v[4] = {0.f, 0.f, 0.f, 0.f};
-    if (rg < R && kg < k_end) {
-      ldq(row_contig ? X + 4 * (rg + kg * ldx) : X + 4 * (kg + rg * ldx), v);
-      v[1] *= sgn; v[2] *= sgn; v[3] *= sgn;
-    }
-    *reinterpret_cast<float4 *>(&tile[k][r][0]) = make_float4(v[0], v[1], v[2], v[3]);
-  }
-  __syncthreads();
-  float4 *o = reinterpret_cast<float4 *>(out + bid * int64_t(kTcChunkFloats));
-  for (int o4 = threadIdx.x; o4 < kTcChunkFloats / 4; o4 += 256) {
-    const int plane = o4 >> 8, rem = o4 & 255;
-    const int rg = rem >> 4, kh = (rem >> 3) & 1, r8 = rem & 7;
-    const int r = rg * 8 + r8, kb = kh * 4, p = plane >> 1, lo = plane & 1;
-    float w[4];
+    for (int it = 0; it < (kTcBM * kTcBK) / 256; ++it) {
+      const int q = threadIdx.x + 256 * it;
+      int r, k;
+      if (row_contig) { r = q % kTcBM; k = q / kTcBM; }
+      else            { k = q % kTcBK; r = q / kTcBK; }
+      const int64_t rg = r0 + r, kg = k0 + k;
+      float v[4] = {0.f, 0.f, 0.f, 0.f};
+      if (rg < R && kg < k_end) {
+        ldq(row_contig ? X + 4 * (rg + kg * ldx) : X + 4 * (kg + rg * ldx), v);
+        v[1] *= sgn; v[2] *= sgn; v[3] *= sgn;
+      }
 #pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      const float x = tile[kb + j][r][p];
-      const float hi = tf32_rna(x);
-      w[j] = lo ? tf32_rna(x - hi) : hi;
+      for (int c = 0; c < 4; ++c) tile[k][c][r] = v[c];
     }
-    o[o4] = make_float4(w[0], w[1], w[2], w[3]);
+    __syncthreads();
+    float4 *o = reinterpret_cast<float4 *>(out + (rt * KT + kt) * int64_t(kTcChunkFloats));
+    for (int o4 = threadIdx.x; o4 < kTcChunkFloats / 4; o4 += 256) {
+      const int plane = o4 >> 8, rem = o4 & 255;
+      const int rg = rem >> 4, kh = (rem >> 3) & 1, r8 = rem & 7;
+      const int r = rg * 8 + r8, kb = kh * 4, p = plane >> 1, lo = plane & 1;
+      float w[4];
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const float x = tile[kb + e][p][r];
+        const float hi = tf32_rna(x);
+        w[e] = lo ? tf32_rna(x - hi) : hi;
+      }
+      // split_halves: rows 64h.. of every plane grouped per half h -> [h][plane][64 x 8]
+      const int dst = j.split_halves ? (rg >> 3) * 1024 + plane * 128 + (rem & 127) : o4;
+      o[dst] = make_float4(w[0], w[1], w[2], w[3]);
+    }
   }
 }
 

@@ -1,0 +1,217 @@
+// qg_tc32_2cta.cuh -- FP32 (3xTF32) QGEMM on CTA pairs: tcgen05.mma.cta_group::2.
+//
+// Same method as qg_tc32.cuh (16 real products per quaternion MAC, D^{p XOR s}
+// += eps(p,s) A^p B^s, Eq. quaternion_prod; three tf32 MMAs per
+// product, A_hi B_hi + A_hi B_lo + A_lo B_hi; eps = -1 as the negate-A bit),
+// but a cluster of two CTAs on one TPC computes a 256 x 128 quaternion tile
+// with M = 256 MMAs issued by the leader CTA: each CTA holds its own 128 rows
+// of A and HALF (64 columns) of B in shared memory, and receives its 128 x 128
+// block of the four accumulators in its own TMEM.  Per CTA that halves the B
+// bytes staged and read per MMA flop, and the M = 256, N = 128 shape issues at
+// the tf32 pipe's full rate (tools/microbench/tf32_peak.cu: 1097 TF vs 1042 TF
+// for the 1-CTA M = 128, N = 128 shape).
+//
+// Operands stream with 2-D TMA over the packed chunk arrays (no swizzle: the
+// chunks are byte images of the canonical K-major UMMA layout): both CTAs load
+// their own A chunk and B half, completing transaction bytes on the LEADER's
+// full barrier (peer bit of the barrier address cleared, .cta_group::2); the
+// leader's commits arrive on both CTAs' empty / accumulator barriers
+// (.multicast::cluster).  The B chunks are packed with split_halves so each
+// CTA's 64-column half is one contiguous 16 KB block.
+#pragma once
+#include <cuda.h>
+#include "qg_tc32.cuh"
+
+namespace qg {
+
+constexpr int kTc2Stages = 4;
+constexpr uint32_t kTc2ABytes = kTcChunkBytes;       // 32 KB: this CTA's 128 rows, 8 planes
+constexpr uint32_t kTc2BBytes = kTcChunkBytes / 2;   // 16 KB: this CTA's 64 columns, 8 planes
+constexpr int kTc2AFloats = kTcChunkFloats;
+constexpr int kTc2BFloats = kTcChunkFloats / 2;
+constexpr size_t kTc2SmemBytes = size_t(kTc2Stages) * (kTc2ABytes + kTc2BBytes) + 256 + 1024;
+constexpr uint32_t kPeerBitMask = 0xFEFFFFFFu;  // shared::cluster address of the leader's copy
+
+struct alignas(64) Tc2Args {
+  CUtensorMap tmA;   // packed A viewed as [rows of 256 floats]; a chunk = 32 rows
+  CUtensorMap tmB;   // packed B (split halves): a half = 16 rows
+  float *C;
+  int64_t ldc, M, N, MT2, NT, KT;  // MT2 = 256-row tile pairs
+  Scalars<float> sc;
+};
+
+// kind::tf32, D f32, K-major A/B, M = 256 (pair), N = 128.
+__host__ __device__ constexpr uint32_t tc2_idesc(bool negate_a) {
+  return (1u << 4) | (2u << 7) | (2u << 10) | ((negate_a ? 1u : 0u) << 13) | (uint32_t(kTcBN >> 3) << 17) |
+         (uint32_t(256 >> 4) << 24);
+}
+
+__device__ __forceinline__ uint32_t cluster_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;\n" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;\n" ::: "memory");
+}
+
+// 2-D TMA load into this CTA's smem; transaction bytes counted on the leader's barrier.
+__device__ __forceinline__ void tma2_load_2d(void *dst, const CUtensorMap *tm, int c0, int c1, uint64_t *bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, "
+      "%3}], [%4];\n" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(tm)), "r"(c0), "r"(c1), "r"(smem_u32(bar) & kPeerBitMask)
+      : "memory");
+}
+
+__device__ __forceinline__ void tc2_mma(uint32_t d_tmem, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
+  asm volatile(
+      "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::2.kind::tf32 [%0], %1, %2, %3, p;\n}\n" ::"r"(d_tmem),
+      "l"(a), "l"(b), "r"(idesc), "r"(acc));
+}
+
+// Arrive (once the leader's prior MMAs complete) on the barrier at this smem
+// offset in BOTH CTAs of the pair.
+__device__ __forceinline__ void tc2_commit_both(uint64_t *bar) {
+  asm volatile(
+      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;\n" ::"r"(
+          smem_u32(bar)),
+      "h"((unsigned short)3)
+      : "memory");
+}
+
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kTcThreads, 1)
+    qgemm_tc32_2cta_kernel(const __grid_constant__ Tc2Args args) {
+  extern __shared__ __align__(128) unsigned char smem_dyn[];
+  unsigned char *smem = smem_dyn + ((1024u - (smem_u32(smem_dyn) & 1023u)) & 1023u);
+  float *sA = reinterpret_cast<float *>(smem);
+  float *sB = sA + kTc2Stages * kTc2AFloats;
+  uint64_t *full = reinterpret_cast<uint64_t *>(sB + kTc2Stages * kTc2BFloats);  // leader's counts both CTAs
+  uint64_t *empty = full + kTc2Stages;
+  uint64_t *acc_full = empty + kTc2Stages;
+  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(acc_full + 1);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t rank = cluster_rank();
+  // tile pair of this cluster, grouped rasterisation as the 1-CTA kernel
+  const int64_t pid = int64_t(blockIdx.x) >> 1;
+  int64_t pm, pn;
+  {
+    const int64_t per_group = int64_t(kTcGroupM) * args.NT;
+    const int64_t g = pid / per_group;
+    const int64_t first_m = g * kTcGroupM;
+    const int64_t gsz = (args.MT2 - first_m) < kTcGroupM ? (args.MT2 - first_m) : kTcGroupM;
+    const int64_t in = pid - g * per_group;
+    pm = first_m + in % gsz;
+    pn = in / gsz;
+  }
+  const int64_t mt = 2 * pm + rank;  // this CTA's 128-row A tile
+  const int64_t KT = args.KT;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kTc2Stages; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    mbar_init(acc_full, 1);
+    fence_mbar_init();
+  }
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], 512;\n" ::"r"(smem_u32(tmem_slot))
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;\n" ::: "memory");
+  }
+  tc_fence_before();
+  cluster_sync_all();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0 && lane == 0) {
+    // ---------------- producer (both CTAs) ----------------
+    int slot = 0;
+    uint32_t phase = 0;
+    for (int64_t kt = 0; kt < KT; ++kt) {
+      if (kt >= kTc2Stages) mbar_wait_guarded(&empty[slot], phase ^ 1u);
+      if (rank == 0) mbar_arrive_expect_tx(&full[slot], 2 * (kTc2ABytes + kTc2BBytes));
+      tma2_load_2d(sA + slot * kTc2AFloats, &args.tmA, 0, int((mt * KT + kt) * 32), &full[slot]);
+      tma2_load_2d(sB + slot * kTc2BFloats, &args.tmB, 0, int((pn * KT + kt) * 32 + rank * 16), &full[slot]);
+      if (++slot == kTc2Stages) { slot = 0; phase ^= 1u; }
+    }
+  } else if (warp == 1 && lane == 0 && rank == 0) {
+    // ---------------- MMA issuer (leader only) ----------------
+    int slot = 0;
+    uint32_t phase = 0;
+    for (int64_t kt = 0; kt < KT; ++kt) {
+      mbar_wait_guarded(&full[slot], phase);
+      tc_fence_after();
+      const uint32_t a0 = smem_u32(sA + slot * kTc2AFloats);
+      const uint32_t b0 = smem_u32(sB + slot * kTc2BFloats);
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        const uint32_t d = tmem + uint32_t(c * kTcBN);
+#pragma unroll
+        for (int p = 0; p < 4; ++p) {
+          const int s = p ^ c;
+          const uint32_t id = tc2_idesc(hneg(p, s));
+          const uint64_t ahi = tc_sdesc(a0 + (p * 2 + 0) * kTcPlaneFloats * 4);
+          const uint64_t alo = tc_sdesc(a0 + (p * 2 + 1) * kTcPlaneFloats * 4);
+          const uint64_t bhi = tc_sdesc(b0 + (s * 2 + 0) * (kTcPlaneFloats / 2) * 4);
+          const uint64_t blo = tc_sdesc(b0 + (s * 2 + 1) * (kTcPlaneFloats / 2) * 4);
+          tc2_mma(d, ahi, bhi, id, (kt > 0 || p > 0) ? 1u : 0u);
+          tc2_mma(d, ahi, blo, id, 1u);
+          tc2_mma(d, alo, bhi, id, 1u);
+        }
+      }
+      tc2_commit_both(&empty[slot]);  // both CTAs may refill this stage
+      if (++slot == kTc2Stages) { slot = 0; phase ^= 1u; }
+    }
+    tc2_commit_both(acc_full);  // accumulators complete, in both CTAs' TMEM
+  } else if (warp >= 4) {
+    // ---------------- epilogue (both CTAs): TMEM -> registers -> C ----------------
+    const int q = warp - 4;
+    const int64_t row = mt * kTcBM + q * 32 + lane;
+    mbar_wait_guarded(acc_full, 0);
+    tc_fence_after();
+    const uint32_t tbase = tmem + (uint32_t(q * 32) << 16);
+    for (int n0 = 0; n0 < kTcBN; n0 += 16) {
+      float d[4][16];
+#pragma unroll
+      for (int c = 0; c < 4; ++c) tmem_ld16(tbase + uint32_t(c * kTcBN + n0), d[c]);
+      tmem_ld_wait();
+      if (row < args.M) {
+        float cold[16][4];
+        if (!args.sc.beta_zero) {
+#pragma unroll
+          for (int jj = 0; jj < 16; ++jj) {
+            const int64_t col = pn * kTcBN + n0 + jj;
+            if (col < args.N) ldq_c(args.C + 4 * (row + col * args.ldc), cold[jj]);
+          }
+        }
+#pragma unroll
+        for (int jj = 0; jj < 16; ++jj) {
+          const int64_t col = pn * kTcBN + n0 + jj;
+          if (col >= args.N) continue;
+          const float acc[4] = {d[0][jj], d[1][jj], d[2][jj], d[3][jj]};
+          float out[4];
+          left_scale(args.sc.alpha, args.sc.alpha_real, acc, out);
+          if (!args.sc.beta_zero) {
+            float bc[4];
+            left_scale(args.sc.beta, args.sc.beta_real, cold[jj], bc);
+#pragma unroll
+            for (int k = 0; k < 4; ++k) out[k] += bc[k];
+          }
+          stq(args.C + 4 * (row + col * args.ldc), out);
+        }
+      }
+    }
+  }
+  tc_fence_before();
+  cluster_sync_all();  // no CTA frees TMEM / exits while its peer's MMAs may still target it
+  if (warp == 0) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, 512;\n" ::"r"(tmem) : "memory");
+  }
+}
+
+}  // namespace qg

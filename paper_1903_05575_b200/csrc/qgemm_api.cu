@@ -20,6 +20,7 @@
 #include "qg_simple.cuh"
 #include "qg_small.cuh"
 #include "qg_tc32.cuh"
+#include "qg_tc32_2cta.cuh"
 
 
 namespace {
@@ -87,7 +88,7 @@ int panel_loop(const PackSpec<T> &pa, const PackSpec<T> &pb, int64_t M, int64_t 
     int64_t est = int64_t((workspace_bytes - res) / bytes_per_ktile<T>(M, N));
     KTp = std::max<int64_t>(1, std::min<int64_t>(KTp - 1, est));
   }
-  const int64_t MT = cdiv(M, Geo<T>::rows), NT = cdiv(N, Geo<T>::rows);
+  const int64_t MT = Geo<T>::a_tiles(M), NT = cdiv(N, Geo<T>::rows);
   T *Ap = reinterpret_cast<T *>(workspace);
   T *Bp = reinterpret_cast<T *>(reinterpret_cast<char *>(workspace) +
                                 align256(size_t(MT) * size_t(KTp) * Geo<T>::chunk));
@@ -100,8 +101,9 @@ int panel_loop(const PackSpec<T> &pa, const PackSpec<T> &pb, int64_t M, int64_t 
     const int64_t k_begin = kt0 * Geo<T>::kq;
     const int64_t k_end = std::min<int64_t>(K, (kt0 + KTp) * Geo<T>::kq);
     const int64_t ktn = cdiv(k_end - k_begin, Geo<T>::kq);
-    rc = launch_pack2<T>(pack_job<T>(pa.X, pa.ldx, pa.row_contig, pa.conj, M, k_begin, k_end, ktn, Ap),
-                         pack_job<T>(pb.X, pb.ldx, pb.row_contig, pb.conj, N, k_begin, k_end, ktn, Bp), st);
+    rc = launch_pack2<T>(pack_job<T>(pa.X, pa.ldx, pa.row_contig, pa.conj, M, k_begin, k_end, ktn, Ap, true),
+                         pack_job<T>(pb.X, pb.ldx, pb.row_contig, pb.conj, N, k_begin, k_end, ktn, Bp, false),
+                         st);
     if (rc) return rc;
     rc = launch_mainloop(Ap, Bp, C, ldc, M, N, ktn, kt0 == 0 ? sc : sc_acc, sk_scratch, st, tri);
     if (rc) return rc;
