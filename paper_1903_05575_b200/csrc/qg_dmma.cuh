@@ -41,7 +41,10 @@
 
 namespace qg {
 
-constexpr int kStages = 3;
+#ifndef QG_DMMA_STAGES
+#define QG_DMMA_STAGES 3
+#endif
+constexpr int kStages = QG_DMMA_STAGES;
 constexpr int kConsumerWarps = 8;
 constexpr int kConsumerThreads = kConsumerWarps * 32;
 // 8 consumer warps + a producer warpgroup; setmaxnreg moves registers from the
