@@ -25,6 +25,10 @@
 namespace qg {
 
 constexpr int kTc2Stages = 4;
+#ifndef QG_TC2_GROUP
+#define QG_TC2_GROUP 4  // swept 2-16 at c3: 4 reads 38 GB from DRAM (8: 56, 16: 105) and is fastest
+#endif
+constexpr int kTc2GroupM = QG_TC2_GROUP;  // pair-rows (256 rows each) per raster group
 constexpr uint32_t kTc2ABytes = kTcChunkBytes;       // 32 KB: this CTA's 128 rows, 8 planes
 constexpr uint32_t kTc2BBytes = kTcChunkBytes / 2;   // 16 KB: this CTA's 64 columns, 8 planes
 constexpr int kTc2AFloats = kTcChunkFloats;
@@ -98,10 +102,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kTcThreads, 1)
   const int64_t pid = int64_t(blockIdx.x) >> 1;
   int64_t pm, pn;
   {
-    const int64_t per_group = int64_t(kTcGroupM) * args.NT;
+    const int64_t per_group = int64_t(kTc2GroupM) * args.NT;
     const int64_t g = pid / per_group;
-    const int64_t first_m = g * kTcGroupM;
-    const int64_t gsz = (args.MT2 - first_m) < kTcGroupM ? (args.MT2 - first_m) : kTcGroupM;
+    const int64_t first_m = g * kTc2GroupM;
+    const int64_t gsz = (args.MT2 - first_m) < kTc2GroupM ? (args.MT2 - first_m) : kTc2GroupM;
     const int64_t in = pid - g * per_group;
     pm = first_m + in % gsz;
     pn = in / gsz;
