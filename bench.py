@@ -232,7 +232,7 @@ def make_roofline(precision, achieved, main_ms, step_ms, pack_ms, steps):
                 "pack_ms_per_step": pack_ms / max(1, steps)}
     # FP32: tcgen05 kind::tf32, 3 MMAs per real product (3xTF32)
     mma = 3 * achieved if achieved else None
-    return {"bound": "tensor", "kernel": "qgemm_tc32_kernel", "achieved": mma,
+    return {"bound": "tensor", "kernel": "qgemm_tc32_2cta_kernel", "achieved": mma,
             "peak": TF32_PEAK_TFLOPS, "unit": "TFLOP/s", "frac": (mma / TF32_PEAK_TFLOPS) if mma else None,
             "achieved_algorithmic": achieved,
             "frac_algorithmic": (achieved / TF32_PEAK_TFLOPS) if achieved else None,
