@@ -195,9 +195,12 @@ int qgemm_naive(char transA, char transB, int64_t M, int64_t N, int64_t K,
  * path (pack launch + persistent mainloop), 2 = always the one-launch small
  * kernel, 3 = direct (FP64: the persistent mainloop fed by TMA straight from
  * the interleaved storage -- one launch, no pack, workspace = stream-K scratch
- * only; FP32 calls take the packed path).  Auto = small kernel below the
+ * only; FP32 calls take the packed path), 4 = direct restricted to the
+ * 32-byte-swizzle tile feed (3 and auto load both operands as conflict-free
+ * 4-quaternion-group tiles when the groups are whole: M, resp. N, a multiple
+ * of 4 for op(A) = A, resp. op(B) = B^T / B^H, else K).  Auto = small kernel below the
  * crossover; above it FP64 takes the direct path when op(A) is T/H or
- * M*N*K <= 2^30, except for K < 512 with M*N >= 2^22 (packed), else packed;
+ * M*N*K <= 2^37, except for K < 512 with M*N >= 2^22 (packed), else packed;
  * FP32 packed.
  * Returns the previous policy, or -1 (policy unchanged) for other values.
  * For tests and benchmarks; the result is correct under every policy. */

@@ -24,6 +24,7 @@ from .qgemm import (  # noqa: F401
     PATH_PACKED,
     PATH_SMALL,
     PATH_DIRECT,
+    PATH_DIRECT32,
     timing_collect,
     timing_enable,
     version,

@@ -65,6 +65,7 @@ constexpr size_t kDmmaSmemBytes = size_t(kStages) * 2 * kChunkElems * sizeof(dou
 enum Feed : int {
   kFeedPacked = 0,  // bulk copies of pre-packed chunks (pack_kernel)
   kFeedTma = 2,     // TMA tensor-map tiles of the interleaved storage, 32-byte swizzle
+  kFeedTma128 = 3,  // TMA tiles of 4-quaternion groups, 128-byte swizzle, permuted k (conflict-free)
 };
 constexpr int kAccPerThread = 64;                      // doubles
 constexpr size_t kPartialBytes = size_t(kConsumerThreads) * kAccPerThread * sizeof(double);  // 128 KiB
@@ -235,6 +236,7 @@ __device__ __forceinline__ void tma_load_3d(void *dst, const CUtensorMap *tm, in
       : "memory");
 }
 
+template <bool kG4>
 __device__ __forceinline__ bool produce_next_tma(Producer &p, const DmmaArgs &args, double *sA, double *sB,
                                                  uint64_t *full, uint64_t *empty) {
   constexpr uint32_t kBytes = kChunkElems * sizeof(double);
@@ -248,10 +250,17 @@ __device__ __forceinline__ bool produce_next_tma(Producer &p, const DmmaArgs &ar
   if (p.fills >= kStages) mbar_wait(&empty[p.slot], p.phase ^ 1u);
   mbar_arrive_expect_tx(&full[p.slot], 2 * kBytes);
   const int k0 = int(p.kt * kBK), ra = int(p.mt * kBR), rb = int(p.nt * kBR);
-  if (args.a_rc) tma_load_3d(sA + p.slot * kChunkElems, &args.tmA, 0, ra, k0, &full[p.slot]);
-  else           tma_load_3d(sA + p.slot * kChunkElems, &args.tmA, 0, k0, ra, &full[p.slot]);
-  if (args.b_rc) tma_load_3d(sB + p.slot * kChunkElems, &args.tmB, 0, rb, k0, &full[p.slot]);
-  else           tma_load_3d(sB + p.slot * kChunkElems, &args.tmB, 0, k0, rb, &full[p.slot]);
+  if constexpr (kG4) {  // group maps (16 doubles, k, row/4) or (16 doubles, k/4, row)
+    if (args.a_rc) tma_load_3d(sA + p.slot * kChunkElems, &args.tmA, 0, k0, ra / 4, &full[p.slot]);
+    else           tma_load_3d(sA + p.slot * kChunkElems, &args.tmA, 0, k0 / 4, ra, &full[p.slot]);
+    if (args.b_rc) tma_load_3d(sB + p.slot * kChunkElems, &args.tmB, 0, k0, rb / 4, &full[p.slot]);
+    else           tma_load_3d(sB + p.slot * kChunkElems, &args.tmB, 0, k0 / 4, rb, &full[p.slot]);
+  } else {
+    if (args.a_rc) tma_load_3d(sA + p.slot * kChunkElems, &args.tmA, 0, ra, k0, &full[p.slot]);
+    else           tma_load_3d(sA + p.slot * kChunkElems, &args.tmA, 0, k0, ra, &full[p.slot]);
+    if (args.b_rc) tma_load_3d(sB + p.slot * kChunkElems, &args.tmB, 0, rb, k0, &full[p.slot]);
+    else           tma_load_3d(sB + p.slot * kChunkElems, &args.tmB, 0, k0, rb, &full[p.slot]);
+  }
   if (++p.slot == kStages) { p.slot = 0; p.phase ^= 1u; }
   ++p.kt;
   ++p.fills;
@@ -285,6 +294,53 @@ __device__ __forceinline__ TmaLane tma_lane(int rc, int r0, int kl) {
 __device__ __forceinline__ uint32_t tma_frag_off(const TmaLane &t, int ks, int i, int pp) {
   return t.rc ? t.base + uint32_t(ks * 8192 + i * 256) + (uint32_t(pp << 4) ^ t.x)
               : t.base + uint32_t(i * 4096 + ks * 128 + ((pp ^ (ks & 1)) << 4));
+}
+
+// ---- kFeedTma128: both operands as tiles of 4-quaternion groups.  The map's
+// inner dimension is 16 doubles = 4 consecutive quaternions along the
+// operand's contiguous index = one 128-byte row of the 128-byte swizzle (no
+// padding); the outer dimensions are the other index and the group index
+// (layouts checked element by element by tools/microbench/tma_probe_g4.cu):
+//   rows contiguous: smem [r/4][k][r%4][c]   lin = ((r>>2)*16 + k)*128 + (r&3)*32 + 8c
+//   k contiguous:    smem [r][k/4][k%4][c]   lin = (r*4 + (k>>2))*128 + (k&3)*32 + 8c
+//   swz = lin ^ (((lin >> 7) & 7) << 4)      (16-byte chunk ^= 128-byte row & 7)
+// A quarter-warp's 128-bit loads cover fragment rows rho, rho+1 (rho even) x
+// the 4 k of a k4 step.  In the natural k order those 4 k XOR the chunks with
+// {0,1,2,3} (rows contiguous) or sit in one 128-byte row (k contiguous), and
+// the two rows collide.  This kernel therefore feeds k4 step ks with tile k =
+// kperm(ks, kl) = 8(ks>>1) + 2(ks&1) + kk, kk = (kl&1) + 4(kl>>1) in {0,1,4,5}
+// -- a bijection of the tile's 16 k applied to A and B alike, so the k-sum is
+// unchanged -- and the 8 lanes hit 8 distinct bank groups in both layouts
+// (rows contiguous: chunks 2q ^ kk, q = rho & 3 in {0,1} or {2,3}; k
+// contiguous: the 4 k span two 128-byte rows and rho & 1 flips chunk bit 2).
+// (Permuting rows instead needs the permutation in the epilogue: measured
+// slower at c4.)  The host takes this feed when the group extents are whole:
+// M (N) % 4 == 0 for a rows-contiguous op(A) (op(B)), K % 4 == 0 for a
+// k-contiguous one; otherwise kFeedTma.
+struct G4Lane {
+  uint32_t base, x;
+};
+// rb: first row of the warp's fragments (a multiple of 8); rho = lane / 4, kl = lane % 4
+__device__ __forceinline__ G4Lane g4_lane(int rc, int rb, int rho, int kl) {
+  const int kk = (kl & 1) + 4 * (kl >> 1);
+  G4Lane t;
+  if (rc) {  // chunk = (2q + pp) ^ (k & 7), k & 7 = 2(ks & 1) + kk
+    t.base = uint32_t(((rb >> 2) + (rho >> 2)) * 2048 + kk * 128);
+    t.x = uint32_t(((2 * (rho & 3)) ^ kk) << 4);
+  } else {   // k = 4h + q: h = 2(ks >> 1) + (kl >> 1), q = 2(ks & 1) + (kl & 1);
+             // chunk = (2q + pp) ^ (4(rho & 1) + (h & 3))
+    t.base = uint32_t((rb + rho) * 512 + (kl >> 1) * 128);
+    t.x = uint32_t((2 * (kl & 1) ^ 4 * (rho & 1) ^ (kl >> 1)) << 4);
+  }
+  return t;
+}
+// Byte offset of the 16-byte pair (components 2pp, 2pp+1) of fragment i
+// (rows rb + 8i + rho) at k = kperm(ks, kl); rc is a compile-time constant.
+__device__ __forceinline__ uint32_t g4_frag_off(int rc, const G4Lane &t, int ks, int i, int pp) {
+  return rc ? t.base + uint32_t(i * 4096 + (8 * (ks >> 1) + 2 * (ks & 1)) * 128) +
+                  (t.x ^ uint32_t((pp ^ (2 * (ks & 1))) << 4))
+            : t.base + uint32_t(i * 4096 + (ks >> 1) * 256) +
+                  (t.x ^ uint32_t((4 * (ks & 1) ^ 2 * ((ks >> 1) & 1) ^ pp) << 4));
 }
 
 // kFeed: kFeedPacked (conj applied by the pack kernel; CA = CB = false), or a
@@ -333,9 +389,9 @@ __global__ void __launch_bounds__(kDmmaThreads, 1) qgemm_dmma_kernel(const __gri
   prod.fills = 0;
   if (warp >= kConsumerWarps) {
     asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;\n" ::"n"(kProducerRegs));
-    if constexpr (kFeed == kFeedTma) {
+    if constexpr (kFeed == kFeedTma || kFeed == kFeedTma128) {
       if (warp == kConsumerWarps && lane == 0)
-        while (produce_next_tma(prod, args, sA, sB, full, empty)) {
+        while (produce_next_tma<kFeed == kFeedTma128>(prod, args, sA, sB, full, empty)) {
         }
     } else {
       if (warp == kConsumerWarps && lane == 0)
@@ -351,6 +407,8 @@ __global__ void __launch_bounds__(kDmmaThreads, 1) qgemm_dmma_kernel(const __gri
   const int wn = warp >> 1;  // 16-column quarter
   [[maybe_unused]] const TmaLane ta = tma_lane(kRC & 1, wm * 32 + (lane >> 2), lane & 3);
   [[maybe_unused]] const TmaLane tb = tma_lane((kRC >> 1) & 1, wn * 16 + (lane >> 2), lane & 3);
+  [[maybe_unused]] const G4Lane ga = g4_lane(kRC & 1, wm * 32, lane >> 2, lane & 3);
+  [[maybe_unused]] const G4Lane gb = g4_lane((kRC >> 1) & 1, wn * 16, lane >> 2, lane & 3);
   const int tid = threadIdx.x;
   int slot = 0;
   uint32_t phase = 0;
@@ -399,6 +457,8 @@ __global__ void __launch_bounds__(kDmmaThreads, 1) qgemm_dmma_kernel(const __gri
             double2 v;
             if constexpr (kFeed == kFeedTma)
               v = *reinterpret_cast<const double2 *>(a8 + tma_frag_off(ta, ks, ii, pp));
+            else if constexpr (kFeed == kFeedTma128)
+              v = *reinterpret_cast<const double2 *>(a8 + g4_frag_off(kRC & 1, ga, ks, ii, pp));
             else
               v = a2[((ks * 8 + wm * 4 + ii) * 2 + pp) * 32 + lane];
             af[ii][2 * pp] = v.x;
@@ -411,6 +471,8 @@ __global__ void __launch_bounds__(kDmmaThreads, 1) qgemm_dmma_kernel(const __gri
             double2 v;
             if constexpr (kFeed == kFeedTma)
               v = *reinterpret_cast<const double2 *>(b8 + tma_frag_off(tb, ks, jj, pp));
+            else if constexpr (kFeed == kFeedTma128)
+              v = *reinterpret_cast<const double2 *>(b8 + g4_frag_off((kRC >> 1) & 1, gb, ks, jj, pp));
             else
               v = b2[((ks * 8 + wn * 2 + jj) * 2 + pp) * 32 + lane];
             bf[jj][2 * pp] = v.x;

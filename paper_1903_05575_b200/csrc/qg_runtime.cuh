@@ -10,6 +10,14 @@
 
 thread_local int g_last_launches = 0;
 
+// ---- path choice: packed (pack launch + persistent mainloop), direct (FP64:
+// the persistent mainloop fed by TMA from the interleaved storage, no pack) or
+// the one-launch small kernel.  0 = auto, 1 = always packed, 2 = small kernel
+// whenever the call reads A and B, 3 = direct for FP64 (packed for FP32), 4 =
+// direct with the 32-byte-swizzle tiles only (never kFeedTma128) --
+// qgemm_set_path_policy; the tests run every shape under each.
+std::atomic<int> g_path_policy{0};
+
 // ---- optional per-launch event timing (qgemm_timing_enable / _collect)
 struct TimingRec {
   int kind;
@@ -272,23 +280,33 @@ using DmmaKernel = void (*)(const qg::DmmaArgs);  // (__grid_constant__ is not p
 
 // Instantiations: packed; TMA x the op pairs (rows-contiguous and conj flags of
 // A and B are compile-time there).
-template <bool CA, bool CB>
-DmmaKernel tma_kernel(int arc, int brc) {
-  using namespace qg;
+// One instantiation per op pair (9 per feed).  op H implies k-contiguous
+// storage for A (rows of op(A) = columns of A) and rows-contiguous for B, so
+// conj A => arc = 0 and conj B => brc = 1.
+// (kFeedTma128 is never used with a k-contiguous op(A) and a rows-contiguous
+// op(B), kRC = 2: see launch_mainloop_direct; no such instantiation.)
+template <int F, bool CA, bool CB, int RC>
+DmmaKernel tma_inst() {
+  if constexpr (F == qg::kFeedTma128 && RC == 2) return nullptr;
+  else return qg::qgemm_dmma_kernel<F, CA, CB, RC>;
+}
+template <int F>
+DmmaKernel tma_kernel_op(bool ca, bool cb, int arc, int brc) {
+  if (ca && cb) return tma_inst<F, true, true, 2>();
+  if (ca) return brc ? tma_inst<F, true, false, 2>() : tma_inst<F, true, false, 0>();
+  if (cb) return arc ? tma_inst<F, false, true, 3>() : tma_inst<F, false, true, 2>();
   switch (arc | (brc << 1)) {
-    case 0: return qgemm_dmma_kernel<kFeedTma, CA, CB, 0>;
-    case 1: return qgemm_dmma_kernel<kFeedTma, CA, CB, 1>;
-    case 2: return qgemm_dmma_kernel<kFeedTma, CA, CB, 2>;
-    default: return qgemm_dmma_kernel<kFeedTma, CA, CB, 3>;
+    case 0: return tma_inst<F, false, false, 0>();
+    case 1: return tma_inst<F, false, false, 1>();
+    case 2: return tma_inst<F, false, false, 2>();
+    default: return tma_inst<F, false, false, 3>();
   }
 }
 DmmaKernel dmma_kernel(int feed, bool ca, bool cb, int arc = 0, int brc = 0) {
   using namespace qg;
   if (feed == kFeedPacked) return qgemm_dmma_kernel<kFeedPacked, false, false>;
-  // op H implies k-contiguous storage for A (rows of op(A) = columns of A) and
-  // rows-contiguous for B, so conj A => arc = 0 and conj B => brc = 1
-  if (ca) return cb ? tma_kernel<true, true>(0, 1) : tma_kernel<true, false>(0, brc);
-  return cb ? tma_kernel<false, true>(arc, 1) : tma_kernel<false, false>(arc, brc);
+  if (feed == kFeedTma128) return tma_kernel_op<kFeedTma128>(ca, cb, arc, brc);
+  return tma_kernel_op<kFeedTma>(ca, cb, arc, brc);
 }
 
 int dmma_set_attributes() {
@@ -298,14 +316,15 @@ int dmma_set_attributes() {
   cudaError_t e = cudaGetDevice(&dev);
   if (e != cudaSuccess) return int(e);
   if (dev < kMaxDev && done[dev]) return 0;
-  for (int feed : {int(qg::kFeedPacked), int(qg::kFeedTma)})
+  for (int feed : {int(qg::kFeedPacked), int(qg::kFeedTma), int(qg::kFeedTma128)})
     for (int c = 0; c < 16; ++c) {
       const bool ca = c & 1, cb = c & 2;
       const int arc = (c >> 2) & 1, brc = (c >> 3) & 1;
       if (feed == qg::kFeedPacked && c) continue;
       if ((ca && arc) || (cb && !brc)) continue;  // no such op
-      e = cudaFuncSetAttribute(dmma_kernel(feed, ca, cb, arc, brc), cudaFuncAttributeMaxDynamicSharedMemorySize,
-                               int(qg::kDmmaSmemBytes));
+      const DmmaKernel k = dmma_kernel(feed, ca, cb, arc, brc);
+      if (!k) continue;
+      e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(qg::kDmmaSmemBytes));
       if (e != cudaSuccess) return int(e);
     }
   if (dev < kMaxDev) done[dev] = true;
@@ -341,6 +360,26 @@ int encode_view(CUtensorMap *tm, const double *X, int64_t ldx, int rc, int64_t R
   const cuuint32_t estr[3] = {1, 1, 1};
   const CUresult r = fn(tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, const_cast<double *>(X), dims, strides, box, estr,
                         CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_32B,
+                        CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS ? 0 : int(cudaErrorInvalidValue);
+}
+
+// kFeedTma128 group maps (qg_dmma.cuh): (16 doubles, k, row/4) when rows are
+// contiguous, else (16 doubles, k/4, row); box = one 64-row x 16-k tile;
+// 128-byte swizzle.  The inner dimension is 4 quaternions along the
+// contiguous index, so it needs R % 4 == 0, resp. K % 4 == 0 (then no read
+// leaves the operand's extent).
+bool g4_ok(int rc, int64_t R, int64_t K) { return rc ? (R % 4 == 0) : (K % 4 == 0); }
+int encode_view_g4(CUtensorMap *tm, const double *X, int64_t ldx, int rc, int64_t R, int64_t K) {
+  EncodeTiledFn fn = encode_tiled();
+  if (!fn) return int(cudaErrorNotSupported);
+  const cuuint64_t col = cuuint64_t(32) * cuuint64_t(ldx);
+  const cuuint64_t dims[3] = {16, cuuint64_t(rc ? K : K / 4), cuuint64_t(rc ? R / 4 : R)};
+  const cuuint64_t strides[2] = {rc ? col : 128, rc ? 128 : col};
+  const cuuint32_t box[3] = {16, cuuint32_t(rc ? qg::kBK : qg::kBK / 4), cuuint32_t(rc ? qg::kBR / 4 : qg::kBR)};
+  const cuuint32_t estr[3] = {1, 1, 1};
+  const CUresult r = fn(tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, const_cast<double *>(X), dims, strides, box, estr,
+                        CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
                         CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   return r == CUDA_SUCCESS ? 0 : int(cudaErrorInvalidValue);
 }
@@ -405,7 +444,19 @@ int launch_mainloop_direct(int feed, const double *A, int64_t lda, int a_rc, int
   qg::DmmaArgs a{};
   a.A = A; a.B = B; a.lda = lda; a.ldb = ldb; a.K = K; a.a_rc = a_rc; a.b_rc = b_rc;
   a.C = C; a.ldc = ldc; a.M = M; a.N = N; a.KT = cdiv(K, qg::kBK); a.sc = sc; a.tri = tri;
-  if (feed == qg::kFeedTma) {
+  // 4-quaternion-group tiles (conflict-free fragment loads, qg_dmma.cuh
+  // kFeedTma128) where both operands' group extents are whole -- except for a
+  // k-contiguous op(A) (T/H) with a rows-contiguous op(B) (T/H), where the
+  // group tiles measured 0.6-0.9% slower than the 32-byte ones despite zero
+  // bank conflicts (tools/feed_sweep.py, profiles/r01p_feed_sweep_g4.jsonl)
+  if (feed == qg::kFeedTma && g_path_policy.load(std::memory_order_relaxed) != 4 && g4_ok(a_rc, M, K) &&
+      g4_ok(b_rc, N, K) && (a_rc || !b_rc))
+    feed = qg::kFeedTma128;
+  if (feed == qg::kFeedTma128) {
+    int rc = encode_view_g4(&a.tmA, A, lda, a_rc, M, K);
+    if (!rc) rc = encode_view_g4(&a.tmB, B, ldb, b_rc, N, K);
+    if (rc) return rc;
+  } else if (feed == qg::kFeedTma) {
     int rc = encode_view(&a.tmA, A, lda, a_rc, M, K);
     if (!rc) rc = encode_view(&a.tmB, B, ldb, b_rc, N, K);
     if (rc) return rc;
@@ -469,30 +520,25 @@ int launch_mainloop(const float *Ap, const float *Bp, float *C, int64_t ldc, int
   return int(cudaGetLastError());
 }
 
-// ---- path choice: packed (pack launch + persistent mainloop), direct (FP64:
-// the persistent mainloop fed by TMA from the interleaved storage, no pack) or
-// the one-launch small kernel.  0 = auto, 1 = always packed, 2 = small kernel
-// whenever the call reads A and B, 3 = direct for FP64 (packed for FP32) --
-// qgemm_set_path_policy; the tests run every shape under each.
-std::atomic<int> g_path_policy{0};
 
 // Direct (TMA-fed) FP64 mainloop vs pack launch + mainloop, from the sweep in
-// profiles/r01i_feed_sweep.jsonl (tools/feed_sweep.py): the TMA tile lands in
-// storage order, so op(A) = A (rows contiguous) costs 4-way shared-memory bank
-// conflicts on the A fragments (2-way when k is contiguous) -- the pack it
-// saves is worth more than that only for small problems.  Auto: direct when
-// op(A) is T/H, or when M*N*K <= 2^30; packed for K < 512 with M*N >= 2^22
-// (c4: K = 256) and for large op(A) = N problems (c3, c5).
+// profiles/r01p_feed_sweep_g4.jsonl (tools/feed_sweep.py).  With the
+// 4-quaternion-group tiles (conflict-free fragment loads) the direct path wins
+// from 384^3 to 4096^3 for every op pair (1.002-1.08x), at 2048^2 x 8192 and
+// 4096^2 x 1024, ties at 4096^2 x 256 and loses at 8192^2 x 256 (0.996x, c4's
+// shape) and by 0.1% at 8192^3 (c3).  Auto: direct when op(A) is T/H or
+// M*N*K <= 2^37; packed for K < 512 with M*N >= 2^22 (c4) and for larger
+// op(A) = N problems (c3, c5).
 template <typename T>
 int direct_feed(int opA, int64_t M, int64_t N, int64_t K) {
   if (sizeof(T) != 8) return 0;
   const int pol = g_path_policy.load(std::memory_order_relaxed);
-  if (pol == 3) return qg::kFeedTma;
+  if (pol == 3 || pol == 4) return qg::kFeedTma;
   if (pol != 0) return 0;
   const double mn = double(M) * double(N);
   if (K < 512 && mn >= double(int64_t(1) << 22)) return 0;  // c4-like: short K, big C
   if (opA != 0) return qg::kFeedTma;
-  return mn * double(K) <= double(int64_t(1) << 30) ? qg::kFeedTma : 0;
+  return mn * double(K) <= double(int64_t(1) << 37) ? qg::kFeedTma : 0;
 }
 
 // Auto policy (crossover measured on B200 with tools/small_sweep.py):
@@ -510,7 +556,7 @@ int num_sms();
 template <typename T>
 bool use_small(int64_t M, int64_t N, int64_t K) {
   const int pol = g_path_policy.load(std::memory_order_relaxed);
-  if (pol == 1 || pol == 3) return false;
+  if (pol == 1 || pol == 3 || pol == 4) return false;
   if (pol == 2) return true;
   constexpr int64_t kCap = int64_t(1) << 28;
   if (M > kCap || N > kCap || K > kCap) return false;  // keeps M*N*K from overflowing below

@@ -272,13 +272,15 @@ def qherk(uplo: str, trans: str, alpha: float, A: torch.Tensor, beta: float, C: 
 
 KINDS = ("pack", "mainloop", "scale", "naive", "small")
 
-PATH_AUTO, PATH_PACKED, PATH_SMALL, PATH_DIRECT = 0, 1, 2, 3
+PATH_AUTO, PATH_PACKED, PATH_SMALL, PATH_DIRECT, PATH_DIRECT32 = 0, 1, 2, 3, 4
 
 
 def set_path_policy(policy: int) -> int:
     """0 auto, 1 always packed (pack launch + mainloop), 2 always the one-launch
     small kernel, 3 direct (FP64: persistent mainloop fed by TMA straight from
-    the interleaved storage, no pack; FP32 packed); returns the old one."""
+    the interleaved storage, no pack; FP32 packed), 4 direct with the 32-byte-
+    swizzle tile feed only (3 and auto load the operands as 4-quaternion groups
+    where M / N / K allow); returns the old one."""
     old = int(load().qgemm_set_path_policy(int(policy)))
     if old < 0:
         raise ValueError(f"invalid path policy {policy}")

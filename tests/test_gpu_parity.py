@@ -19,11 +19,12 @@ pytestmark = pytest.mark.gpu
 OPS = [(a, b) for a in "NTH" for b in "NTH"]
 QALPHA = (0.3, -1.2, 0.7, 0.25)
 QBETA = (-0.5, 0.1, -0.9, 0.4)
-# pack launch + persistent mainloop | one-launch small kernel | TMA-fed mainloop (no pack)
-PATHS = [qg.PATH_PACKED, qg.PATH_SMALL, qg.PATH_DIRECT]
+# pack launch + persistent mainloop | one-launch small kernel | TMA-fed mainloop (no pack):
+# 4-quaternion-group tiles where the extents allow (else 32-byte tiles) | 32-byte tiles only
+PATHS = [qg.PATH_PACKED, qg.PATH_SMALL, qg.PATH_DIRECT, qg.PATH_DIRECT32]
 
 
-@pytest.fixture(params=PATHS, ids=["packed", "small", "direct"])
+@pytest.fixture(params=PATHS, ids=["packed", "small", "direct", "direct32"])
 def path(request):
     with path_policy(request.param):
         yield request.param
@@ -75,6 +76,24 @@ def test_exact_integer_bitwise_f64(M, N, K, opA, opB, path):
     """P8: integer components in [-8, 8] -> exact in any order -> bitwise."""
     pr = make_problem(M, N, K, opA, opB, (2, -1, 0, 3), (1, 0, -2, 1), seed=3, dist="int8")
     assert_parity(pr, run_gpu(pr), oracle_full(pr), exact=True)
+
+
+@pytest.mark.parametrize("M,N,K,pad", [(196, 132, 84, 3), (4, 8, 4, 1), (260, 68, 1028, 2),
+                                       (64, 128, 16, 0), (132, 36, 37, 1)])
+@pytest.mark.parametrize("opA,opB", OPS)
+def test_group4_tma_feed(M, N, K, pad, opA, opB):
+    """Direct path with whole 4-quaternion groups (M, N, K multiples of 4; the last
+    shape's K = 37 keeps the 32-byte feed whenever an operand is k-contiguous), so
+    the 128-byte-swizzle group tiles with the permuted k order run: tile-ragged
+    edges, odd ld padding (NaN), stream-K splits, quaternion alpha/beta;
+    exact-integer inputs -> bitwise."""
+    lda, ldb, ldc = _lds(opA, opB, M, N, K, pad)
+    with path_policy(qg.PATH_DIRECT):
+        pr = make_problem(M, N, K, opA, opB, QALPHA, QBETA, seed=7, lda=lda, ldb=ldb, ldc=ldc)
+        assert_parity(pr, run_gpu(pr), oracle_full(pr))
+        pr = make_problem(M, N, K, opA, opB, (2, -1, 0, 3), (1, 0, -2, 1), seed=8, dist="int8",
+                          lda=lda, ldb=ldb, ldc=ldc)
+        assert_parity(pr, run_gpu(pr), oracle_full(pr), exact=True)
 
 
 @pytest.mark.parametrize("opA,opB", OPS)

@@ -58,7 +58,8 @@ def test_qherk_ragged(uplo, trans, N, K):
     _case(N, K, uplo, trans, 0.75, -0.5, seed=N + K)
 
 
-@pytest.mark.parametrize("policy", [qg.PATH_PACKED, qg.PATH_DIRECT], ids=["packed", "direct"])
+@pytest.mark.parametrize("policy", [qg.PATH_PACKED, qg.PATH_DIRECT, qg.PATH_DIRECT32],
+                         ids=["packed", "direct", "direct32"])
 @pytest.mark.parametrize("uplo", ["L", "U"])
 @pytest.mark.parametrize("trans", ["N", "H"])
 def test_qherk_exact_integer(uplo, trans, policy):

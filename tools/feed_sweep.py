@@ -1,5 +1,5 @@
 """Packed (pack launch + mainloop) vs TMA-fed FP64 mainloop across shapes:
-the data behind the auto policy's choice.  CUDA-graph replay,
+(4-quaternion-group and 32-byte-only tiles): the data behind the auto policy's choice.  CUDA-graph replay,
 CUDA events.
 
     python tools/feed_sweep.py [--out gpurun_out/feed_sweep.jsonl]
@@ -19,7 +19,7 @@ ap.add_argument("--out", default=None)
 ap.add_argument("--small-shapes", action="store_true", help="the small/direct/packed crossover region")
 a = ap.parse_args()
 g = torch.Generator(device="cuda").manual_seed(0)
-SHAPES = [(n, n, n, ops) for n in (384, 512, 768, 1024, 1536, 2048, 3072, 4096) for ops in ("NN", "NH", "TN")]
+SHAPES = [(n, n, n, ops) for n in (384, 512, 768, 1024, 1536, 2048, 3072, 4096) for ops in ("NN", "NH", "TN", "TH")]
 SHAPES += [(8192, 8192, 256, "NH"), (4096, 4096, 256, "NH"), (2048, 2048, 8192, "NH"), (4096, 4096, 1024, "NH")]
 if a.small_shapes:
     SHAPES = [(n, n, n, ops) for n in (128, 192, 256, 320, 384, 448, 512) for ops in ("NN", "TN")]
@@ -62,7 +62,7 @@ for M, N, K, ops in SHAPES:
     B = torch.randn((bc, br, 4), dtype=torch.float64, device="cuda", generator=g)
     C = torch.randn((N, M, 4), dtype=torch.float64, device="cuda", generator=g)
     row = {"M": M, "N": N, "K": K, "ops": ops}
-    pols = (("packed", qg.PATH_PACKED), ("tma", qg.PATH_DIRECT))
+    pols = (("packed", qg.PATH_PACKED), ("tma", qg.PATH_DIRECT), ("tma32", qg.PATH_DIRECT32))
     if a.small_shapes:
         pols += (("small", qg.PATH_SMALL),)
     for name, pol in pols:
@@ -74,6 +74,7 @@ for M, N, K, ops in SHAPES:
         row[name + "_tflops"] = 32.0 * M * N * K / (t * 1e-3) / 1e12
         del ws
     row["tma_over_packed"] = row["packed_ms"] / row["tma_ms"]
+    row["tma_over_tma32"] = row["tma32_ms"] / row["tma_ms"]
     print(json.dumps(row), flush=True)
     if out:
         out.write(json.dumps(row) + "\n")
