@@ -4,7 +4,8 @@ Inputs come from the counter-based generator (synth/gpu_gen.py) so the host can
 regenerate exactly the rows/columns the oracle needs; outputs are compared on
 sampled entries computed by the oracle one by one, plus properties that hold at
 any size (Hermiticity for c4; finiteness with a NaN-filled C and
-beta = 0 for c5).  c5 runs with a 16 GB workspace, i.e. through the K-panel loop.
+beta = 0 for c5); c4 is also checked in full, every entry against the oracle
+(~2.5 minutes).  c5 runs with a 16 GB workspace, i.e. through the K-panel loop.
 """
 from __future__ import annotations
 
@@ -63,6 +64,33 @@ def test_c4_full_size_hermitian_rank_k():
     err = float(np.abs(got - ref).max())
     assert err <= tol, (err, tol)
     del A, C
+    _free()
+
+
+def test_c4_full_size_every_entry_vs_oracle():
+    """c4 in full (SURVEY §8(c) coverage table: 'c4 full (8.8e12 flops) + P12'):
+    every one of the 32768^2 entries against the oracle, 1024 columns at a time
+    (the oracle runs on all host cores; ~2 minutes on a 16-core host).  C0 is the
+    counter-generated Hermitian matrix, copied to the host block by block."""
+    n, K, blk = 32768, 256, 1024
+    A = counter_matrix(0, 1, n, K, "cuda")
+    C0 = counter_hermitian(0, 3, n, "cuda")
+    C = C0.clone()
+    qg.qgemm("N", "H", 1.0, A, A, 1.0, C, M=n, N=n, K=K)
+    torch.cuda.synchronize()
+    A_h = A.cpu().numpy()                                  # stored n x K: (K, n, 4)
+    maxa = float(np.abs(A_h).max())
+    tol = 1e-12 * K * maxa * maxa + 8 * 2.0 ** -53 * float(C0.abs().max()) * 4
+    worst = 0.0
+    for j0 in range(0, n, blk):
+        # columns j0.. of op(B) = A^H are rows j0.. of stored A, op H
+        B_blk = np.ascontiguousarray(A_h[:, j0:j0 + blk, :])   # (K, blk, 4)
+        ref = C0[j0:j0 + blk].cpu().numpy()                    # (blk, n, 4), beta = 1
+        oracle.qgemm("N", "H", n, blk, K, 1, A_h, B_blk, 1, ref)
+        got = C[j0:j0 + blk].cpu().numpy()
+        worst = max(worst, float(np.abs(got - ref).max()))
+        assert worst <= tol, (j0, worst, tol)
+    del A, C0, C
     _free()
 
 
