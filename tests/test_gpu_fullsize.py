@@ -70,15 +70,17 @@ def test_c4_full_size_hermitian_rank_k():
 def test_c4_full_size_every_entry_vs_oracle():
     """c4 in full (SURVEY §8(c) coverage table: 'c4 full (8.8e12 flops) + P12'):
     every one of the 32768^2 entries against the oracle, 1024 columns at a time
-    (the oracle runs on all host cores; ~2 minutes on a 16-core host).  C0 is the
-    counter-generated Hermitian matrix, copied to the host block by block."""
+    (the oracle runs on all host cores; ~2.5 minutes on a 16-core host).  C0 is the
+    counter-generated Hermitian matrix (the seeded generator's torch twin, bitwise
+    equal to the host one: test_counter_generator_device_matches_host), copied to
+    the host block by block."""
     n, K, blk = 32768, 256, 1024
     A = counter_matrix(0, 1, n, K, "cuda")
     C0 = counter_hermitian(0, 3, n, "cuda")
     C = C0.clone()
     qg.qgemm("N", "H", 1.0, A, A, 1.0, C, M=n, N=n, K=K)
     torch.cuda.synchronize()
-    A_h = A.cpu().numpy()                                  # stored n x K: (K, n, 4)
+    A_h = counter_matrix(0, 1, n, K, "cpu").numpy()        # stored n x K: (K, n, 4), host generator
     maxa = float(np.abs(A_h).max())
     tol = 1e-12 * K * maxa * maxa + 8 * 2.0 ** -53 * float(C0.abs().max()) * 4
     worst = 0.0
