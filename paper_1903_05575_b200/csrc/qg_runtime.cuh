@@ -580,8 +580,11 @@ int num_sms() {
   return sms;
 }
 
+#ifndef QG_SMALL_MIN_STEPS
+#define QG_SMALL_MIN_STEPS 2  // k4 steps per warp at least (after the split)
+#endif
 #ifndef QG_SMALL_CTAS_PER_SM
-#define QG_SMALL_CTAS_PER_SM 4
+#define QG_SMALL_CTAS_PER_SM (16 / QG_SMALL_WARPS)  // resident at <= 128 registers
 #endif
 
 template <typename T>
@@ -597,12 +600,14 @@ int launch_small(const T *A, int64_t lda, int a_rc, int a_cj, const T *B, int64_
   const int64_t tm = cdiv(M, 8), tn = cdiv(N, 8), steps = cdiv(K, 4);
   const int64_t sms = num_sms();
   // split K over more warps while the grid still fits one wave of resident
-  // CTAs (4 per SM at <= 128 registers) and each warp keeps >= 2 k4 steps:
+  // CTAs (QG_SMALL_CTAS_PER_SM per SM) and each warp keeps >= QG_SMALL_MIN_STEPS k4 steps:
   // shorter per-warp load->DMMA chains, same number of waves
+  constexpr int W = qg::kSmallWarps;
   int S = 1;
-  while (S < 4 && cdiv(tm, 4 / (2 * S)) * tn <= QG_SMALL_CTAS_PER_SM * sms && steps >= 4 * S) S *= 2;
+  while (S < W && cdiv(tm, W / (2 * S)) * tn <= QG_SMALL_CTAS_PER_SM * sms && steps >= 2 * QG_SMALL_MIN_STEPS * S)
+    S *= 2;
   a.S = S;
-  a.m_blocks = cdiv(tm, 4 / S);
+  a.m_blocks = cdiv(tm, W / S);
   const int64_t blocks = a.m_blocks * tn;
   if (blocks > INT32_MAX) return int(cudaErrorInvalidConfiguration);
   { int ti = tstart(kSmall, st);

@@ -19,9 +19,9 @@
 // FP32 storage: quaternions are widened to double on load and the FP64 result
 // is rounded once on store -- more accurate than the FP32 tolerance requires.
 //
-// CTA = 4 warps.  With split factor S in {1, 2, 4} (host: as large as keeps the
-// grid within one wave of resident CTAs), warp w computes the 8x8 tile
-// (w / S) of the CTA's (4/S) M-stacked tiles over the (w % S)-th of S equal
+// CTA = W = QG_SMALL_WARPS warps.  With split factor S in {1, 2, .., W} (host: as
+// large as keeps the grid within one wave of resident CTAs), warp w computes the
+// 8x8 tile (w / S) of the CTA's (W/S) M-stacked tiles over the (w % S)-th of S equal
 // ranges of k4 steps; partials are summed in a fixed order through shared
 // memory (deterministic), then lane l applies the alpha/beta epilogue (left
 // products) to the two quaternions it owns: C(m0 + l/4, n0 + 2(l%4) + i).
@@ -30,7 +30,11 @@
 
 namespace qg {
 
-constexpr int kSmallThreads = 128;
+#ifndef QG_SMALL_WARPS
+#define QG_SMALL_WARPS 4
+#endif
+constexpr int kSmallWarps = QG_SMALL_WARPS;
+constexpr int kSmallThreads = kSmallWarps * 32;
 constexpr int kSmallUnroll = 4;  // k4 steps whose loads are issued together
 
 struct SmallArgs {
@@ -67,6 +71,25 @@ __device__ __forceinline__ void load_rk(const T *X, int64_t ldx, int rows_contig
   }
 }
 
+// The same element in two halves, so that every load of an unrolled group is
+// issued before any is consumed (a load inside a range branch followed by its
+// conj fix-up serialised the round trips: ncu long-scoreboard stalls on the
+// fix-ups, ~4x the DMMA time at c1): rk_addr clamps an out-of-range (r, k) to
+// the base pointer (a valid address; the value is discarded), rk_fix zeroes or
+// conjugates after all loads are in flight.
+template <typename T>
+__device__ __forceinline__ const T *rk_addr(const T *X, int64_t ldx, int rows_contig, int64_t r, int64_t k,
+                                            int64_t R, int64_t K, bool &ok) {
+  ok = r < R && k < K;
+  return ok ? (rows_contig ? X + 4 * (r + k * ldx) : X + 4 * (k + r * ldx)) : X;
+}
+__device__ __forceinline__ void rk_fix(bool ok, int conj, double (&q)[4]) {
+  const double s = conj ? -1.0 : 1.0;
+  q[0] = ok ? q[0] : 0.0;
+#pragma unroll
+  for (int c = 1; c < 4; ++c) q[c] = ok ? s * q[c] : 0.0;
+}
+
 // One k4 step of the 8x8 warp tile: 16 DMMA.8x8x4, acc^{p^s} += eps(p,s) A^p B^s.
 __device__ __forceinline__ void small_step(double (&acc)[4][2], const double (&qa)[4], const double (&qb)[4]) {
   double nb[4];
@@ -80,13 +103,13 @@ __device__ __forceinline__ void small_step(double (&acc)[4][2], const double (&q
 
 template <typename T>
 // (<= 128 registers: 4 CTAs per SM -- occupancy, not ILP, sets its speed; measured)
-__global__ void __launch_bounds__(kSmallThreads, 4) qgemm_small_kernel(SmallArgs a) {
+__global__ void __launch_bounds__(kSmallThreads, 512 / kSmallThreads) qgemm_small_kernel(SmallArgs a) {
   __shared__ double red[kSmallThreads / 32][32][8];
   const T *A = static_cast<const T *>(a.A);
   const T *B = static_cast<const T *>(a.B);
   T *C = static_cast<T *>(a.C);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int S = a.S, tiles_per_cta = 4 / S;
+  const int S = a.S, tiles_per_cta = kSmallWarps / S;
   const int tile = warp / S, part = warp % S;
   const int64_t mb = int64_t(blockIdx.x) % a.m_blocks, nb = int64_t(blockIdx.x) / a.m_blocks;
   const int64_t m0 = (mb * tiles_per_cta + tile) * 8;
@@ -116,11 +139,17 @@ __global__ void __launch_bounds__(kSmallThreads, 4) qgemm_small_kernel(SmallArgs
     int64_t st = s0;
     for (; st + kSmallUnroll <= s1; st += kSmallUnroll) {  // loads of 4 steps in flight
       double qa[kSmallUnroll][4], qb[kSmallUnroll][4];
+      bool oka[kSmallUnroll], okb[kSmallUnroll];
 #pragma unroll
       for (int u = 0; u < kSmallUnroll; ++u) {
         const int64_t k = (st + u) * 4 + lk;
-        load_rk(A, a.lda, a.a_rc, a.a_cj, m0 + lr, k, a.M, a.K, qa[u]);
-        load_rk(B, a.ldb, a.b_rc, a.b_cj, n0 + lr, k, a.N, a.K, qb[u]);
+        ld_quat_d(rk_addr(A, a.lda, a.a_rc, m0 + lr, k, a.M, a.K, oka[u]), qa[u]);
+        ld_quat_d(rk_addr(B, a.ldb, a.b_rc, n0 + lr, k, a.N, a.K, okb[u]), qb[u]);
+      }
+#pragma unroll
+      for (int u = 0; u < kSmallUnroll; ++u) {
+        rk_fix(oka[u], a.a_cj, qa[u]);
+        rk_fix(okb[u], a.b_cj, qb[u]);
       }
 #pragma unroll
       for (int u = 0; u < kSmallUnroll; ++u) small_step(acc, qa[u], qb[u]);
