@@ -541,15 +541,19 @@ int direct_feed(int opA, int64_t M, int64_t N, int64_t K) {
   return mn * double(K) <= double(int64_t(1) << 37) ? qg::kFeedTma : 0;
 }
 
-// Auto policy (crossover measured on B200 with tools/small_sweep.py):
-//  * FP64: the small kernel up to 2^24 quaternion multiply-adds (256^3); the
-//    persistent DMMA mainloop (TMA-fed) wins from 320^3;
+// Auto policy (crossover measured on B200 with tools/small_sweep.py, DESIGN.md §6;
+// profiles/r01p_small_sweep_f64.jsonl):
+//  * FP64: the small kernel up to 2^25 quaternion multiply-adds (320^3: 49 us vs
+//    60 direct; tie at 384^3), for K <= 16 (C-traffic bound: 4096^2 x 2 takes
+//    350 us vs 564), and for few output tiles with long K (<= 64 tiles of 64x64,
+//    K >= 4 max(M, N): the cluster split over K beats stream-K's owner
+//    reductions, 64x64x8192: 53 us vs 332; 128x128x4096: 96 vs 153);
 //  * FP32: up to 2^25 (the tcgen05 path has a 128x128 tile and no split-K), and
 //    up to 2^28 when that path would launch fewer than 1/4 as many CTAs as
 //    there are SMs and K >= 4 max(M, N) (small M x N, long K);
 //    but not for K <= 16 with M*N >= 2^20: there the FP32 call is C-traffic
 //    bound and the packed tcgen05 epilogue streams C better.
-constexpr int64_t kSmallMaxMacs = int64_t(1) << 24;
+constexpr int64_t kSmallMaxMacs = int64_t(1) << 25;
 
 int num_sms();
 
@@ -562,9 +566,12 @@ bool use_small(int64_t M, int64_t N, int64_t K) {
   if (M > kCap || N > kCap || K > kCap) return false;  // keeps M*N*K from overflowing below
   const double macs = double(M) * double(N) * double(K);
   if (macs > double(kCap)) return false;
-  if (sizeof(T) == 8) return macs <= double(kSmallMaxMacs);  // 256^3: small 36.9 us vs direct 45
+  if (sizeof(T) == 8) {
+    if (macs <= double(kSmallMaxMacs) || K <= 16) return true;
+    return cdiv(M, 64) * cdiv(N, 64) <= 64 && K >= 4 * std::max(M, N);
+  }
   if (K <= 16 && double(M) * double(N) >= double(1 << 20)) return false;
-  if (macs <= double(2 * kSmallMaxMacs)) return true;
+  if (macs <= double(kSmallMaxMacs)) return true;
   const int64_t tc_ctas = cdiv(M, 128) * cdiv(N, 128);
   return 4 * tc_ctas < num_sms() && K >= 4 * std::max(M, N);
 }
@@ -580,6 +587,9 @@ int num_sms() {
   return sms;
 }
 
+#ifndef QG_SMALL_CLUSTER_MIN_STEPS
+#define QG_SMALL_CLUSTER_MIN_STEPS 16
+#endif
 #ifndef QG_SMALL_MIN_STEPS
 #define QG_SMALL_MIN_STEPS 2  // k4 steps per warp at least (after the split)
 #endif
@@ -609,10 +619,38 @@ int launch_small(const T *A, int64_t lda, int a_rc, int a_cj, const T *B, int64_
   a.S = S;
   a.m_blocks = cdiv(tm, W / S);
   const int64_t blocks = a.m_blocks * tn;
-  if (blocks > INT32_MAX) return int(cudaErrorInvalidConfiguration);
+  // long K with few tiles: split each tile's K over a cluster of Z CTAs too
+  // (partials summed through distributed shared memory) while the grid fits one
+  // wave and every warp keeps >= QG_SMALL_CLUSTER_MIN_STEPS k4 steps (below
+  // that the cluster launch and barriers cost more than they save: c1 4.0 us
+  // at Z = 1 vs 4.7 at Z = 2)
+  int Z = 1;
+  if (S == W)
+    while (Z < qg::kSmallMaxCluster && blocks * 2 * Z <= QG_SMALL_CTAS_PER_SM * sms &&
+           steps >= QG_SMALL_CLUSTER_MIN_STEPS * S * 2 * Z)
+      Z *= 2;
+  a.Z = Z;
+  if (blocks * Z > INT32_MAX) return int(cudaErrorInvalidConfiguration);
+  cudaError_t e = cudaSuccess;
   { int ti = tstart(kSmall, st);
-  qg::qgemm_small_kernel<T><<<unsigned(blocks), qg::kSmallThreads, 0, st>>>(a);
+  if (Z == 1) {
+    qg::qgemm_small_kernel<T, false><<<unsigned(blocks), qg::kSmallThreads, 0, st>>>(a);
+  } else {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(unsigned(blocks * Z));
+    cfg.blockDim = dim3(qg::kSmallThreads);
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = unsigned(Z);
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    e = cudaLaunchKernelEx(&cfg, qg::qgemm_small_kernel<T, true>, a);
+  }
   tstop(ti, st); }
+  if (e != cudaSuccess) return int(e);
   ++g_last_launches;
   return int(cudaGetLastError());
 }

@@ -43,6 +43,7 @@ struct SmallArgs {
   int64_t lda, ldb, ldc, M, N, K;
   int a_rc, a_cj, b_rc, b_cj;  // operand views of load_rk (from opA, opB)
   int S;                       // warps per 8x8 tile splitting K
+  int Z;                       // CTAs per 8x8 tile splitting K (a thread-block cluster; S == W when > 1)
   int64_t m_blocks;            // CTAs along M (1-D grid: m fastest)
   Scalars<double> sc;
 };
@@ -101,30 +102,57 @@ __device__ __forceinline__ void small_step(double (&acc)[4][2], const double (&q
     for (int s = 0; s < 4; ++s) dmma_8x8x4(acc[p ^ s], qa[p], hneg(p, s) ? nb[s] : qb[s]);
 }
 
-template <typename T>
+constexpr int kSmallMaxCluster = 8;
+
+__device__ __forceinline__ void cluster_arrive_relaxed() {
+  asm volatile("barrier.cluster.arrive.relaxed.aligned;\n" ::: "memory");
+}
+__device__ __forceinline__ void cluster_arrive_release() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n" ::: "memory");
+}
+__device__ __forceinline__ void cluster_wait() { asm volatile("barrier.cluster.wait.acquire.aligned;\n" ::: "memory"); }
+// Store a double into CTA `rank`'s shared memory at the address of `p` in this CTA.
+__device__ __forceinline__ void st_dsmem(const double *p, uint32_t rank, double v) {
+  uint32_t remote;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;\n" : "=r"(remote) : "r"(smem_u32(p)), "r"(rank));
+  asm volatile("st.shared::cluster.f64 [%0], %1;\n" ::"r"(remote), "d"(v) : "memory");
+}
+
+// Z > 1 (host: only when S == W, i.e. one 8x8 tile per CTA, for long K): the Z
+// CTAs of a thread-block cluster split the tile's k4 steps; ranks 1..Z-1 store
+// their CTA-reduced partial into rank 0's shared memory (DSMEM), rank 0 adds
+// them in rank order (deterministic) and runs the epilogue.
+// (kZ: a separate instantiation, so the Z = 1 kernel carries none of it.)
+template <typename T, bool kZ>
 // (<= 128 registers: 4 CTAs per SM -- occupancy, not ILP, sets its speed; measured)
 __global__ void __launch_bounds__(kSmallThreads, 512 / kSmallThreads) qgemm_small_kernel(SmallArgs a) {
   __shared__ double red[kSmallThreads / 32][32][8];
+  __shared__ double zred[kZ ? kSmallMaxCluster - 1 : 1][32][8];
   const T *A = static_cast<const T *>(a.A);
   const T *B = static_cast<const T *>(a.B);
   T *C = static_cast<T *>(a.C);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int S = a.S, tiles_per_cta = kSmallWarps / S;
+  const int S = a.S, tiles_per_cta = kSmallWarps / S, Z = kZ ? a.Z : 1;
   const int tile = warp / S, part = warp % S;
-  const int64_t mb = int64_t(blockIdx.x) % a.m_blocks, nb = int64_t(blockIdx.x) / a.m_blocks;
+  const uint32_t z = kZ ? cluster_rank() : 0u;
+  if constexpr (kZ) cluster_arrive_relaxed();  // (waited on before the first DSMEM store)
+  const int64_t cta = int64_t(blockIdx.x) / Z;
+  const int64_t mb = cta % a.m_blocks, nb = cta / a.m_blocks;
   const int64_t m0 = (mb * tiles_per_cta + tile) * 8;
   const int64_t n0 = nb * 8;
   const int lr = lane >> 2, lk = lane & 3;
 
-  // this warp's k4 steps
-  const int64_t steps = (a.K + 3) / 4;
-  const int64_t per = (steps + S - 1) / S;
-  const int64_t s0 = min(steps, int64_t(part) * per), s1 = min(steps, s0 + per);
+  // this warp's k4 steps: rank z's share of the tile, then part `part` of it
+  const int64_t steps_all = (a.K + 3) / 4;
+  const int64_t perz = (steps_all + Z - 1) / Z;
+  const int64_t z0 = min(steps_all, int64_t(z) * perz), z1 = min(steps_all, z0 + perz);
+  const int64_t per = (z1 - z0 + S - 1) / S;
+  const int64_t s0 = min(z1, z0 + int64_t(part) * per), s1 = min(z1, s0 + per);
 
   // C is independent of the k loop: the epilogue warps prefetch their two
   // quaternions into L1 first, so the C read latency overlaps the mainloop
   // (a prefetch, not a load: no registers held across the loop)
-  if (part == 0 && !a.sc.beta_zero && m0 + lr < a.M) {
+  if (part == 0 && z == 0 && !a.sc.beta_zero && m0 + lr < a.M) {
 #pragma unroll
     for (int i = 0; i < 2; ++i)
       if (n0 + 2 * lk + i < a.N)
@@ -172,14 +200,35 @@ __global__ void __launch_bounds__(kSmallThreads, 512 / kSmallThreads) qgemm_smal
       }
     }
     __syncthreads();
-    if (part != 0) return;
-    for (int w = 1; w < S; ++w)
+    if (part == 0)
+      for (int w = 1; w < S; ++w)
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          acc[c][0] += red[warp + w][lane][2 * c];
+          acc[c][1] += red[warp + w][lane][2 * c + 1];
+        }
+  }
+  // then across the cluster (every thread takes part in the cluster barriers)
+  if constexpr (kZ) {
+    cluster_wait();  // every CTA of the cluster is running: DSMEM is live
+    if (z > 0 && part == 0)
 #pragma unroll
       for (int c = 0; c < 4; ++c) {
-        acc[c][0] += red[warp + w][lane][2 * c];
-        acc[c][1] += red[warp + w][lane][2 * c + 1];
+        st_dsmem(&zred[z - 1][lane][2 * c], 0, acc[c][0]);
+        st_dsmem(&zred[z - 1][lane][2 * c + 1], 0, acc[c][1]);
       }
+    cluster_arrive_release();
+    cluster_wait();
+    if (z > 0) return;
+    if (part == 0)
+      for (int r = 0; r < Z - 1; ++r)
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          acc[c][0] += zred[r][lane][2 * c];
+          acc[c][1] += zred[r][lane][2 * c + 1];
+        }
   }
+  if (part != 0) return;
 
   const int64_t row = m0 + lr;
   if (row >= a.M) return;

@@ -174,13 +174,16 @@ def test_direct_path_workspace_is_stream_k_scratch(lib):
 
 
 def test_small_path_needs_no_workspace(lib):
-    """Auto policy: below 2^24 quaternion MACs the one-launch kernel is used and
-    no workspace is requested; above it the packed path's size is returned."""
+    """Auto policy: below 2^25 quaternion MACs (and for K <= 16 or few-tile long-K
+    FP64 shapes) the one-launch kernel is used and no workspace is requested;
+    above it the direct / packed path's size is returned."""
     lib.qgemm_set_path_policy(0)
     assert lib.qgemm_workspace_bytes(b"N", b"N", 64, 64, 64, 0) == 0
     assert lib.qgemm_workspace_bytes(b"T", b"H", 256, 256, 256, 1) == 0   # FP32: <= 2^25
-    assert lib.qgemm_workspace_bytes(b"N", b"N", 256, 256, 256, 0) == 0   # FP64: <= 2^24
-    assert lib.qgemm_workspace_bytes(b"N", b"N", 257, 256, 256, 0) > 0    # FP64 above: direct
+    assert lib.qgemm_workspace_bytes(b"N", b"N", 320, 320, 320, 0) == 0   # FP64: <= 2^25
+    assert lib.qgemm_workspace_bytes(b"N", b"N", 384, 384, 384, 0) > 0    # FP64 above: direct
+    assert lib.qgemm_workspace_bytes(b"N", b"N", 64, 64, 8192, 0) == 0    # few tiles, long K
+    assert lib.qgemm_workspace_bytes(b"N", b"N", 4096, 4096, 2, 0) == 0   # K <= 16
     assert lib.qgemm_workspace_bytes(b"N", b"H", 8192, 8192, 8192, 0) > 0
     # huge single factors must not overflow M*N*K into the small path
     assert lib.qgemm_workspace_bytes(b"N", b"N", 1 << 40, 1 << 40, 1, 0) > 0

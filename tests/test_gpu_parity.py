@@ -234,17 +234,30 @@ def test_auto_policy_picks_one_launch_for_small_shapes():
 
 
 @pytest.mark.parametrize("M,N,K", [(1, 1, 1), (8, 8, 4), (9, 7, 3), (40, 3, 1000), (3, 700, 9),
-                                   (256, 256, 256), (31, 257, 64), (4000, 2, 5)])
+                                   (256, 256, 256), (31, 257, 64), (4000, 2, 5), (64, 64, 4096),
+                                   (16, 24, 2053), (8, 8, 100), (5, 3, 2001)])
 @pytest.mark.parametrize("precision", ["f64", "f32"])
 def test_small_kernel_split_and_edges(M, N, K, precision):
-    """Every split factor S (1/2/4 warps per 8x8 tile over K), ragged M/N/K
-    tails, long-K and skinny shapes, both storage types, through the small path."""
+    """Every split factor S (1/2/4 warps per 8x8 tile over K) and cluster split Z
+    (1..8 CTAs per tile over K, partials through distributed shared memory),
+    ragged M/N/K tails, long-K and skinny shapes, both storage types, through
+    the small path."""
     pr = make_problem(M, N, K, "T", "H", QALPHA, QBETA, seed=11, dist="normal",
                       lda=K + 1, ldb=N + 2, ldc=M + 3)
     with path_policy(qg.PATH_SMALL):
         got = run_gpu(pr, precision)
         assert qg.last_launch_count() == 1
     assert_parity(pr, got, oracle_full(pr), precision=precision)
+
+
+@pytest.mark.parametrize("opA,opB", OPS)
+def test_small_kernel_cluster_split_exact(opA, opB):
+    """Cluster split over K (Z = 8: 64 tiles x 8 CTAs) with exact-integer inputs:
+    the DSMEM reduction must give the oracle's result bitwise, for every op pair."""
+    pr = make_problem(64, 56, 3001, opA, opB, (2, -1, 0, 3), (1, 0, -2, 1), seed=12, dist="int8")
+    with path_policy(qg.PATH_SMALL):
+        got = run_gpu(pr)
+    assert_parity(pr, got, oracle_full(pr), exact=True)
 
 
 def test_concurrent_streams_do_not_share_workspace():

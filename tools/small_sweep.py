@@ -1,4 +1,4 @@
-"""Crossover sweep: packed path vs one-launch small kernel (qgemm_set_path_policy).
+"""Crossover sweep: packed path vs one-launch small kernel (and, FP64, the direct path) (qgemm_set_path_policy).
 
 Each call is captured once in a CUDA graph and replayed (host ctypes time is not
 on the device timeline), CUDA events around the replays.
@@ -25,7 +25,8 @@ g = torch.Generator(device="cuda").manual_seed(0)
 
 SHAPES = [(n, n, n) for n in (16, 32, 64, 96, 128, 192, 256, 320, 384, 448, 512, 640, 768)]
 SHAPES += [(64, 64, 4096), (4096, 64, 64), (64, 4096, 64), (256, 256, 1024), (1024, 1024, 16),
-           (128, 128, 4096), (2048, 2048, 4)]
+           (128, 128, 4096), (2048, 2048, 4), (64, 64, 8192), (32, 32, 32768), (4096, 4096, 2),
+           (512, 512, 128), (128, 128, 2048)]
 
 
 def graph_time(call, nrep=100):
@@ -55,7 +56,10 @@ for M, N, K in SHAPES:
     B = 2 * torch.rand((N, K, 4), dtype=dt, device="cuda", generator=g) - 1
     C = 2 * torch.rand((N, M, 4), dtype=dt, device="cuda", generator=g) - 1
     row = {"M": M, "N": N, "K": K, "dtype": a.precision}
-    for name, pol in (("packed", qg.PATH_PACKED), ("small", qg.PATH_SMALL)):
+    pols = (("packed", qg.PATH_PACKED), ("small", qg.PATH_SMALL))
+    if a.precision == "f64":
+        pols += (("direct", qg.PATH_DIRECT),)
+    for name, pol in pols:
         old = qg.set_path_policy(pol)
         need = qg.workspace_bytes("N", "N", M, N, K, dt)
         ws = torch.empty(max(need, 256), dtype=torch.uint8, device="cuda")
