@@ -548,7 +548,8 @@ int direct_feed(int opA, int64_t M, int64_t N, int64_t K) {
 //    350 us vs 564), and for few output tiles with long K (<= 64 tiles of 64x64,
 //    K >= 4 max(M, N): the cluster split over K beats stream-K's owner
 //    reductions, 64x64x8192: 53 us vs 332; 128x128x4096: 96 vs 153);
-//  * FP32: up to 2^25 (the tcgen05 path has a 128x128 tile and no split-K), and
+//  * FP32: up to 2^26 (384^3: 74 us vs 115 packed; tie at 448^3 -- the tcgen05
+//    path has 256x128 pair tiles and no split-K), and
 //    up to 2^28 when that path would launch fewer than 1/4 as many CTAs as
 //    there are SMs and K >= 4 max(M, N) (small M x N, long K);
 //    but not for K <= 16 with M*N >= 2^20: there the FP32 call is C-traffic
@@ -571,7 +572,7 @@ bool use_small(int64_t M, int64_t N, int64_t K) {
     return cdiv(M, 64) * cdiv(N, 64) <= 64 && K >= 4 * std::max(M, N);
   }
   if (K <= 16 && double(M) * double(N) >= double(1 << 20)) return false;
-  if (macs <= double(kSmallMaxMacs)) return true;
+  if (macs <= double(2 * kSmallMaxMacs)) return true;
   const int64_t tc_ctas = cdiv(M, 128) * cdiv(N, 128);
   return 4 * tc_ctas < num_sms() && K >= 4 * std::max(M, N);
 }
