@@ -73,6 +73,9 @@ def qgemm_rowsharded(transA: str, transB: str, alpha, A_local: torch.Tensor, B: 
         local_gemm(transA, transB, alpha, A_local, B, beta, C_local, M=m_loc, N=N, K=K)
     if not gather:
         return C_local
+    # gloo moves host memory only: CUDA tensors are staged through the host
+    # there (bench.py --debug-one-device); NCCL sends device memory directly
+    host_stage = C_local.is_cuda and dist.get_backend(group) == "gloo"
     if rank == root:
         assert C_full is not None and C_full.shape[0] == N and C_full.shape[1] >= M
         C_full[:, r0:r1, :].copy_(C_local[:, :m_loc, :])
@@ -84,7 +87,8 @@ def qgemm_rowsharded(transA: str, transB: str, alpha, A_local: torch.Tensor, B: 
             s0, s1 = rows_for_rank(M, world, src)
             if s1 == s0:
                 continue
-            buf = torch.empty((N, s1 - s0, 4), dtype=C_local.dtype, device=C_local.device)
+            buf = torch.empty((N, s1 - s0, 4), dtype=C_local.dtype,
+                              device="cpu" if host_stage else C_local.device)
             bufs.append((s0, s1, buf))
             ops.append(dist.P2POp(dist.irecv, buf, src, group))
         for w in dist.batch_isend_irecv(ops) if ops else []:
@@ -94,6 +98,8 @@ def qgemm_rowsharded(transA: str, transB: str, alpha, A_local: torch.Tensor, B: 
         return C_full
     if m_loc > 0:
         send = C_local if C_local.shape[1] == m_loc else C_local[:, :m_loc, :].contiguous()
+        if host_stage:
+            send = send.cpu()
         for w in dist.batch_isend_irecv([dist.P2POp(dist.isend, send, root, group)]):
             w.wait()
     return C_local
