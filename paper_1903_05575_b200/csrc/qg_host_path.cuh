@@ -14,6 +14,17 @@
 #ifndef QG_HOST_PANELS
 #define QG_HOST_PANELS 16
 #endif
+// Chunk p > 0 is QG_HOST_GROWTH^(p-1) times the second one (capped at
+// QG_HOST_KC_MAX): uploads run ~6x faster than the mainloop consumes K at c3,
+// so later chunks can grow, and every chunk fewer saves one C pass + relaunch
+// (c3: chunks 256, 1024, 2048, 4096, 768; 489.4 ms per call vs 493.1 with
+// uniform 1024-chunks; growth 3-4 up to 8192 exposes 12-16 ms of uploads).
+#ifndef QG_HOST_GROWTH
+#define QG_HOST_GROWTH 2
+#endif
+#ifndef QG_HOST_KC_MAX
+#define QG_HOST_KC_MAX 4096
+#endif
 // ---------------------------------------------------------------------------
 // Host-resident operands (qgemm_host / qgemm_host_f32): the end-to-end call.
 //
@@ -34,11 +45,13 @@
 template <typename T>
 struct HostPlan {
   bool small = false;       // one-launch kernel on the whole problem (Q = P = 1)
-  int64_t Kc0 = 0, Kc = 0, Q = 0;  // first K chunk (short: compute starts early), later chunks, count
+  int64_t Kc0 = 0, Kc = 0, Q = 0;  // first K chunk (short: compute starts early), largest chunk, count
   int64_t Nj = 0, P = 0;    // C column panel width and count (last chunk / downloads)
   size_t off_cold = 0;      // device copy of the caller's C (beta != 0); off_C = 0
   size_t off_sa[2], off_sb[2], off_pa[2], off_pb[2], off_sk = 0, total = 0;
-  int64_t k_begin(int64_t p) const { return p == 0 ? 0 : Kc0 + (p - 1) * Kc; }
+  std::vector<int64_t> kb;  // chunk p covers k in [kb[p], kb[p+1])
+  int64_t k_begin(int64_t p) const { return kb[size_t(p)]; }
+  int64_t k_len(int64_t p) const { return kb[size_t(p) + 1] - kb[size_t(p)]; }
 };
 
 template <typename T>
@@ -49,13 +62,25 @@ HostPlan<T> host_plan(int64_t M, int64_t N, int64_t K) {
   h.small = use_small<T>(M, N, K);
   if (h.small || K == 0) {
     h.Kc0 = h.Kc = std::max<int64_t>(K, 1); h.Q = 1; h.Nj = N; h.P = 1;
+    h.kb = {0, K};
   } else {
     // chunks of ~K/8 (256..2048); the first one a quarter of that, so the first
-    // mainloop waits only for a small upload
-    h.Kc = std::min<int64_t>(cdiv(K, kq) * kq,
+    // mainloop waits only for a small upload; later ones growing by QG_HOST_GROWTH
+    const int64_t kc1 = std::min<int64_t>(cdiv(K, kq) * kq,
                              std::max<int64_t>(256, std::min<int64_t>(2048, cdiv(cdiv(K, QG_HOST_KC_DIV), kq) * kq)));
-    h.Kc0 = std::min<int64_t>(h.Kc, std::max<int64_t>(kq, cdiv(cdiv(h.Kc, QG_HOST_KC0_DIV), kq) * kq));
-    h.Q = K <= h.Kc0 ? 1 : 1 + cdiv(K - h.Kc0, h.Kc);
+    h.Kc0 = std::min<int64_t>(kc1, std::max<int64_t>(kq, cdiv(cdiv(kc1, QG_HOST_KC0_DIV), kq) * kq));
+    h.kb.push_back(0);
+    int64_t k = std::min<int64_t>(K, h.Kc0), len = kc1;
+    h.kb.push_back(k);
+    h.Kc = h.Kc0;
+    while (k < K) {
+      const int64_t l = std::min<int64_t>(K - k, len);
+      h.Kc = std::max(h.Kc, l);
+      k += l;
+      h.kb.push_back(k);
+      len = std::max<int64_t>(kc1, std::min<int64_t>(int64_t(QG_HOST_KC_MAX), len * QG_HOST_GROWTH));
+    }
+    h.Q = int64_t(h.kb.size()) - 1;
     h.Nj = std::min<int64_t>(cdiv(N, rows) * rows, std::max<int64_t>(256, cdiv(cdiv(N, QG_HOST_PANELS), rows) * rows));
     h.P = cdiv(N, h.Nj);
   }
@@ -164,7 +189,7 @@ int qgemm_host_impl(char transA, char transB, int64_t M, int64_t N, int64_t K, c
   const int a_rc = sh.oa == 0, a_cj = sh.oa == 2, b_rc = sh.ob != 0, b_cj = sh.ob == 2;
   auto chunk = [&](int64_t p, int64_t &k0, int64_t &kc) {
     k0 = h.k_begin(p);
-    kc = std::min<int64_t>(K, p == 0 ? h.Kc0 : k0 + h.Kc) - k0;
+    kc = h.k_len(p);
   };
   auto stage = [&](int64_t p) -> int {  // on H
     const int sl = int(p & 1);
