@@ -55,6 +55,9 @@ constexpr int kConsumerRegs = 232;
 #ifndef QG_GROUP_M
 #define QG_GROUP_M 8
 #endif
+#ifndef QG_C_PREFETCH_KT
+#define QG_C_PREFETCH_KT 2  // k-tiles before the end of a tile at which its C tile is prefetched to L2
+#endif
 constexpr int kGroupM = QG_GROUP_M;  // rasterisation: M-tiles per group (L2 reuse of panels)
 // ring + barriers + 1 KB so the ring can start on a 1024-byte boundary
 constexpr size_t kDmmaSmemBytes = size_t(kStages) * 2 * kChunkElems * sizeof(double) + 2 * kStages * 8 + 1024;
@@ -424,8 +427,9 @@ __global__ void __launch_bounds__(kDmmaThreads, 1) qgemm_dmma_kernel(const __gri
         for (int c = 0; c < 4; ++c) acc[i][j][c][0] = acc[i][j][c][1] = 0.0;
 
     // k-tile at which to warm L2 with this unit's C tile (beta != 0, epilogue here)
-    const int64_t kt_prefetch =
-        (u.kb == 0 && !args.sc.beta_zero) ? (u.ke - 2 > u.kb ? u.ke - 2 : u.kb) : int64_t(-1);
+    const int64_t kt_prefetch = (QG_C_PREFETCH_KT > 0 && u.kb == 0 && !args.sc.beta_zero)
+                                    ? (u.ke - QG_C_PREFETCH_KT > u.kb ? u.ke - QG_C_PREFETCH_KT : u.kb)
+                                    : int64_t(-1);
     for (int64_t kt = u.kb; kt < u.ke; ++kt) {
       if (kt == kt_prefetch) {
         int64_t pmt, pnt;
