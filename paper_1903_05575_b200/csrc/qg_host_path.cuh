@@ -98,8 +98,8 @@ HostPlan<T> host_plan(int64_t M, int64_t N, int64_t K) {
     const size_t pb = align256(size_t(cdiv(N, Geo<T>::rows)) * size_t(ktc) * Geo<T>::chunk);
     for (int i = 0; i < 2; ++i) { h.off_pa[i] = off; if (i < nbuf) off += pa; }
     for (int i = 0; i < 2; ++i) { h.off_pb[i] = off; if (i < nbuf) off += pb; }
-    h.off_sk = off;
-    off += sk_reserve<T>(M, N, cdiv(K, kq));
+    h.off_sk = off;  // (the last chunk's column panels may split differently: reserve for both)
+    off += std::max(sk_reserve<T>(M, N, cdiv(K, kq)), sk_reserve<T>(M, h.Nj, cdiv(K, kq)));
   } else {
     for (int i = 0; i < 2; ++i) h.off_pa[i] = h.off_pb[i] = off;
     h.off_sk = off;

@@ -136,9 +136,29 @@ size_t sk_slots_bytes(int64_t M, int64_t N, int64_t ktiles) {
   const int64_t tiles = cdiv(M, qg::kBR) * cdiv(N, qg::kBR);
   return align256(size_t(max_grid(tiles, ktiles)) * qg::kPartialBytes);
 }
+int num_sms();
+
+// FP32 pair kernel: K splits per 256 x 128 tile pair when there are fewer pairs
+// than one wave (one pair per 2 SMs) -- as many as fill the wave, at most 8,
+// each split >= 4 k-tiles.  Monotone in ktiles, so a reserve sized for the
+// whole K covers every K-panel launch.
+int64_t tc2_splits(int64_t M, int64_t N, int64_t ktiles) {
+  if (!QG_TC32_2CTA) return 1;
+  const int64_t pairs = cdiv(M, 2 * qg::kTcBM) * cdiv(N, qg::kTcBN);
+  const int64_t wave = std::max<int64_t>(1, num_sms() / 2);
+  if (pairs >= wave) return 1;
+  return std::max<int64_t>(1, std::min<int64_t>({wave / pairs, 8, ktiles / 4}));
+}
+size_t tc2_part_bytes(int64_t M, int64_t N, int64_t ktiles) {
+  const int64_t S = tc2_splits(M, N, ktiles);
+  if (S <= 1) return 0;
+  const int64_t pairs = cdiv(M, 2 * qg::kTcBM) * cdiv(N, qg::kTcBN);
+  return align256(size_t(pairs) * size_t(S) * 2 * size_t(qg::kTc2PartFloats) * sizeof(float));
+}
+
 template <typename T>
 size_t sk_reserve(int64_t M, int64_t N, int64_t ktiles) {
-  if (sizeof(T) != 8) return 0;
+  if (sizeof(T) != 8) return tc2_part_bytes(M, N, ktiles);
   return sk_slots_bytes<T>(M, N, ktiles) + align256(size_t(2 * qg::kMaxPersistentCTAs) * sizeof(int));
 }
 
@@ -480,7 +500,7 @@ int encode_packed_2d(CUtensorMap *tm, const float *base, int64_t chunks, int box
 }
 
 int launch_mainloop(const float *Ap, const float *Bp, float *C, int64_t ldc, int64_t M, int64_t N, int64_t KT,
-                    const qg::Scalars<float> &sc, void * /*sk_scratch*/, cudaStream_t st,
+                    const qg::Scalars<float> &sc, void *sk_scratch, cudaStream_t st,
                     int /*tri: FP64 only*/ = 0) {
   constexpr int kMaxDev = 64;
   static bool attr_set[kMaxDev] = {false};
@@ -502,12 +522,24 @@ int launch_mainloop(const float *Ap, const float *Bp, float *C, int64_t ldc, int
     int rc = encode_packed_2d(&t.tmA, Ap, 2 * t.MT2 * KT, 32);
     if (!rc) rc = encode_packed_2d(&t.tmB, Bp, t.NT * KT, 16);
     if (rc) return rc;
-    const int64_t grid = 2 * t.MT2 * t.NT;
+    // fewer tile pairs than a wave: split K (the caller reserved tc2_part_bytes
+    // at sk_scratch), then one reduce + epilogue launch
+    t.S = sk_scratch ? int(tc2_splits(M, N, KT)) : 1;
+    t.part = static_cast<float *>(sk_scratch);
+    const int64_t grid = 2 * t.MT2 * t.NT * t.S;
     if (grid > INT32_MAX) return int(cudaErrorInvalidConfiguration);
     { int ti = tstart(kMain, st);
     qg::qgemm_tc32_2cta_kernel<<<unsigned(grid), qg::kTcThreads, qg::kTc2SmemBytes, st>>>(t);
     tstop(ti, st); }
     ++g_last_launches;
+    if (t.S > 1) {
+      cudaError_t e = cudaGetLastError();
+      if (e != cudaSuccess) return int(e);
+      { int ti = tstart(kMain, st);
+      qg::tc2_reduce_kernel<<<dim3(unsigned(2 * t.MT2 * t.NT), qg::kTcBN / 16), qg::kTcBM, 0, st>>>(t);
+      tstop(ti, st); }
+      ++g_last_launches;
+    }
     return int(cudaGetLastError());
   }
   qg::Tc32Args t;

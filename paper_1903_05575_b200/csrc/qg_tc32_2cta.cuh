@@ -42,7 +42,22 @@ struct alignas(64) Tc2Args {
   float *C;
   int64_t ldc, M, N, MT2, NT, KT;  // MT2 = 256-row tile pairs
   Scalars<float> sc;
+  int S;             // K splits per tile pair (1: the epilogue updates C)
+  float *part;       // S > 1: raw accumulators, kTc2PartFloats per CTA, summed by tc2_reduce_kernel
 };
+// One CTA's raw partial: 4 components x 128 columns x 128 rows, rows fastest.
+constexpr int64_t kTc2PartFloats = 4 * int64_t(kTcBN) * kTcBM;
+
+// Tile pair `pid` of the grouped raster (kTc2GroupM pair-rows per group).
+__device__ __forceinline__ void tc2_tile(int64_t pid, int64_t MT2, int64_t NT, int64_t &pm, int64_t &pn) {
+  const int64_t per_group = int64_t(kTc2GroupM) * NT;
+  const int64_t g = pid / per_group;
+  const int64_t first_m = g * kTc2GroupM;
+  const int64_t gsz = (MT2 - first_m) < kTc2GroupM ? (MT2 - first_m) : kTc2GroupM;
+  const int64_t in = pid - g * per_group;
+  pm = first_m + in % gsz;
+  pn = in / gsz;
+}
 
 // kind::tf32, D f32, K-major A/B, M = 256 (pair), N = 128.
 __host__ __device__ constexpr uint32_t tc2_idesc(bool negate_a) {
@@ -93,20 +108,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kTcThreads, 1)
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t rank = cluster_rank();
-  // tile pair of this cluster, grouped rasterisation as the 1-CTA kernel
-  const int64_t pid = int64_t(blockIdx.x) >> 1;
+  // tile pair of this cluster (grouped rasterisation as the 1-CTA kernel) and,
+  // with S > 1 splits, its share [k0, k1) of the k-tiles
+  const int64_t cid = int64_t(blockIdx.x) >> 1;
+  const int64_t pid = cid / args.S, ks = cid % args.S;
   int64_t pm, pn;
-  {
-    const int64_t per_group = int64_t(kTc2GroupM) * args.NT;
-    const int64_t g = pid / per_group;
-    const int64_t first_m = g * kTc2GroupM;
-    const int64_t gsz = (args.MT2 - first_m) < kTc2GroupM ? (args.MT2 - first_m) : kTc2GroupM;
-    const int64_t in = pid - g * per_group;
-    pm = first_m + in % gsz;
-    pn = in / gsz;
-  }
+  tc2_tile(pid, args.MT2, args.NT, pm, pn);
   const int64_t mt = 2 * pm + rank;  // this CTA's 128-row A tile
   const int64_t KT = args.KT;
+  const int64_t k0 = ks * KT / args.S, k1 = (ks + 1) * KT / args.S;
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < kTc2Stages; ++s) {
@@ -130,8 +140,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kTcThreads, 1)
     // ---------------- producer (both CTAs) ----------------
     int slot = 0;
     uint32_t phase = 0;
-    for (int64_t kt = 0; kt < KT; ++kt) {
-      if (kt >= kTc2Stages) mbar_wait_guarded(&empty[slot], phase ^ 1u);
+    for (int64_t kt = k0; kt < k1; ++kt) {
+      if (kt - k0 >= kTc2Stages) mbar_wait_guarded(&empty[slot], phase ^ 1u);
       if (rank == 0) mbar_arrive_expect_tx(&full[slot], 2 * (kTc2ABytes + kTc2BBytes));
       tma2_load_2d(sA + slot * kTc2AFloats, &args.tmA, 0, int((mt * KT + kt) * 32), &full[slot]);
       tma2_load_2d(sB + slot * kTc2BFloats, &args.tmB, 0, int((pn * KT + kt) * 32 + rank * 16), &full[slot]);
@@ -141,7 +151,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kTcThreads, 1)
     // ---------------- MMA issuer (leader only) ----------------
     int slot = 0;
     uint32_t phase = 0;
-    for (int64_t kt = 0; kt < KT; ++kt) {
+    for (int64_t kt = k0; kt < k1; ++kt) {
       mbar_wait_guarded(&full[slot], phase);
       tc_fence_after();
       const uint32_t a0 = smem_u32(sA + slot * kTc2AFloats);
@@ -157,7 +167,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kTcThreads, 1)
           const uint64_t alo = tc_sdesc(a0 + (p * 2 + 1) * kTcPlaneFloats * 4);
           const uint64_t bhi = tc_sdesc(b0 + (s * 2 + 0) * (kTcPlaneFloats / 2) * 4);
           const uint64_t blo = tc_sdesc(b0 + (s * 2 + 1) * (kTcPlaneFloats / 2) * 4);
-          tc2_mma(d, ahi, bhi, id, (kt > 0 || p > 0) ? 1u : 0u);
+          tc2_mma(d, ahi, bhi, id, (kt > k0 || p > 0) ? 1u : 0u);
           tc2_mma(d, ahi, blo, id, 1u);
           tc2_mma(d, alo, bhi, id, 1u);
         }
@@ -173,11 +183,20 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kTcThreads, 1)
     mbar_wait_guarded(acc_full, 0);
     tc_fence_after();
     const uint32_t tbase = tmem + (uint32_t(q * 32) << 16);
+    float *part = args.S > 1 ? args.part + ((pid * args.S + ks) * 2 + rank) * kTc2PartFloats : nullptr;
     for (int n0 = 0; n0 < kTcBN; n0 += 16) {
       float d[4][16];
 #pragma unroll
       for (int c = 0; c < 4; ++c) tmem_ld16(tbase + uint32_t(c * kTcBN + n0), d[c]);
       tmem_ld_wait();
+      if (part) {  // split K: park the raw sums (coalesced over the 32 rows of the warp)
+#pragma unroll
+        for (int c = 0; c < 4; ++c)
+#pragma unroll
+          for (int jj = 0; jj < 16; ++jj)
+            __stcg(part + (int64_t(c) * kTcBN + n0 + jj) * kTcBM + q * 32 + lane, d[c][jj]);
+        continue;
+      }
       if (row < args.M) {
         float cold[16][4];
         if (!args.sc.beta_zero) {
@@ -210,6 +229,40 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kTcThreads, 1)
   if (warp == 0) {
     tc_fence_after();
     asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, 512;\n" ::"r"(tmem) : "memory");
+  }
+}
+
+// Split-K epilogue: C(row, col) <- alpha (x) sum_ks part_ks + beta (x) C, the S
+// partials added in split order (deterministic).  Block = one CTA tile's 128
+// rows (threads) x 16 columns; grid = (2 * pairs, 8).
+__global__ void __launch_bounds__(kTcBM) tc2_reduce_kernel(const __grid_constant__ Tc2Args args) {
+  const int64_t cta = blockIdx.x, pid = cta >> 1;
+  const int rank = int(cta & 1);
+  int64_t pm, pn;
+  tc2_tile(pid, args.MT2, args.NT, pm, pn);
+  const int64_t row = (2 * pm + rank) * kTcBM + threadIdx.x;
+  if (row >= args.M) return;
+  const float *p0 = args.part + (pid * args.S * 2 + rank) * kTc2PartFloats + threadIdx.x;
+  const int64_t stride = 2 * kTc2PartFloats;  // next split, same rank
+  for (int j = 0; j < 16; ++j) {
+    const int cl = int(blockIdx.y) * 16 + j;
+    const int64_t col = pn * kTcBN + cl;
+    if (col >= args.N) break;
+    float acc[4] = {0.f, 0.f, 0.f, 0.f};
+    for (int k = 0; k < args.S; ++k)
+#pragma unroll
+      for (int c = 0; c < 4; ++c) acc[c] += __ldcg(p0 + k * stride + (int64_t(c) * kTcBN + cl) * kTcBM);
+    float *cp = args.C + 4 * (row + col * args.ldc);
+    float out[4];
+    left_scale(args.sc.alpha, args.sc.alpha_real, acc, out);
+    if (!args.sc.beta_zero) {
+      float cold[4], bc[4];
+      ldq_c(cp, cold);
+      left_scale(args.sc.beta, args.sc.beta_real, cold, bc);
+#pragma unroll
+      for (int c = 0; c < 4; ++c) out[c] += bc[c];
+    }
+    stq(cp, out);
   }
 }
 
