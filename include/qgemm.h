@@ -65,8 +65,8 @@
  *
  * Small problems: below the library's measured
  * crossover (FP64: M*N*K <= 2^25 quaternion multiply-adds, K <= 16, or at most
- * 64 output tiles of 64 x 64 with K >= 4 max(M, N); FP32: <= 2^26, or
- * small M x N with long K), qgemm/qgemm_f32 run ONE kernel that reads
+ * 64 output tiles of 64 x 64 with K >= 4 max(M, N); FP32: <= 2^25, or
+ * M <= 256, N <= 128 with K >= 8 max(M, N)), qgemm/qgemm_f32 run ONE kernel that reads
  * op(A)/op(B) in place (no pack, no workspace);
  * qgemm_workspace_bytes() then returns 0 and `workspace` may be NULL.  The
  * path is a pure function of (transA, M, N, K), the precision and the path

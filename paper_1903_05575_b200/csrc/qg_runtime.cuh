@@ -139,8 +139,8 @@ size_t sk_slots_bytes(int64_t M, int64_t N, int64_t ktiles) {
 int num_sms();
 
 // FP32 pair kernel: K splits per 256 x 128 tile pair when there are fewer pairs
-// than one wave (one pair per 2 SMs) -- as many as fill the wave, at most 8,
-// each split >= 4 k-tiles.  Monotone in ktiles, so a reserve sized for the
+// than one wave (one pair per 2 SMs) -- as many as fill the wave, at most 8
+// (16 measured 10-19% slower at 320^3-512^3), each split >= 4 k-tiles.  Monotone in ktiles, so a reserve sized for the
 // whole K covers every K-panel launch.
 int64_t tc2_splits(int64_t M, int64_t N, int64_t ktiles) {
   if (!QG_TC32_2CTA) return 1;
@@ -580,10 +580,9 @@ int direct_feed(int opA, int64_t M, int64_t N, int64_t K) {
 //    350 us vs 564), and for few output tiles with long K (<= 64 tiles of 64x64,
 //    K >= 4 max(M, N): the cluster split over K beats stream-K's owner
 //    reductions, 64x64x8192: 53 us vs 332; 128x128x4096: 96 vs 153);
-//  * FP32: up to 2^26 (384^3: 74 us vs 115 packed; tie at 448^3 -- the tcgen05
-//    path has 256x128 pair tiles and no split-K), and
-//    up to 2^28 when that path would launch fewer than 1/4 as many CTAs as
-//    there are SMs and K >= 4 max(M, N) (small M x N, long K);
+//  * FP32: up to 2^25 (320^3: 49 us vs 53 for the split-K pair kernel; 384^3:
+//    74 vs 55), and up to 2^28 for a single 256x128 tile pair with
+//    K >= 8 max(M, N) (profiles/r01p_small_sweep_f32.jsonl);
 //    but not for K <= 16 with M*N >= 2^20: there the FP32 call is C-traffic
 //    bound and the packed tcgen05 epilogue streams C better.
 constexpr int64_t kSmallMaxMacs = int64_t(1) << 25;
@@ -604,9 +603,10 @@ bool use_small(int64_t M, int64_t N, int64_t K) {
     return cdiv(M, 64) * cdiv(N, 64) <= 64 && K >= 4 * std::max(M, N);
   }
   if (K <= 16 && double(M) * double(N) >= double(1 << 20)) return false;
-  if (macs <= double(2 * kSmallMaxMacs)) return true;
-  const int64_t tc_ctas = cdiv(M, 128) * cdiv(N, 128);
-  return 4 * tc_ctas < num_sms() && K >= 4 * std::max(M, N);
+  if (macs <= double(kSmallMaxMacs)) return true;
+  // one 256 x 128 tile pair and a long K: even split 8 ways the pair kernel
+  // fills a tenth of the GPU (64x64x4096: small 31 us vs 148)
+  return cdiv(M, 256) * cdiv(N, 128) == 1 && K >= 8 * std::max(M, N);
 }
 
 int num_sms() {

@@ -179,8 +179,9 @@ def test_small_path_needs_no_workspace(lib):
     above it the direct / packed path's size is returned."""
     lib.qgemm_set_path_policy(0)
     assert lib.qgemm_workspace_bytes(b"N", b"N", 64, 64, 64, 0) == 0
-    assert lib.qgemm_workspace_bytes(b"T", b"H", 384, 384, 384, 1) == 0   # FP32: <= 2^26
-    assert lib.qgemm_workspace_bytes(b"T", b"H", 448, 448, 448, 1) > 0    # FP32 above: packed
+    assert lib.qgemm_workspace_bytes(b"T", b"H", 320, 320, 320, 1) == 0   # FP32: <= 2^25
+    assert lib.qgemm_workspace_bytes(b"T", b"H", 384, 384, 384, 1) > 0    # FP32 above: packed (split K)
+    assert lib.qgemm_workspace_bytes(b"N", b"N", 64, 64, 4096, 1) == 0    # FP32: one pair, long K
     assert lib.qgemm_workspace_bytes(b"N", b"N", 320, 320, 320, 0) == 0   # FP64: <= 2^25
     assert lib.qgemm_workspace_bytes(b"N", b"N", 384, 384, 384, 0) > 0    # FP64 above: direct
     assert lib.qgemm_workspace_bytes(b"N", b"N", 64, 64, 8192, 0) == 0    # few tiles, long K
