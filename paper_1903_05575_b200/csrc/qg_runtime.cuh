@@ -279,6 +279,12 @@ int persistent_ctas() {
   return r;
 }
 
+// Full waves folded into the stream-K part (besides the partial last wave):
+// 0 = data-parallel for every full wave, stream-K over the remainder only
+// (c2: 35.32-35.51 vs 35.24-35.41 TFLOP/s graph-replayed with 1).
+#ifndef QG_SK_FULL_WAVES
+#define QG_SK_FULL_WAVES 0
+#endif
 // Persistent "data-parallel + stream-K" schedule (see qg_dmma.cuh).
 void plan_schedule(qg::DmmaArgs &a, int resident) {
   a.T = a.tri ? a.MT * (a.MT + 1) / 2 : a.MT * a.NT;
@@ -287,8 +293,8 @@ void plan_schedule(qg::DmmaArgs &a, int resident) {
   const int64_t waves = a.T / G, rem = a.T % G;
   if (rem == 0) {
     a.dp_tiles = a.T;
-  } else if (waves >= 2) {
-    a.dp_tiles = (waves - 1) * G;  // last full wave + remainder go stream-K
+  } else if (waves >= QG_SK_FULL_WAVES) {
+    a.dp_tiles = (waves - QG_SK_FULL_WAVES) * G;  // the last QG_SK_FULL_WAVES full waves + remainder go stream-K
   } else {
     a.dp_tiles = 0;
   }
