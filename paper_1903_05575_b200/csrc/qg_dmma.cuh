@@ -107,16 +107,34 @@ __device__ __forceinline__ void tile_coords(int64_t pid, int64_t MT, int64_t NT,
 }
 
 // Tile t of the work list: full grid (grouped raster) or, for the triangular
-// (QHERK) schedule, row-major over the lower triangle t = mt(mt+1)/2 + nt.
+// (QHERK) schedule, the lower triangle in bands of kGroupM tile rows, each band
+// column by column (rows inner) like the grouped raster: band b (rows
+// [8b, 8b + h), h <= 8) holds 8b*h tiles left of its diagonal block, then the
+// h(h+1)/2 tiles of that block; bands start at t = 32 b^2 + 4 b (kGroupM = 8).
 __device__ __forceinline__ void work_tile(const DmmaArgs &a, int64_t t, int64_t &mt, int64_t &nt) {
   if (a.tri == 0) {
     tile_coords(t, a.MT, a.NT, mt, nt);
     return;
   }
-  int64_t r = int64_t((sqrt(8.0 * double(t) + 1.0) - 1.0) * 0.5);
-  while (r * (r + 1) / 2 > t) --r;
-  while ((r + 1) * (r + 2) / 2 <= t) ++r;
-  const int64_t c = t - r * (r + 1) / 2;
+  constexpr int64_t G = kGroupM;
+  auto band_start = [](int64_t b) { return (G * G / 2) * b * b + (G * (G + 1) / 2 - G * G / 2) * b; };
+  int64_t b = int64_t((-double(G * (G + 1) / 2 - G * G / 2) +
+                       sqrt(double(G * (G + 1) / 2 - G * G / 2) * double(G * (G + 1) / 2 - G * G / 2) +
+                            2.0 * double(G * G) * double(t))) / double(G * G));
+  while (b > 0 && band_start(b) > t) --b;
+  while (band_start(b + 1) <= t) ++b;
+  const int64_t r0 = G * b, h = (a.MT - r0) < G ? (a.MT - r0) : G;
+  const int64_t u = t - band_start(b);
+  int64_t r, c;
+  if (u < r0 * h) {
+    c = u / h;
+    r = r0 + u % h;
+  } else {  // diagonal block: column j has rows j..h-1
+    int64_t v = u - r0 * h, j = 0;
+    while (v >= h - j) { v -= h - j; ++j; }
+    c = r0 + j;
+    r = r0 + j + v;
+  }
   if (a.tri == 1) { mt = r; nt = c; }
   else            { mt = c; nt = r; }
 }
