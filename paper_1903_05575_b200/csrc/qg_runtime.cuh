@@ -262,20 +262,26 @@ int launch_pack2(const qg::PackJob<T> &ja, const qg::PackJob<T> &jb, cudaStream_
   return int(cudaGetLastError());
 }
 
+// Per-device caches below are atomics: any host thread may make the first call
+// on a device; racing initialisations store the same value.
+constexpr int kMaxDev = 64;
+
 // Resident CTAs of the persistent FP64 mainloop on the current device.
 // (cached per device: the query costs microseconds, which matter at c1 sizes)
 int persistent_ctas() {
-  constexpr int kMaxDev = 64;
-  static int cache[kMaxDev] = {0};
+  static std::atomic<int> cache[kMaxDev];
   int dev = 0, sms = 0, per_sm = 0;
   if (cudaGetDevice(&dev) != cudaSuccess) return 0;
-  if (dev < kMaxDev && cache[dev] > 0) return cache[dev];
+  if (dev < kMaxDev) {
+    const int c = cache[dev].load(std::memory_order_relaxed);
+    if (c > 0) return c;
+  }
   if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess) return 0;
   if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, qg::qgemm_dmma_kernel<qg::kFeedPacked, false, false>,
                                                     qg::kDmmaThreads, qg::kDmmaSmemBytes) != cudaSuccess)
     return 0;
   const int r = std::min(qg::kMaxPersistentCTAs, sms * std::max(1, per_sm));
-  if (dev < kMaxDev) cache[dev] = r;
+  if (dev < kMaxDev) cache[dev].store(r, std::memory_order_relaxed);
   return r;
 }
 
@@ -336,12 +342,11 @@ DmmaKernel dmma_kernel(int feed, bool ca, bool cb, int arc = 0, int brc = 0) {
 }
 
 int dmma_set_attributes() {
-  constexpr int kMaxDev = 64;
-  static bool done[kMaxDev] = {false};
+  static std::atomic<bool> done[kMaxDev];
   int dev = 0;
   cudaError_t e = cudaGetDevice(&dev);
   if (e != cudaSuccess) return int(e);
-  if (dev < kMaxDev && done[dev]) return 0;
+  if (dev < kMaxDev && done[dev].load(std::memory_order_acquire)) return 0;
   for (int feed : {int(qg::kFeedPacked), int(qg::kFeedTma), int(qg::kFeedTma128)})
     for (int c = 0; c < 16; ++c) {
       const bool ca = c & 1, cb = c & 2;
@@ -353,7 +358,7 @@ int dmma_set_attributes() {
       e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(qg::kDmmaSmemBytes));
       if (e != cudaSuccess) return int(e);
     }
-  if (dev < kMaxDev) done[dev] = true;
+  if (dev < kMaxDev) done[dev].store(true, std::memory_order_release);
   return 0;
 }
 
@@ -363,15 +368,15 @@ using EncodeTiledFn = CUresult (*)(CUtensorMap *, CUtensorMapDataType, cuuint32_
                                    const cuuint64_t *, const cuuint32_t *, const cuuint32_t *, CUtensorMapInterleave,
                                    CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
 EncodeTiledFn encode_tiled() {
-  static EncodeTiledFn fn = nullptr;
-  if (fn) return fn;
+  static std::atomic<EncodeTiledFn> fn{nullptr};
+  if (EncodeTiledFn f = fn.load(std::memory_order_acquire)) return f;
   void *p = nullptr;
   cudaDriverEntryPointQueryResult q;
   if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) != cudaSuccess ||
       q != cudaDriverEntryPointSuccess)
     return nullptr;
-  fn = reinterpret_cast<EncodeTiledFn>(p);
-  return fn;
+  fn.store(reinterpret_cast<EncodeTiledFn>(p), std::memory_order_release);
+  return reinterpret_cast<EncodeTiledFn>(p);
 }
 
 // 3-D map of an R x K operand view over interleaved FP64 storage (ld in
@@ -508,18 +513,17 @@ int encode_packed_2d(CUtensorMap *tm, const float *base, int64_t chunks, int box
 int launch_mainloop(const float *Ap, const float *Bp, float *C, int64_t ldc, int64_t M, int64_t N, int64_t KT,
                     const qg::Scalars<float> &sc, void *sk_scratch, cudaStream_t st,
                     int /*tri: FP64 only*/ = 0) {
-  constexpr int kMaxDev = 64;
-  static bool attr_set[kMaxDev] = {false};
+  static std::atomic<bool> attr_set[kMaxDev];
   int dev = 0;
   if (cudaGetDevice(&dev) != cudaSuccess) return int(cudaErrorInvalidDevice);
-  if (dev >= kMaxDev || !attr_set[dev]) {
+  if (dev >= kMaxDev || !attr_set[dev].load(std::memory_order_acquire)) {
     cudaError_t e = cudaFuncSetAttribute(qg::qgemm_tc32_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          int(qg::kTcSmemBytes));
     if (e == cudaSuccess)
       e = cudaFuncSetAttribute(qg::qgemm_tc32_2cta_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                int(qg::kTc2SmemBytes));
     if (e != cudaSuccess) return int(e);
-    if (dev < kMaxDev) attr_set[dev] = true;
+    if (dev < kMaxDev) attr_set[dev].store(true, std::memory_order_release);
   }
   if (QG_TC32_2CTA) {
     qg::Tc2Args t{};
@@ -616,14 +620,13 @@ bool use_small(int64_t M, int64_t N, int64_t K) {
 }
 
 int num_sms() {
-  static int sms = 0;
-  if (sms > 0) return sms;
+  static std::atomic<int> cache[kMaxDev];
   int dev = 0, v = 0;
-  if (cudaGetDevice(&dev) != cudaSuccess ||
-      cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || v <= 0)
-    return 148;
-  sms = v;
-  return sms;
+  if (cudaGetDevice(&dev) != cudaSuccess) return 148;
+  if (dev < kMaxDev && (v = cache[dev].load(std::memory_order_relaxed)) > 0) return v;
+  if (cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || v <= 0) return 148;
+  if (dev < kMaxDev) cache[dev].store(v, std::memory_order_relaxed);
+  return v;
 }
 
 #ifndef QG_SMALL_CLUSTER_MIN_STEPS

@@ -9,6 +9,7 @@
 // needs is root's C mapped into every rank's address space: a CUDA IPC handle
 // of the allocation that holds it, plus the byte offset of C inside that
 // allocation (allocators such as PyTorch's hand out interior pointers).
+#include <atomic>
 #include <cstdint>
 #include <cstring>
 #include <cuda.h>
@@ -23,15 +24,15 @@ using AddressRangeFn = CUresult (*)(CUdeviceptr *, size_t *, CUdeviceptr);
 // cuMemGetAddressRange through the runtime's driver entry point, so that the
 // library does not link libcuda (it must load on machines without a driver).
 AddressRangeFn address_range() {
-  static AddressRangeFn fn = nullptr;
-  if (fn) return fn;
+  static std::atomic<AddressRangeFn> fn{nullptr};  // (any host thread may make the first call)
+  if (AddressRangeFn f = fn.load(std::memory_order_acquire)) return f;
   void *p = nullptr;
   cudaDriverEntryPointQueryResult q;
   if (cudaGetDriverEntryPoint("cuMemGetAddressRange", &p, cudaEnableDefault, &q) != cudaSuccess ||
       q != cudaDriverEntryPointSuccess)
     return nullptr;
-  fn = reinterpret_cast<AddressRangeFn>(p);
-  return fn;
+  fn.store(reinterpret_cast<AddressRangeFn>(p), std::memory_order_release);
+  return reinterpret_cast<AddressRangeFn>(p);
 }
 
 }  // namespace

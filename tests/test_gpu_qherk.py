@@ -70,6 +70,15 @@ def test_qherk_exact_integer(uplo, trans, policy):
         _case(130, 256, uplo, trans, 0.75, -0.5, seed=4)
 
 
+@pytest.mark.parametrize("uplo", ["L", "U"])
+@pytest.mark.parametrize("trans", ["N", "H"])
+def test_qherk_multi_band_exact(uplo, trans):
+    """N = 1297 -> 21 tile rows: two full bands of 8 tile rows of the banded
+    triangle raster plus a partial band of 5, a ragged last tile row, stream-K
+    over the remainder; exact-integer inputs -> bitwise."""
+    _case(1297, 40, uplo, trans, 2.0, 1.0, seed=5, dist="int8", exact=True)
+
+
 def test_qherk_quick_returns_and_scale():
     N, K = 40, 8
     rng = np.random.default_rng(0)
