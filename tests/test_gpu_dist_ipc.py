@@ -26,15 +26,16 @@ from tests.tolerance import tolerance
 pytestmark = pytest.mark.gpu
 
 
-def _worker(rank, world, port, opA, opB, M, N, K, q):
+def _worker(rank, world, port, opA, opB, M, N, K, q, dist_kind="normal"):
     import paper_1903_05575_b200 as qg
     from paper_1903_05575_b200.dist import PeerC, qgemm_rowsharded_p2p, rows_for_rank
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     torch.cuda.set_device(0)
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
-        pr = make_problem(M, N, K, opA, opB, (0.5, 0.25, -1, 0.1), (1, -0.5, 0, 0.2), seed=7,
-                          dist="normal", ldc=M + 5)
+        exact = dist_kind == "int8"
+        pr = make_problem(M, N, K, opA, opB, (2, -1, 0, 1) if exact else (0.5, 0.25, -1, 0.1),
+                          (1, 0, -1, 0) if exact else (1, -0.5, 0, 0.2), seed=7, dist=dist_kind, ldc=M + 5)
         r0, r1 = rows_for_rank(M, world, rank)
         A_loc = (np.ascontiguousarray(pr.A[:, r0:r1, :]) if opA == "N"
                  else np.ascontiguousarray(pr.A[r0:r1, :, :]))
@@ -64,7 +65,17 @@ def _worker(rank, world, port, opA, opB, M, N, K, q):
             tol = 3 * tolerance("f64", K, pr.A, a_rows, pr.B, b_rows, pr.beta, ref, M)
             err = float(np.abs(got[:, :M] - ref[:, :M]).max())
             pad_ok = bool(np.array_equal(got[:, M:], pr.C[:, M:]))
-            q.put((err <= tol, err, tol, pad_ok, qg.last_launch_count() > 0))
+            ok = err <= tol
+            if exact:  # sharded == oracle == single-GPU qgemm on the whole problem, bitwise
+                C1 = torch.from_numpy(pr.C.copy()).to(dev)
+                A1 = torch.from_numpy(pr.A).to(dev)
+                for _ in range(2):
+                    qg.qgemm(opA, opB, pr.alpha, A1, torch.from_numpy(pr.B).to(dev), pr.beta, C1,
+                             M=M, N=N, K=K)
+                single = C1.cpu().numpy()
+                ok = (bool(np.array_equal(got[:, :M], ref[:, :M]))
+                      and bool(np.array_equal(got[:, :M], single[:, :M])))
+            q.put((ok, err, tol, pad_ok, qg.last_launch_count() > 0))
         dist.barrier()
         peer.close()
     finally:
@@ -79,12 +90,16 @@ def _free_port():
     return p
 
 
+@pytest.mark.parametrize("dist_kind", ["normal", "int8"])
 @pytest.mark.parametrize("opA,opB,M,N,K", [("N", "H", 400, 300, 257), ("T", "N", 130, 70, 65)])
-def test_p2p_epilogue_into_root_c_two_processes(opA, opB, M, N, K):
+def test_p2p_epilogue_into_root_c_two_processes(opA, opB, M, N, K, dist_kind):
+    """normal: within tolerance of the oracle; int8 (exact-integer inputs): the
+    sharded result is bitwise equal to the oracle and to the single-GPU qgemm of
+    the whole problem (SURVEY §8(e) invariant, T8)."""
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, 2, port, opA, opB, M, N, K, q))
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, opA, opB, M, N, K, q, dist_kind))
              for r in range(2)]
     for p in procs:
         p.start()
