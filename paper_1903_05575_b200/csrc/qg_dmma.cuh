@@ -55,6 +55,9 @@ constexpr int kConsumerRegs = 232;
 #ifndef QG_GROUP_M
 #define QG_GROUP_M 8
 #endif
+#ifndef QG_C_PREFETCH_BULK
+#define QG_C_PREFETCH_BULK 1  // 1: the producer lane bulk-prefetches C tiles; 0: consumer lanes prefetch per quaternion
+#endif
 #ifndef QG_C_PREFETCH_KT
 #define QG_C_PREFETCH_KT 2  // k-tiles before the end of a tile at which its C tile is prefetched to L2
 #endif
@@ -73,6 +76,44 @@ enum Feed : int {
 constexpr int kAccPerThread = 64;                      // doubles
 constexpr size_t kPartialBytes = size_t(kConsumerThreads) * kAccPerThread * sizeof(double);  // 128 KiB
 constexpr int kMaxPersistentCTAs = 256;
+
+// ---- optional phase trace (diagnostic builds only, -DQG_TRACE; read back with
+// qgemm_debug_trace): consumer thread 0 of every CTA stamps %globaltimer at
+// phase boundaries; event = (code << 56) | ns.  Codes: 1 consumers start,
+// 2 unit start, 3 unit k-loop done, 4 stream-K fixup done (contributor parked /
+// owner summed), 5 epilogue done, 6 consumers done.
+#ifdef QG_TRACE
+constexpr int kTraceEv = 48;
+__device__ unsigned long long g_trace[256][kTraceEv];
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+// (the last slot always holds the final event, so long unit lists keep it)
+#define QG_TR(code)                                                                                 \
+  do {                                                                                              \
+    if (threadIdx.x == 0 && (tr_n < kTraceEv - 1 || (code) == 6))                                   \
+      g_trace[blockIdx.x][(code) == 6 ? kTraceEv - 1 : tr_n++] =                                    \
+          ((unsigned long long)(code) << 56) | (gtimer() & ((1ull << 56) - 1));                     \
+  } while (0)
+// stamp once `dep` (a loaded value) is available: the asm takes it as an input
+#define QG_TR_DEP(code, dep)                                                                        \
+  do {                                                                                              \
+    if (threadIdx.x == 0 && tr_n < kTraceEv - 1) {                                                  \
+      unsigned long long t_;                                                                        \
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_) : "d"(dep));                             \
+      g_trace[blockIdx.x][tr_n++] = ((unsigned long long)(code) << 56) | (t_ & ((1ull << 56) - 1)); \
+    }                                                                                               \
+  } while (0)
+#else
+#define QG_TR(code) \
+  do {              \
+  } while (0)
+#define QG_TR_DEP(code, dep) \
+  do {                       \
+  } while (0)
+#endif
 
 struct alignas(64) DmmaArgs {
   CUtensorMap tmA, tmB;  // TMA feed: 3-D maps (component, view row, k) or (component, k, view row)
@@ -208,7 +249,27 @@ struct Producer {
   int slot;
   uint32_t phase;
   int64_t fills;
+  int64_t c_pref_kt;  // k-tile at which to L2-prefetch the unit's C tile (-1: none)
 };
+
+// L2 prefetch of the C tile (mt, nt) by the TMA engine: one bulk prefetch per
+// column (up to 64 quaternions = 2 KB contiguous).  Issued by the producer lane
+// QG_C_PREFETCH_KT k-tiles before a unit that runs the epilogue ends.
+__device__ __forceinline__ void prefetch_c_tile(const DmmaArgs &a, int64_t mt, int64_t nt) {
+  const int64_t r0 = mt * kBR, c0 = nt * kBR;
+  const int64_t rows = (a.M - r0) < kBR ? (a.M - r0) : kBR;
+  const int64_t cols = (a.N - c0) < kBR ? (a.N - c0) : kBR;
+  const uint32_t bytes = uint32_t(rows) * 32u;
+  for (int64_t j = 0; j < cols; ++j) {
+    const double *p = a.C + 4 * (r0 + (c0 + j) * a.ldc);
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;\n" ::"l"(p), "r"(bytes) : "memory");
+  }
+}
+__device__ __forceinline__ void producer_unit_prefetch(Producer &p, const DmmaArgs &a, const Unit &u) {
+  p.c_pref_kt = (QG_C_PREFETCH_BULK && QG_C_PREFETCH_KT > 0 && u.kb == 0 && !a.sc.beta_zero)
+                    ? (u.ke - QG_C_PREFETCH_KT > u.kb ? u.ke - QG_C_PREFETCH_KT : u.kb)
+                    : int64_t(-1);
+}
 
 // Issue the next fill (bulk copies of one A and one B chunk); false when done.
 __device__ __forceinline__ bool produce_next(Producer &p, const DmmaArgs &args, double *sA, double *sB,
@@ -217,13 +278,14 @@ __device__ __forceinline__ bool produce_next(Producer &p, const DmmaArgs &args, 
   while (p.kt >= p.ke) {
     Unit u;
     if (!p.it.next(args, u)) return false;
-    int64_t mt, nt;
-    work_tile(args, u.t, mt, nt);
-    p.a_src = args.Ap + mt * args.KT * kChunkElems;
-    p.b_src = args.Bp + nt * args.KT * kChunkElems;
+    work_tile(args, u.t, p.mt, p.nt);
+    p.a_src = args.Ap + p.mt * args.KT * kChunkElems;
+    p.b_src = args.Bp + p.nt * args.KT * kChunkElems;
     p.kt = u.kb;
     p.ke = u.ke;
+    producer_unit_prefetch(p, args, u);
   }
+  if (p.kt == p.c_pref_kt) prefetch_c_tile(args, p.mt, p.nt);
   if (p.fills >= kStages) mbar_wait(&empty[p.slot], p.phase ^ 1u);
   mbar_arrive_expect_tx(&full[p.slot], 2 * kBytes);
   bulk_g2s(sA + p.slot * kChunkElems, p.a_src + p.kt * kChunkElems, kBytes, &full[p.slot]);
@@ -267,7 +329,9 @@ __device__ __forceinline__ bool produce_next_tma(Producer &p, const DmmaArgs &ar
     work_tile(args, u.t, p.mt, p.nt);
     p.kt = u.kb;
     p.ke = u.ke;
+    producer_unit_prefetch(p, args, u);
   }
+  if (p.kt == p.c_pref_kt) prefetch_c_tile(args, p.mt, p.nt);
   if (p.fills >= kStages) mbar_wait(&empty[p.slot], p.phase ^ 1u);
   mbar_arrive_expect_tx(&full[p.slot], 2 * kBytes);
   const int k0 = int(p.kt * kBK), ra = int(p.mt * kBR), rb = int(p.nt * kBR);
@@ -408,6 +472,8 @@ __global__ void __launch_bounds__(kDmmaThreads, 1) qgemm_dmma_kernel(const __gri
   prod.slot = 0;
   prod.phase = 0;
   prod.fills = 0;
+  prod.c_pref_kt = -1;
+  prod.mt = prod.nt = 0;
   if (warp >= kConsumerWarps) {
     asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;\n" ::"n"(kProducerRegs));
     if constexpr (kFeed == kFeedTma || kFeed == kFeedTma128) {
@@ -435,7 +501,10 @@ __global__ void __launch_bounds__(kDmmaThreads, 1) qgemm_dmma_kernel(const __gri
   uint32_t phase = 0;
   WorkIter it = make_iter(args, sp);
   Unit u;
+  [[maybe_unused]] int tr_n = 0;
+  QG_TR(1);
   while (it.next(args, u)) {
+    QG_TR(2);
     double acc[4][2][4][2];
 #pragma unroll
     for (int i = 0; i < 4; ++i)
@@ -445,7 +514,7 @@ __global__ void __launch_bounds__(kDmmaThreads, 1) qgemm_dmma_kernel(const __gri
         for (int c = 0; c < 4; ++c) acc[i][j][c][0] = acc[i][j][c][1] = 0.0;
 
     // k-tile at which to warm L2 with this unit's C tile (beta != 0, epilogue here)
-    const int64_t kt_prefetch = (QG_C_PREFETCH_KT > 0 && u.kb == 0 && !args.sc.beta_zero)
+    const int64_t kt_prefetch = (!QG_C_PREFETCH_BULK && QG_C_PREFETCH_KT > 0 && u.kb == 0 && !args.sc.beta_zero)
                                     ? (u.ke - QG_C_PREFETCH_KT > u.kb ? u.ke - QG_C_PREFETCH_KT : u.kb)
                                     : int64_t(-1);
     for (int64_t kt = u.kb; kt < u.ke; ++kt) {
@@ -524,6 +593,7 @@ __global__ void __launch_bounds__(kDmmaThreads, 1) qgemm_dmma_kernel(const __gri
       if (++slot == kStages) { slot = 0; phase ^= 1u; }
     }
 
+    QG_TR(3);
     const bool whole = (u.kb == 0 && u.ke == KT);
     if (!whole) {
       // stream-K fixup (only tiles >= dp_tiles are ever split)
@@ -542,6 +612,7 @@ __global__ void __launch_bounds__(kDmmaThreads, 1) qgemm_dmma_kernel(const __gri
         __threadfence();
         consumer_bar();
         if (tid == 0) atomicAdd(&args.flags[lt], 1);
+        QG_TR(4);
         continue;
       }
       // owner: wait for every other CTA holding a piece of this tile, add their partials
@@ -575,6 +646,7 @@ __global__ void __launch_bounds__(kDmmaThreads, 1) qgemm_dmma_kernel(const __gri
       }
     }
 
+    QG_TR(4);
     // ---------------- epilogue ----------------
     // D fragment of m8n8k4: lane holds D[lane/4][2*(lane%4) + e], e = 0, 1.
     int64_t mt, nt;
@@ -601,6 +673,7 @@ __global__ void __launch_bounds__(kDmmaThreads, 1) qgemm_dmma_kernel(const __gri
             cp[i2][jj][e] = args.C + 4 * (row + col * args.ldc);
             if (!args.sc.beta_zero && ok[i2][jj][e]) ldq_c(cp[i2][jj][e], cold[i2][jj][e]);
           }
+      QG_TR_DEP(7 + h, cold[0][0][0][0]);  // batch h's first C load has landed
 #pragma unroll
       for (int i2 = 0; i2 < 2; ++i2)
 #pragma unroll
@@ -627,7 +700,9 @@ __global__ void __launch_bounds__(kDmmaThreads, 1) qgemm_dmma_kernel(const __gri
             stq(cp[i2][jj][e], out);
           }
     }
+    QG_TR(5);
   }
+  QG_TR(6);
 }
 
 }  // namespace qg

@@ -284,4 +284,18 @@ const char *qgemm_version(void) {
          "FP32 tcgen05 3xTF32; one-launch small kernel)";
 }
 
+#ifdef QG_TRACE
+// Diagnostic builds only (-DQG_TRACE, not declared in include/qgemm.h): copy the
+// DMMA kernel's phase trace (256 CTAs x 48 events, see qg_dmma.cuh) to host and
+// clear it.
+int qgemm_debug_trace(unsigned long long *host, int n) {
+  const size_t bytes = std::min(size_t(n), size_t(256 * qg::kTraceEv)) * sizeof(unsigned long long);
+  cudaError_t e = cudaDeviceSynchronize();
+  if (e == cudaSuccess) e = cudaMemcpyFromSymbol(host, qg::g_trace, bytes);
+  static unsigned long long zeros[256 * qg::kTraceEv];
+  if (e == cudaSuccess) e = cudaMemcpyToSymbol(qg::g_trace, zeros, sizeof(zeros));
+  return int(e);
+}
+#endif
+
 }  // extern "C"
