@@ -8,8 +8,9 @@ alpha=beta=1, components i.i.d. N(0,1), FP64 -- the config the north star's
 scaling, rank r owns an 8192-row block of C and A (M = 8192 N), B is broadcast
 from rank 0 with NCCL every step and C is gathered to rank 0 (dist.py).
 
-A "step" = one qgemm call = pack A + pack B + DMMA mainloop with fused
-epilogue.  Inputs (2.15 GB per matrix) are far
+A "step" = one qgemm call = the DMMA mainloop fed by TMA straight from the
+interleaved storage (rows a2+a3 fused into it), with the fused epilogue
+(SURVEY §8(a) rows a1-a5); under the packed policy, pack A + pack B + mainloop.  Inputs (2.15 GB per matrix) are far
 larger than the 126 MB L2, so no flush is needed between steps.
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
@@ -224,7 +225,8 @@ def make_roofline(precision, achieved, main_ms, step_ms, pack_ms, steps):
         return {"bound": "tensor", "kernel": "qgemm_dmma_kernel", "achieved": achieved,
                 "peak": FP64_DMMA_PEAK_TFLOPS, "unit": "TFLOP/s",
                 "frac": (achieved / FP64_DMMA_PEAK_TFLOPS) if achieved else None,
-                "traffic": _traffic("f64_mainloop_bytes_per_launch"),
+                "traffic": _traffic("f64_mainloop_bytes_per_launch" if pack_ms else
+                                    "f64_direct_mainloop_bytes_per_launch"),
                 "peak_source": "measured DMMA.8x8x4 loop on this pool's B200, "
                                "tools/microbench/fp64_pipes.cu (profiles/r01_fp64_pipes.txt)",
                 "frac_of_nominal_37_22": (achieved / FP64_NOMINAL_TFLOPS) if achieved else None,
@@ -554,7 +556,8 @@ def run_ours(args):
                                ("+bcastB+p2p-epilogue-into-root-C" if peer is not None
                                 else "+bcastB+gatherC") if world > 1 else ""),
                            "l2": "inputs (2.15 GB/matrix) >> 126 MB L2; no flush",
-                           "timed": "pack A + pack B + DMMA mainloop/epilogue per step"
+                           "timed": ("pack A + pack B + DMMA mainloop/epilogue per step" if pack_cnt else
+                                     "TMA-fed DMMA mainloop/epilogue (no pack) per step")
                                     + ((" + NCCL broadcast(B) + epilogue stores into root's C "
                                         "over NVLink + completion all_reduce" if peer is not None
                                         else " + NCCL broadcast(B) + gather(C)")

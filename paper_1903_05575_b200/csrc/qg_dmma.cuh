@@ -55,6 +55,9 @@ constexpr int kConsumerRegs = 232;
 #ifndef QG_GROUP_M
 #define QG_GROUP_M 8
 #endif
+#ifndef QG_C_RING
+#define QG_C_RING 1  // epilogue C tiles through the ring by TMA (see produce_c_stage)
+#endif
 #ifndef QG_C_PREFETCH_BULK
 #define QG_C_PREFETCH_BULK 1  // 1: the producer lane bulk-prefetches C tiles; 0: consumer lanes prefetch per quaternion
 #endif
@@ -117,6 +120,8 @@ __device__ __forceinline__ unsigned long long gtimer() {
 
 struct alignas(64) DmmaArgs {
   CUtensorMap tmA, tmB;  // TMA feed: 3-D maps (component, view row, k) or (component, k, view row)
+  CUtensorMap tmC;       // QG_C_RING: C as (component, column, row), box 4 x 64 x 16, 32-byte swizzle
+  int c_ring;            // host: C tiles through the ring for this launch (see launch_dmma)
   const double *Ap;  // packed path: packed A panel, MT x KT chunks
   const double *Bp;  // packed path: packed B panel, NT x KT chunks
   // TMA feed: op(A) / op(B) read in place as R x K views -- X~(r, k) at
@@ -240,6 +245,24 @@ __device__ __forceinline__ int ld_acquire(const int *p) {
   return v;
 }
 
+// 3-D TMA tile load completing on an mbarrier (transaction bytes).
+__device__ __forceinline__ void tma_load_3d(void *dst, const CUtensorMap *tm, int c0, int c1, int c2,
+                                            uint64_t *bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], "
+      "[%5];\n" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(tm)), "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(bar))
+      : "memory");
+}
+
+// 3-D TMA tile store from shared memory (bulk-group completion).
+__device__ __forceinline__ void tma_store_3d(const CUtensorMap *tm, const void *src, int c0, int c1, int c2) {
+  asm volatile("cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%1, %2, %3}], [%4];\n" ::"l"(
+                   reinterpret_cast<uint64_t>(tm)),
+               "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(src))
+               : "memory");
+}
+
 // Producer cursor over the CTA's (unit, k-tile) sequence.
 struct Producer {
   WorkIter it;
@@ -250,7 +273,43 @@ struct Producer {
   uint32_t phase;
   int64_t fills;
   int64_t c_pref_kt;  // k-tile at which to L2-prefetch the unit's C tile (-1: none)
+  int c_left;         // QG_C_RING: C stages still to issue for the current unit
+  bool c_load;        // ... and whether they load C (beta != 0, or QHERK)
 };
+
+// ---- C through the ring (QG_C_RING): a unit that runs the epilogue is
+// followed in the ring by two C stages -- batch h = rows 16h.. and 32 + 16h..
+// of the 64 x 64 tile, one 32 KB TMA box each ([row 16][col 64][4 comps],
+// 32-byte swizzle) into the slot's A and B halves, i.e. the quaternions consumer
+// half wm of batch h owns.  The consumers read C from shared memory, write the
+// results back in place and one thread TMA-stores the boxes (the TMA unit clips
+// the M / N edges): the epilogue's global traffic runs at TMA rates instead of
+// 128-bit per-lane loads and stores with 64 KB in flight per batch.
+// Without a C read (beta = 0, not QHERK) there are no C stages: the plain
+// per-lane store epilogue is faster there.  QHERK always loads C, so the
+// untouched triangle of a diagonal tile is stored back unchanged.
+constexpr uint32_t kCBoxBytes = 16u * 64u * 32u;  // 32 KB = one slot half
+__device__ __forceinline__ void produce_c_stage(Producer &p, const DmmaArgs &args, double *sA, double *sB,
+                                                uint64_t *full, uint64_t *empty) {
+  const int h = 2 - p.c_left;
+  if (p.fills >= kStages) mbar_wait(&empty[p.slot], p.phase ^ 1u);
+  if (p.c_load) {
+    mbar_arrive_expect_tx(&full[p.slot], 2 * kCBoxBytes);
+    const int n0 = int(p.nt * kBR), r0 = int(p.mt * kBR) + 16 * h;
+    tma_load_3d(sA + p.slot * kChunkElems, &args.tmC, 0, n0, r0, &full[p.slot]);
+    tma_load_3d(sB + p.slot * kChunkElems, &args.tmC, 0, n0, r0 + 32, &full[p.slot]);
+  } else {
+    mbar_arrive(&full[p.slot]);
+  }
+  if (++p.slot == kStages) { p.slot = 0; p.phase ^= 1u; }
+  --p.c_left;
+  ++p.fills;
+}
+template <bool kRing>
+__device__ __forceinline__ void producer_unit_c(Producer &p, const DmmaArgs &a, const Unit &u) {
+  p.c_load = !a.sc.beta_zero || a.tri != 0;
+  p.c_left = (kRing && a.c_ring && u.kb == 0 && p.c_load) ? 2 : 0;
+}
 
 // L2 prefetch of the C tile (mt, nt) by the TMA engine: one bulk prefetch per
 // column (up to 64 quaternions = 2 KB contiguous).  Issued by the producer lane
@@ -265,8 +324,10 @@ __device__ __forceinline__ void prefetch_c_tile(const DmmaArgs &a, int64_t mt, i
     asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;\n" ::"l"(p), "r"(bytes) : "memory");
   }
 }
+template <bool kRing>
 __device__ __forceinline__ void producer_unit_prefetch(Producer &p, const DmmaArgs &a, const Unit &u) {
-  p.c_pref_kt = (QG_C_PREFETCH_BULK && QG_C_PREFETCH_KT > 0 && u.kb == 0 && !a.sc.beta_zero)
+  p.c_pref_kt = (!(kRing && a.c_ring) && QG_C_PREFETCH_BULK && QG_C_PREFETCH_KT > 0 && u.kb == 0 &&
+                 !a.sc.beta_zero)
                     ? (u.ke - QG_C_PREFETCH_KT > u.kb ? u.ke - QG_C_PREFETCH_KT : u.kb)
                     : int64_t(-1);
 }
@@ -283,7 +344,7 @@ __device__ __forceinline__ bool produce_next(Producer &p, const DmmaArgs &args, 
     p.b_src = args.Bp + p.nt * args.KT * kChunkElems;
     p.kt = u.kb;
     p.ke = u.ke;
-    producer_unit_prefetch(p, args, u);
+    producer_unit_prefetch<false>(p, args, u);
   }
   if (p.kt == p.c_pref_kt) prefetch_c_tile(args, p.mt, p.nt);
   if (p.fills >= kStages) mbar_wait(&empty[p.slot], p.phase ^ 1u);
@@ -310,26 +371,23 @@ __device__ __forceinline__ bool produce_next(Producer &p, const DmmaArgs &args, 
 // time, and those 8 lanes hit only 2 bank groups when rows are contiguous
 // (4-way conflicts; ncu) or 4 when k is contiguous (2-way) -- the price of not
 // packing, which auto pays only where the sweep shows it wins.
-__device__ __forceinline__ void tma_load_3d(void *dst, const CUtensorMap *tm, int c0, int c1, int c2,
-                                            uint64_t *bar) {
-  asm volatile(
-      "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], "
-      "[%5];\n" ::"r"(smem_u32(dst)),
-      "l"(reinterpret_cast<uint64_t>(tm)), "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(bar))
-      : "memory");
-}
 
 template <bool kG4>
 __device__ __forceinline__ bool produce_next_tma(Producer &p, const DmmaArgs &args, double *sA, double *sB,
                                                  uint64_t *full, uint64_t *empty) {
   constexpr uint32_t kBytes = kChunkElems * sizeof(double);
-  while (p.kt >= p.ke) {
+  while (p.kt >= p.ke && p.c_left == 0) {
     Unit u;
     if (!p.it.next(args, u)) return false;
     work_tile(args, u.t, p.mt, p.nt);
     p.kt = u.kb;
     p.ke = u.ke;
-    producer_unit_prefetch(p, args, u);
+    producer_unit_prefetch<QG_C_RING>(p, args, u);
+    producer_unit_c<QG_C_RING>(p, args, u);
+  }
+  if (p.kt >= p.ke) {
+    produce_c_stage(p, args, sA, sB, full, empty);
+    return true;
   }
   if (p.kt == p.c_pref_kt) prefetch_c_tile(args, p.mt, p.nt);
   if (p.fills >= kStages) mbar_wait(&empty[p.slot], p.phase ^ 1u);
@@ -437,6 +495,10 @@ __device__ __forceinline__ uint32_t g4_frag_off(int rc, const G4Lane &t, int ks,
 // contiguous -- compile-time, so the fragment offsets fold into immediates.
 template <int kFeed, bool CA, bool CB, int kRC = 0>
 __global__ void __launch_bounds__(kDmmaThreads, 1) qgemm_dmma_kernel(const __grid_constant__ DmmaArgs args) {
+  // C tiles through the ring only in the direct-feed instantiations: it speeds
+  // up c2 (direct, 1.3%) but slowed the packed kernel at c3 / c4 (A/B in one run,
+  // DESIGN.md §6) -- and code it does not use changed the packed kernel's code
+  constexpr bool kRing = QG_C_RING && kFeed != kFeedPacked;
   extern __shared__ __align__(128) unsigned char smem_dyn[];
   // (offset arithmetic on the shared array, not an integer round trip, so the
   // compiler keeps shared-space loads: LDS, not generic LD)
@@ -473,6 +535,8 @@ __global__ void __launch_bounds__(kDmmaThreads, 1) qgemm_dmma_kernel(const __gri
   prod.phase = 0;
   prod.fills = 0;
   prod.c_pref_kt = -1;
+  prod.c_left = 0;
+  prod.c_load = false;
   prod.mt = prod.nt = 0;
   if (warp >= kConsumerWarps) {
     asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;\n" ::"n"(kProducerRegs));
@@ -514,7 +578,8 @@ __global__ void __launch_bounds__(kDmmaThreads, 1) qgemm_dmma_kernel(const __gri
         for (int c = 0; c < 4; ++c) acc[i][j][c][0] = acc[i][j][c][1] = 0.0;
 
     // k-tile at which to warm L2 with this unit's C tile (beta != 0, epilogue here)
-    const int64_t kt_prefetch = (!QG_C_PREFETCH_BULK && QG_C_PREFETCH_KT > 0 && u.kb == 0 && !args.sc.beta_zero)
+    const int64_t kt_prefetch = (!(kRing && args.c_ring) && !QG_C_PREFETCH_BULK && QG_C_PREFETCH_KT > 0 && u.kb == 0 &&
+                                 !args.sc.beta_zero)
                                     ? (u.ke - QG_C_PREFETCH_KT > u.kb ? u.ke - QG_C_PREFETCH_KT : u.kb)
                                     : int64_t(-1);
     for (int64_t kt = u.kb; kt < u.ke; ++kt) {
@@ -651,6 +716,66 @@ __global__ void __launch_bounds__(kDmmaThreads, 1) qgemm_dmma_kernel(const __gri
     // D fragment of m8n8k4: lane holds D[lane/4][2*(lane%4) + e], e = 0, 1.
     int64_t mt, nt;
     work_tile(args, u.t, mt, nt);
+    // (beta = 0 outside QHERK: no C read -- the plain store path below is faster)
+    if (kRing && args.c_ring && (!args.sc.beta_zero || args.tri != 0)) {
+      // C tile through the ring (produce_c_stage): read, update in place, TMA store.
+      int slots[2];
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        slots[h] = slot;
+        mbar_wait(&full[slot], phase);
+        unsigned char *box = reinterpret_cast<unsigned char *>((wm ? sB : sA) + slot * kChunkElems);
+#pragma unroll
+        for (int i2 = 0; i2 < 2; ++i2)
+#pragma unroll
+          for (int jj = 0; jj < 2; ++jj)
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {
+              const int ii = 2 * h + i2;
+              const int rl = i2 * 8 + (lane >> 2);                    // row in the 16-row box
+              const int cl = (wn * 2 + jj) * 8 + 2 * (lane & 3) + e;  // column in the tile
+              const int64_t row = mt * kBR + (wm * 4 + ii) * 8 + (lane >> 2);
+              const int64_t col = nt * kBR + cl;
+              const bool ok = args.tri == 0 || (args.tri == 1 ? row >= col : row <= col);
+              if (!ok) continue;  // QHERK: the other triangle goes back as loaded
+              const uint32_t lin = uint32_t(rl * 64 + cl) * 32u;
+              double2 *q0 = reinterpret_cast<double2 *>(box + (lin ^ (((lin >> 7) & 1u) << 4)));
+              double2 *q1 = reinterpret_cast<double2 *>(box + ((lin + 16u) ^ ((((lin + 16u) >> 7) & 1u) << 4)));
+              const double q[4] = {acc[ii][jj][0][e], acc[ii][jj][1][e], acc[ii][jj][2][e], acc[ii][jj][3][e]};
+              double out[4];
+              left_scale(args.sc.alpha, args.sc.alpha_real, q, out);
+              if (!args.sc.beta_zero) {
+                const double2 c01 = *q0, c23 = *q1;
+                const double cold[4] = {c01.x, c01.y, c23.x, c23.y};
+                double bc[4];
+                left_scale(args.sc.beta, args.sc.beta_real, cold, bc);
+#pragma unroll
+                for (int k = 0; k < 4; ++k) out[k] += bc[k];
+              }
+              if (args.tri != 0 && row == col) out[1] = out[2] = out[3] = 0.0;  // real diagonal (R18)
+              *q0 = make_double2(out[0], out[1]);
+              *q1 = make_double2(out[2], out[3]);
+            }
+        asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");  // smem writes -> TMA store
+        consumer_bar();
+        if (tid == 0) {
+          const int n0 = int(nt * kBR), r0 = int(mt * kBR) + 16 * h;
+          tma_store_3d(&args.tmC, sA + slot * kChunkElems, 0, n0, r0);
+          tma_store_3d(&args.tmC, sB + slot * kChunkElems, 0, n0, r0 + 32);
+          asm volatile("cp.async.bulk.commit_group;\n" ::: "memory");
+        }
+        if (++slot == kStages) { slot = 0; phase ^= 1u; }
+      }
+      // the slots return to the producer once the TMA unit has read them
+      if (tid == 0) asm volatile("cp.async.bulk.wait_group.read 0;\n" ::: "memory");
+      consumer_bar();
+      if (lane == 0) {
+        mbar_arrive(&empty[slots[0]]);
+        mbar_arrive(&empty[slots[1]]);
+      }
+      QG_TR(5);
+      continue;
+    }
     // Two batches of 8 quaternions: all C loads of a batch are issued before
     // any store, so the 8 round trips overlap (the compiler cannot reorder
     // loads of C above stores to C on its own).
@@ -702,6 +827,7 @@ __global__ void __launch_bounds__(kDmmaThreads, 1) qgemm_dmma_kernel(const __gri
     }
     QG_TR(5);
   }
+  if (kRing && args.c_ring && tid == 0) asm volatile("cp.async.bulk.wait_group 0;\n" ::: "memory");
   QG_TR(6);
 }
 

@@ -288,6 +288,9 @@ int persistent_ctas() {
 // Full waves folded into the stream-K part (besides the partial last wave):
 // 0 = data-parallel for every full wave, stream-K over the remainder only
 // (c2: 35.32-35.51 vs 35.24-35.41 TFLOP/s graph-replayed with 1).
+#ifndef QG_C_RING_MIN_KT
+#define QG_C_RING_MIN_KT 32
+#endif
 #ifndef QG_SK_FULL_WAVES
 #define QG_SK_FULL_WAVES 0
 #endif
@@ -415,8 +418,32 @@ int encode_view_g4(CUtensorMap *tm, const double *X, int64_t ldx, int rc, int64_
   return r == CUDA_SUCCESS ? 0 : int(cudaErrorInvalidValue);
 }
 
+// C as (component, column, row) for the ring epilogue: box 4 x 64 columns x 16
+// rows = 32 KB, 32-byte swizzle (smem [row][col][component]).
+int encode_c(CUtensorMap *tm, const double *C, int64_t ldc, int64_t M, int64_t N) {
+  EncodeTiledFn fn = encode_tiled();
+  if (!fn) return int(cudaErrorNotSupported);
+  const cuuint64_t dims[3] = {4, cuuint64_t(N), cuuint64_t(M)};
+  const cuuint64_t strides[2] = {cuuint64_t(32) * cuuint64_t(ldc), 32};
+  const cuuint32_t box[3] = {4, 64, 16};
+  const cuuint32_t estr[3] = {1, 1, 1};
+  const CUresult r = fn(tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, const_cast<double *>(C), dims, strides, box, estr,
+                        CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_32B,
+                        CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS ? 0 : int(cudaErrorInvalidValue);
+}
+
 // Schedule + stream-K scratch + launch of a filled-in DmmaArgs (operands set).
 int launch_dmma(qg::DmmaArgs &a, DmmaKernel kernel, void *sk_scratch, cudaStream_t st) {
+  // the epilogue's C tiles go through the ring (qg_dmma.cuh produce_c_stage) --
+  // except for short-K full grids: at c4 (16 k-tiles per tile) the C boxes'
+  // TMA requests compete with the A/B stream (DMMA-active 94.7% vs 96.0%,
+  // 250.1 vs 247.4 ms), while c2 / c3 / QHERK gain
+  a.c_ring = QG_C_RING && (a.tri != 0 || a.KT >= QG_C_RING_MIN_KT);
+  if (a.c_ring) {
+    const int e = encode_c(&a.tmC, a.C, a.ldc, a.M, a.N);
+    if (e) return e;
+  }
   int rc = dmma_set_attributes();
   if (rc) return rc;
   const int resident = persistent_ctas();
@@ -563,24 +590,24 @@ int launch_mainloop(const float *Ap, const float *Bp, float *C, int64_t ldc, int
 }
 
 
-// Direct (TMA-fed) FP64 mainloop vs pack launch + mainloop, from the sweep in
-// profiles/r01p_feed_sweep_g4.jsonl (tools/feed_sweep.py).  With the
-// 4-quaternion-group tiles (conflict-free fragment loads) the direct path wins
-// from 384^3 to 4096^3 for every op pair (1.002-1.08x), at 2048^2 x 8192 and
-// 4096^2 x 1024, ties at 4096^2 x 256 and loses at 8192^2 x 256 (0.996x, c4's
-// shape) and by 0.1% at 8192^3 (c3).  Auto: direct when op(A) is T/H or
-// M*N*K <= 2^37; packed for K < 512 with M*N >= 2^22 (c4) and for larger
-// op(A) = N problems (c3, c5).
+// Direct (TMA-fed) FP64 mainloop vs pack launch + mainloop.  With the
+// 4-quaternion-group tiles (conflict-free fragment loads) and the C tiles
+// through the ring, the direct path wins at every size measured
+// (profiles/r01q_feed_sweep_ring.jsonl, r01q_ab_policy.txt): 384^3 1.08x, c2
+// 1.04x, 4096^3 1.010x, c3 1.006x, c4 (K = 256) 1.012x, QHERK at c4 1.018x.
+// Auto: direct whenever the group tiles apply (op(A) = N needs M % 4 == 0 and,
+// with op(B) = T/H, N % 4 == 0, else K % 4 == 0), and for op(A) = T/H always
+// (k-contiguous A: 2-way conflicts at worst); otherwise (32-byte tiles, 4-way
+// conflicts on a rows-contiguous op(A)) only up to 2^37 quaternion MACs.
 template <typename T>
-int direct_feed(int opA, int64_t M, int64_t N, int64_t K) {
+int direct_feed(int opA, int opB, int64_t M, int64_t N, int64_t K) {
   if (sizeof(T) != 8) return 0;
   const int pol = g_path_policy.load(std::memory_order_relaxed);
   if (pol == 3 || pol == 4) return qg::kFeedTma;
   if (pol != 0) return 0;
-  const double mn = double(M) * double(N);
-  if (K < 512 && mn >= double(int64_t(1) << 22)) return 0;  // c4-like: short K, big C
   if (opA != 0) return qg::kFeedTma;
-  return mn * double(K) <= double(int64_t(1) << 37) ? qg::kFeedTma : 0;
+  const bool g4 = M % 4 == 0 && (opB != 0 ? N % 4 == 0 : K % 4 == 0);
+  return (g4 || double(M) * double(N) * double(K) <= double(int64_t(1) << 37)) ? qg::kFeedTma : 0;
 }
 
 // Auto policy (crossover measured on B200 with tools/small_sweep.py, DESIGN.md §6;

@@ -61,7 +61,7 @@ int qgemm_impl(char transA, char transB, int64_t M, int64_t N, int64_t K, const 
     return launch_small<T>(A, lda, pa.row_contig, pa.conj, B, ldb, pb.row_contig, pb.conj, C, ldc, M, N, K,
                            alpha, beta, st);
   if constexpr (sizeof(T) == 8) {
-    if (const int feed = direct_feed<T>(sh.oa, M, N, K)) {  // one launch; workspace = stream-K scratch
+    if (const int feed = direct_feed<T>(sh.oa, sh.ob, M, N, K)) {  // one launch; workspace = stream-K scratch
       if (workspace == nullptr || (reinterpret_cast<uintptr_t>(workspace) & 255u)) return -14;
       if (workspace_bytes < sk_reserve<T>(M, N, cdiv(K, Geo<T>::kq))) return -15;
       return launch_mainloop_direct(feed, A, lda, pa.row_contig, pa.conj, B, ldb, pb.row_contig, pb.conj, C,
@@ -144,7 +144,7 @@ int qherk_impl(char uplo, char trans, int64_t N, int64_t K, double alpha, const 
   qg::Scalars<double> sc = make_scalars(al, be);
   if (!reads_a) return launch_scale(C, ldc, N, N, sc, st, tri);
   if (workspace == nullptr || (reinterpret_cast<uintptr_t>(workspace) & 255u)) return -11;
-  if (const int feed = direct_feed<double>(ot, N, N, K)) {
+  if (const int feed = direct_feed<double>(ot, ot == 0 ? 2 : 0, N, N, K)) {
     if (workspace_bytes < sk_reserve<double>(N, N, cdiv(K, qg::kBK))) return -12;
     // same operand views as the packed path below (conj folded into the signs)
     return launch_mainloop_direct(feed, A, lda, ot == 0 ? 1 : 0, ot == 0 ? 0 : 1, A, lda, ot == 0 ? 1 : 0,
@@ -163,7 +163,7 @@ template <typename T>
 size_t ws_bytes(char transA, char transB, int64_t M, int64_t N, int64_t K, bool minimum) {
   if (op_code(transA) < 0 || op_code(transB) < 0 || M <= 0 || N <= 0 || K <= 0) return 0;
   if (use_small<T>(M, N, K)) return 0;  // the small kernel needs no workspace
-  if (direct_feed<T>(op_code(transA), M, N, K))
+  if (direct_feed<T>(op_code(transA), op_code(transB), M, N, K))
     return sk_reserve<T>(M, N, cdiv(K, Geo<T>::kq));  // stream-K scratch only
   return workspace_for<T>(M, N, K, minimum ? 1 : cdiv(K, Geo<T>::kq));
 }
@@ -229,7 +229,7 @@ size_t qherk_workspace_bytes(char uplo, char trans, int64_t N, int64_t K) {
   const int ot = op_code(trans);
   if (!(uplo == 'L' || uplo == 'l' || uplo == 'U' || uplo == 'u') || (ot != 0 && ot != 2) || N <= 0 || K <= 0)
     return 0;
-  if (direct_feed<double>(ot, N, N, K)) return sk_reserve<double>(N, N, cdiv(K, qg::kBK));
+  if (direct_feed<double>(ot, ot == 0 ? 2 : 0, N, N, K)) return sk_reserve<double>(N, N, cdiv(K, qg::kBK));
   return workspace_for<double>(N, N, K, cdiv(K, qg::kBK));
 }
 

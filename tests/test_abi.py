@@ -128,6 +128,7 @@ def test_qherk_invalid_arguments(lib, kw, code):
 
 
 def test_workspace_sizes(lib):
+    old = lib.qgemm_set_path_policy(1)  # the packed path's sizes
     f64 = lib.qgemm_workspace_bytes(b"N", b"H", 8192, 8192, 8192, 0)
     f32 = lib.qgemm_workspace_bytes(b"N", b"H", 8192, 8192, 8192, 1)
     # packed A + B (no padding at tile multiples) + stream-K scratch of the FP64
@@ -141,6 +142,7 @@ def test_workspace_sizes(lib):
     assert lib.qgemm_workspace_min_bytes(b"N", b"N", 100, 70, 1000, 0) == 4 * 32768 + 126 * 131072 + 2048
     assert lib.qgemm_workspace_bytes(b"N", b"N", 0, 5, 5, 0) == 0
     assert lib.qgemm_workspace_bytes(b"X", b"N", 5, 5, 5, 0) == 0
+    lib.qgemm_set_path_policy(old)
 
 
 def test_path_policy_setter(lib):
@@ -164,13 +166,17 @@ def test_direct_path_workspace_is_stream_k_scratch(lib):
         assert lib.qgemm_workspace_min_bytes(b"N", b"H", 8192, 8192, 8192, 0) == sk
         assert lib.qgemm_workspace_bytes(b"N", b"H", 8192, 8192, 8192, 1) == 2 * 8192 * 8192 * 32
         assert lib.qherk_workspace_bytes(b"L", b"N", 32768, 256) == sk
-    for pol in (0, 1):  # auto: packed for c4's K = 256 and for c3 (op(A) = N, large)
-        lib.qgemm_set_path_policy(pol)
-        assert lib.qherk_workspace_bytes(b"L", b"N", 32768, 256) > sk
-        assert lib.qgemm_workspace_bytes(b"N", b"H", 8192, 8192, 8192, 0) > sk
-    lib.qgemm_set_path_policy(0)  # auto: direct for op(A) = T/H, and for N up to 1024^3
+    lib.qgemm_set_path_policy(1)  # packed
+    assert lib.qherk_workspace_bytes(b"L", b"N", 32768, 256) > sk
+    assert lib.qgemm_workspace_bytes(b"N", b"H", 8192, 8192, 8192, 0) > sk
+    # auto: direct wherever the 4-quaternion-group tiles apply (c3, c4, c5, QHERK),
+    # for op(A) = T/H, and up to 2^37 MACs otherwise; packed for a large ragged op(A) = N
+    lib.qgemm_set_path_policy(0)
+    assert lib.qherk_workspace_bytes(b"L", b"N", 32768, 256) == sk
+    assert lib.qgemm_workspace_bytes(b"N", b"H", 8192, 8192, 8192, 0) == sk
     assert lib.qgemm_workspace_bytes(b"T", b"N", 8192, 8192, 8192, 0) == sk
     assert lib.qgemm_workspace_bytes(b"N", b"N", 1024, 1024, 1024, 0) == sk
+    assert lib.qgemm_workspace_bytes(b"N", b"N", 8191, 8192, 8192, 0) > sk   # M % 4 != 0, > 2^37
 
 
 def test_small_path_needs_no_workspace(lib):

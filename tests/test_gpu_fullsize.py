@@ -96,21 +96,33 @@ def test_c4_full_size_every_entry_vs_oracle():
     _free()
 
 
-def test_c5_full_size_kpanel_nan_c():
-    """c5: M = N = K = 32768, N/N, alpha = 1, beta = 0 with C NaN-filled; 16 GB
-    workspace (K-panel loop); 66 x 66 sampled entries (incl. first/last
-    row/column) from the oracle on host-regenerated rows of A / columns of B."""
+@pytest.mark.parametrize("mode", ["packed_kpanels", "auto_direct"])
+def test_c5_full_size_kpanel_nan_c(mode):
+    """c5: M = N = K = 32768, N/N, alpha = 1, beta = 0 with C NaN-filled; either the
+    packed path with a 16 GB workspace (K-panel loop) or the auto path (TMA-fed
+    mainloop, one launch, stream-K scratch only); 66 x 66 sampled entries (incl.
+    first/last row/column) from the oracle on host-regenerated rows of A / columns of B."""
     n = 32768
     A = counter_matrix(0, 1, n, n, "cuda")
     B = counter_matrix(0, 2, n, n, "cuda")
     C = torch.full((n, n, 4), float("nan"), dtype=torch.float64, device="cuda")
-    ws_bytes = 16 * 10 ** 9
-    assert ws_bytes < qg.workspace_bytes("N", "N", n, n, n)
-    ws = torch.empty(ws_bytes, dtype=torch.uint8, device="cuda")
-    qg.qgemm("N", "N", 1.0, A, B, 0.0, C, workspace=ws)
-    torch.cuda.synchronize()
-    assert qg.last_launch_count() > 3          # several K-panels
-    assert bool(torch.isfinite(C).all())      # beta = 0: C never read (R3)
+    if mode == "packed_kpanels":
+        ws_bytes = 16 * 10 ** 9
+        old = qg.set_path_policy(qg.PATH_PACKED)
+        try:
+            assert ws_bytes < qg.workspace_bytes("N", "N", n, n, n)
+            ws = torch.empty(ws_bytes, dtype=torch.uint8, device="cuda")
+            qg.qgemm("N", "N", 1.0, A, B, 0.0, C, workspace=ws)
+            torch.cuda.synchronize()
+            assert qg.last_launch_count() > 3      # several K-panels
+        finally:
+            qg.set_path_policy(old)
+    else:
+        ws = None
+        qg.qgemm("N", "N", 1.0, A, B, 0.0, C)
+        torch.cuda.synchronize()
+        assert qg.last_launch_count() == 1         # no pack, no K-panels
+    assert bool(torch.isfinite(C).all())          # beta = 0: C never read (R3)
     rng = np.random.default_rng(5)
     rows = np.concatenate([[0, n - 1], rng.integers(0, n, 64)])
     cols = np.concatenate([[0, n - 1], rng.integers(0, n, 64)])

@@ -109,6 +109,22 @@ def test_f32_split_k_pair_kernel(M, N, K, opA, opB):
         assert_parity(pr, run_gpu(pr, "f32"), oracle_full(pr), exact=True)
 
 
+@pytest.mark.parametrize("M,N,K", [(130, 70, 520), (64, 1, 512), (1, 64, 600), (257, 129, 1000)])
+@pytest.mark.parametrize("opA,opB", OPS)
+@pytest.mark.parametrize("policy", [qg.PATH_PACKED, qg.PATH_DIRECT], ids=["packed", "direct"])
+def test_ring_epilogue_edges(M, N, K, opA, opB, policy):
+    """K >= 512 (>= 32 k-tiles): the FP64 epilogue reads C through the ring (TMA
+    load, update in shared memory, TMA store clipped at the M / N edges), on
+    ragged tiles, degenerate M or N, padded ld (sentinel in C's padding must
+    survive), quaternion alpha/beta; exact-integer inputs -> bitwise."""
+    with path_policy(policy):
+        pr = make_problem(M, N, K, opA, opB, QALPHA, QBETA, seed=15, ldc=M + 3)
+        assert_parity(pr, run_gpu(pr), oracle_full(pr))
+        pr = make_problem(M, N, K, opA, opB, (2, -1, 0, 3), (1, 0, -2, 1), seed=16, dist="int8",
+                          ldc=M + 3)
+        assert_parity(pr, run_gpu(pr), oracle_full(pr), exact=True)
+
+
 @pytest.mark.parametrize("opA,opB", OPS)
 def test_exact_integer_bitwise_f32(opA, opB, path):
     """P8 in FP32: |partial sums| <= 2^24, so FP32 is exact too."""

@@ -26,7 +26,7 @@ for pol_name, pol in (("auto", qg.PATH_AUTO), ("direct", qg.PATH_DIRECT)):
         torch.cuda.synchronize()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         best = 1e30
-        for _ in range(3):
+        for _ in range(6):
             e0.record()
             qg.qgemm("N", "H", 1.0, A, A, beta, C, M=n, N=n, K=K, workspace=ws)
             e1.record()
