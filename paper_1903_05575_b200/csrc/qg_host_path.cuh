@@ -45,6 +45,7 @@
 template <typename T>
 struct HostPlan {
   bool small = false;       // one-launch kernel on the whole problem (Q = P = 1)
+  bool direct = false;      // FP64 chunks on the TMA-fed mainloop (no pack)
   int64_t Kc0 = 0, Kc = 0, Q = 0;  // first K chunk (short: compute starts early), largest chunk, count
   int64_t Nj = 0, P = 0;    // C column panel width and count (last chunk / downloads)
   size_t off_cold = 0;      // device copy of the caller's C (beta != 0); off_C = 0
@@ -55,8 +56,11 @@ struct HostPlan {
 };
 
 template <typename T>
-HostPlan<T> host_plan(int64_t M, int64_t N, int64_t K) {
+HostPlan<T> host_plan(int oa, int ob, int64_t M, int64_t N, int64_t K) {
   HostPlan<T> h;
+  // FP64: each chunk's mainloop reads the staged operands in place (TMA-fed,
+  // no pack launch, no packed buffers) where the device path would
+  h.direct = sizeof(T) == 8 && K > 0 && direct_feed<T>(oa, ob, M, N, K) != 0;
   constexpr size_t qb = 4 * sizeof(T);
   const int64_t kq = Geo<T>::kq, rows = 128;  // panel width: multiple of both tile sizes (64, 128)
   h.small = use_small<T>(M, N, K);
@@ -92,13 +96,17 @@ HostPlan<T> host_plan(int64_t M, int64_t N, int64_t K) {
   const int nbuf = (h.Q > 1) ? 2 : 1;
   for (int i = 0; i < 2; ++i) { h.off_sa[i] = off; if (i < nbuf) off += sa; }
   for (int i = 0; i < 2; ++i) { h.off_sb[i] = off; if (i < nbuf) off += sb; }
-  if (!h.small && K > 0) {
+  if (!h.small && K > 0 && !h.direct) {
     const int64_t ktc = cdiv(h.Kc, kq);
     const size_t pa = align256(size_t(Geo<T>::a_tiles(M)) * size_t(ktc) * Geo<T>::chunk);
     const size_t pb = align256(size_t(cdiv(N, Geo<T>::rows)) * size_t(ktc) * Geo<T>::chunk);
     for (int i = 0; i < 2; ++i) { h.off_pa[i] = off; if (i < nbuf) off += pa; }
     for (int i = 0; i < 2; ++i) { h.off_pb[i] = off; if (i < nbuf) off += pb; }
     h.off_sk = off;  // (the last chunk's column panels may split differently: reserve for both)
+    off += std::max(sk_reserve<T>(M, N, cdiv(K, kq)), sk_reserve<T>(M, h.Nj, cdiv(K, kq)));
+  } else if (!h.small && K > 0) {  // direct: stream-K scratch only
+    for (int i = 0; i < 2; ++i) h.off_pa[i] = h.off_pb[i] = off;
+    h.off_sk = off;
     off += std::max(sk_reserve<T>(M, N, cdiv(K, kq)), sk_reserve<T>(M, h.Nj, cdiv(K, kq)));
   } else {
     for (int i = 0; i < 2; ++i) h.off_pa[i] = h.off_pb[i] = off;
@@ -158,7 +166,7 @@ int qgemm_host_impl(char transA, char transB, int64_t M, int64_t N, int64_t K, c
   if (rc != 0) return rc;
   if (M == 0 || N == 0) return 0;
   const int64_t Ke = reads_ab ? K : 0;  // alpha == 0 behaves as K == 0
-  const HostPlan<T> h = host_plan<T>(M, N, Ke);
+  const HostPlan<T> h = host_plan<T>(op_code(transA), op_code(transB), M, N, Ke);
   if (workspace == nullptr || (reinterpret_cast<uintptr_t>(workspace) & 255u)) return -14;
   if (workspace_bytes < h.total) return -15;
   cudaStream_t S = reinterpret_cast<cudaStream_t>(stream);
@@ -256,15 +264,34 @@ int qgemm_host_impl(char transA, char transB, int64_t M, int64_t N, int64_t K, c
     const int64_t ktn = cdiv(kc, Geo<T>::kq);
     T *pa = reinterpret_cast<T *>(ws + h.off_pa[sl]);
     T *pb = reinterpret_cast<T *>(ws + h.off_pb[sl]);
-    QH_TRY(launch_pack2<T>(pack_job<T>(reinterpret_cast<const T *>(ws + h.off_sa[sl]), lda_s, a_rc, a_cj, M, 0, kc, ktn, pa, true),
-                           pack_job<T>(reinterpret_cast<const T *>(ws + h.off_sb[sl]), ldb_s, b_rc, b_cj, N, 0, kc, ktn, pb, false), S));
-    ++launches;
-    packed[size_t(p)] = hs.ev();
-    QH_TRY(int(cudaEventRecord(packed[size_t(p)], S)));
+    const T *sa = reinterpret_cast<const T *>(ws + h.off_sa[sl]);
+    const T *sb = reinterpret_cast<const T *>(ws + h.off_sb[sl]);
+    if (!h.direct) {
+      QH_TRY(launch_pack2<T>(pack_job<T>(sa, lda_s, a_rc, a_cj, M, 0, kc, ktn, pa, true),
+                             pack_job<T>(sb, ldb_s, b_rc, b_cj, N, 0, kc, ktn, pb, false), S));
+      ++launches;
+    }
+    // staging slot sl is free again once the pack (or, direct, the chunk's mainloop) has run
+    auto release_slot = [&]() -> int {
+      packed[size_t(p)] = hs.ev();
+      return int(cudaEventRecord(packed[size_t(p)], S));
+    };
+    // one mainloop over columns [n0, n0 + nj) of this chunk into Cdj
+    auto mainloop = [&](int64_t n0, int64_t nj, T *Cdj, const qg::Scalars<T> &s_) -> int {
+      if constexpr (sizeof(T) == 8) {
+        if (h.direct)
+          return launch_mainloop_direct(qg::kFeedTma, sa, lda_s, a_rc, a_cj, sb + 4 * (b_rc ? n0 : n0 * ldb_s),
+                                        ldb_s, b_rc, b_cj, Cdj, M, M, nj, kc, s_, sk, S);
+      }
+      const T *pbj = pb + size_t(n0 / Geo<T>::rows) * size_t(ktn) * (Geo<T>::chunk / sizeof(T));
+      return launch_mainloop(pa, pbj, Cdj, M, M, nj, ktn, s_, sk, S);
+    };
+    if (!h.direct) QH_TRY(release_slot());
     const qg::Scalars<T> &scp = p == 0 ? sc0 : sc_acc;
     if (p != h.Q - 1) {
-      QH_TRY(launch_mainloop(pa, pb, Cd, M, M, N, ktn, scp, sk, S));
+      QH_TRY(mainloop(0, N, Cd, scp));
       ++launches;
+      if (h.direct) QH_TRY(release_slot());
       if (!folded && p == p_fold) {
         QH_TRY(int(cudaStreamWaitEvent(S, c_up, 0)));
         QH_TRY(launch_axpby(Cd, M, Cold, M, M, N, sc, S));
@@ -276,9 +303,8 @@ int qgemm_host_impl(char transA, char transB, int64_t M, int64_t N, int64_t K, c
     if (!folded) QH_TRY(int(cudaStreamWaitEvent(S, c_up, 0)));
     for (int64_t j = 0; j < h.P; ++j) {  // last chunk: per column panel, each downloaded at once
       const int64_t n0 = j * h.Nj, nj = std::min<int64_t>(N, n0 + h.Nj) - n0;
-      const T *pbj = pb + size_t(n0 / Geo<T>::rows) * size_t(ktn) * (Geo<T>::chunk / sizeof(T));
       T *Cdj = Cd + 4 * (n0 * M);
-      QH_TRY(launch_mainloop(pa, pbj, Cdj, M, M, nj, ktn, scp, sk, S));
+      QH_TRY(mainloop(n0, nj, Cdj, scp));
       ++launches;
       if (!folded) {
         QH_TRY(launch_axpby(Cdj, M, Cold + 4 * (n0 * M), M, M, nj, sc, S));
@@ -297,6 +323,6 @@ int qgemm_host_impl(char transA, char transB, int64_t M, int64_t N, int64_t K, c
 template <typename T>
 size_t host_ws_bytes(char transA, char transB, int64_t M, int64_t N, int64_t K) {
   if (op_code(transA) < 0 || op_code(transB) < 0 || M <= 0 || N <= 0 || K < 0) return 0;
-  return host_plan<T>(M, N, K).total;
+  return host_plan<T>(op_code(transA), op_code(transB), M, N, K).total;
 }
 

@@ -36,15 +36,19 @@ def run_host(pr, precision="f64", pin=True, stream=None, workspace=None):
     return C.double().numpy()
 
 
+@pytest.mark.parametrize("policy", [qg.PATH_AUTO, qg.PATH_PACKED], ids=["auto_direct", "packed"])
 @pytest.mark.parametrize("opA,opB", OPS)
-def test_host_chunked_all_ops(opA, opB):
+def test_host_chunked_all_ops(opA, opB, policy):
     M, N, K = 300, 520, 700  # K chunks 64/256/380 (growing x2), C panels 256/256/8
     lda = (M if opA == "N" else K) + 3
     ldb = (K if opB == "N" else N) + 1
     pr = make_problem(M, N, K, opA, opB, QALPHA, QBETA, seed=21, lda=lda, ldb=ldb, ldc=M + 2)
-    assert_parity(pr, run_host(pr), oracle_full(pr))
-    # 3 packs (A+B per chunk), 2 full mainloops, 1 beta*C fold-in, 3 panel mainloops
-    assert qg.last_launch_count() == 3 + 2 + 1 + 3
+    with path_policy(policy):
+        assert_parity(pr, run_host(pr), oracle_full(pr))
+        # [3 packs (A+B per chunk), packed only] + 2 full mainloops + 1 beta*C
+        # fold-in + 3 panel mainloops; auto reads the staged chunks in place (TMA)
+        packs = 3 if policy == qg.PATH_PACKED else 0
+        assert qg.last_launch_count() == packs + 2 + 1 + 3
 
 
 @pytest.mark.parametrize("opA,opB", [("N", "H"), ("T", "N"), ("H", "T")])
