@@ -418,6 +418,19 @@ int encode_view_g4(CUtensorMap *tm, const double *X, int64_t ldx, int rc, int64_
   return r == CUDA_SUCCESS ? 0 : int(cudaErrorInvalidValue);
 }
 
+// The ring epilogue moves C with the TMA unit; C in another GPU's memory (the
+// multi-GPU driver stores row blocks straight into root's C over peer memory,
+// dist.qgemm_rowsharded_p2p) keeps the per-lane load / store epilogue.
+bool c_is_local(const void *C) {
+  cudaPointerAttributes at{};
+  int dev = 0;
+  if (cudaPointerGetAttributes(&at, C) != cudaSuccess || cudaGetDevice(&dev) != cudaSuccess) {
+    cudaGetLastError();  // (clear a sticky-free error from the query)
+    return false;
+  }
+  return at.type == cudaMemoryTypeDevice && at.device == dev;
+}
+
 // C as (component, column, row) for the ring epilogue: box 4 x 64 columns x 16
 // rows = 32 KB, 32-byte swizzle (smem [row][col][component]).
 int encode_c(CUtensorMap *tm, const double *C, int64_t ldc, int64_t M, int64_t N) {
@@ -439,7 +452,7 @@ int launch_dmma(qg::DmmaArgs &a, DmmaKernel kernel, void *sk_scratch, cudaStream
   // except for short-K full grids: at c4 (16 k-tiles per tile) the C boxes'
   // TMA requests compete with the A/B stream (DMMA-active 94.7% vs 96.0%,
   // 250.1 vs 247.4 ms), while c2 / c3 / QHERK gain
-  a.c_ring = QG_C_RING && (a.tri != 0 || a.KT >= QG_C_RING_MIN_KT);
+  a.c_ring = QG_C_RING && (a.tri != 0 || a.KT >= QG_C_RING_MIN_KT) && c_is_local(a.C);
   if (a.c_ring) {
     const int e = encode_c(&a.tmC, a.C, a.ldc, a.M, a.N);
     if (e) return e;
