@@ -200,9 +200,10 @@ int qgemm_naive(char transA, char transB, int64_t M, int64_t N, int64_t K,
  * 32-byte-swizzle tile feed (3 and auto load both operands as conflict-free
  * 4-quaternion-group tiles when the groups are whole: M, resp. N, a multiple
  * of 4 for op(A) = A, resp. op(B) = B^T / B^H, else K).  Auto = small kernel below the
- * crossover; above it FP64 takes the direct path when op(A) is T/H or
- * M*N*K <= 2^37, except for K < 512 with M*N >= 2^22 (packed), else packed;
- * FP32 packed.
+ * crossover; above it FP64 takes the direct path whenever the group tiles
+ * apply (op(A) = A: M % 4 == 0 and N % 4 (op(B) = B^T/B^H) resp. K % 4 == 0),
+ * when op(A) is T/H, and otherwise up to M*N*K <= 2^37; else packed; FP32
+ * packed (the tcgen05 pair kernel, split over K below one wave).
  * Returns the previous policy, or -1 (policy unchanged) for other values.
  * For tests and benchmarks; the result is correct under every policy. */
 int qgemm_set_path_policy(int policy);
