@@ -22,6 +22,12 @@
 #ifndef QG_HOST_GROWTH
 #define QG_HOST_GROWTH 2
 #endif
+#ifndef QG_HOST_BIG_LAST
+#define QG_HOST_BIG_LAST 1
+#endif
+#ifndef QG_HOST_LAST_SPLIT
+#define QG_HOST_LAST_SPLIT 4  // the last column panel is cut into this many (its download is exposed)
+#endif
 #ifndef QG_HOST_KC_MAX
 #define QG_HOST_KC_MAX 4096
 #endif
@@ -85,6 +91,14 @@ HostPlan<T> host_plan(int oa, int ob, int64_t M, int64_t N, int64_t K) {
       len = std::max<int64_t>(kc1, std::min<int64_t>(int64_t(QG_HOST_KC_MAX), len * QG_HOST_GROWTH));
     }
     h.Q = int64_t(h.kb.size()) - 1;
+    // the last chunk runs per column panel with each panel's download behind the
+    // next panel's compute: make it the longest chunk (a short remainder moves one
+    // place forward) so the compute per column dwarfs the download per column
+    if (QG_HOST_BIG_LAST && h.Q >= 3) {
+      const int64_t last = h.kb[size_t(h.Q)] - h.kb[size_t(h.Q - 1)];
+      const int64_t prev = h.kb[size_t(h.Q - 1)] - h.kb[size_t(h.Q - 2)];
+      if (last < prev) h.kb[size_t(h.Q - 1)] = h.kb[size_t(h.Q - 2)] + last;
+    }
     h.Nj = std::min<int64_t>(cdiv(N, rows) * rows, std::max<int64_t>(256, cdiv(cdiv(N, QG_HOST_PANELS), rows) * rows));
     h.P = cdiv(N, h.Nj);
   }
@@ -301,8 +315,17 @@ int qgemm_host_impl(char transA, char transB, int64_t M, int64_t N, int64_t K, c
       continue;
     }
     if (!folded) QH_TRY(int(cudaStreamWaitEvent(S, c_up, 0)));
-    for (int64_t j = 0; j < h.P; ++j) {  // last chunk: per column panel, each downloaded at once
+    // last chunk: per column panel, each downloaded at once; the very last panel
+    // in QG_HOST_LAST_SPLIT pieces (multiples of 128 columns: a packed FP32 B
+    // panel starts on a 128-column tile) so less is exposed
+    std::vector<std::pair<int64_t, int64_t>> panels;
+    for (int64_t j = 0; j < h.P; ++j) {
       const int64_t n0 = j * h.Nj, nj = std::min<int64_t>(N, n0 + h.Nj) - n0;
+      const int64_t piece = (j == h.P - 1) ? std::max<int64_t>(128, cdiv(cdiv(nj, QG_HOST_LAST_SPLIT), 128) * 128) : nj;
+      for (int64_t c = 0; c < nj; c += piece) panels.emplace_back(n0 + c, std::min(piece, nj - c));
+    }
+    for (const auto &pn : panels) {
+      const int64_t n0 = pn.first, nj = pn.second;
       T *Cdj = Cd + 4 * (n0 * M);
       QH_TRY(mainloop(n0, nj, Cdj, scp));
       ++launches;

@@ -51,6 +51,20 @@ def test_host_chunked_all_ops(opA, opB, policy):
         assert qg.last_launch_count() == packs + 2 + 1 + 3
 
 
+@pytest.mark.parametrize("precision", ["f64", "f32"])
+@pytest.mark.parametrize("opA,opB", [("N", "H"), ("T", "N")])
+def test_host_big_last_chunk_and_split_last_panel(opA, opB, precision):
+    """K = 1100 -> chunks 64/256/512/268, reordered so the longest runs last
+    (64/256/268/512); N = 1024 -> 4 column panels of 256, the last one cut in
+    two 128-column pieces (packed FP32 B panels start on 128-column tiles)."""
+    pr = make_problem(256, 1024, 1100, opA, opB, QALPHA, QBETA, seed=24,
+                      dist="normal" if precision == "f32" else "uniform")
+    got = run_host(pr, precision)
+    assert_parity(pr, got, oracle_full(pr), precision=precision)
+    if precision == "f64":  # direct chunks: 3 chunk mainloops + fold + 3 panels + 2 pieces
+        assert qg.last_launch_count() == 3 + 1 + 3 + 2
+
+
 @pytest.mark.parametrize("opA,opB", [("N", "H"), ("T", "N"), ("H", "T")])
 def test_host_f32_chunked(opA, opB):
     pr = make_problem(260, 700, 900, opA, opB, QALPHA, QBETA, seed=22, dist="normal")
