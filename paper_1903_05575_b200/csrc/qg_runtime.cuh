@@ -288,6 +288,9 @@ int persistent_ctas() {
 // Full waves folded into the stream-K part (besides the partial last wave):
 // 0 = data-parallel for every full wave, stream-K over the remainder only
 // (c2: 35.32-35.51 vs 35.24-35.41 TFLOP/s graph-replayed with 1).
+#ifndef QG_RING_TRI
+#define QG_RING_TRI 1  // QHERK launches take the ring whatever their K (c4 QHERK 125.0 vs 125.8 ms)
+#endif
 #ifndef QG_C_RING_MIN_KT
 #define QG_C_RING_MIN_KT 32
 #endif
@@ -452,7 +455,7 @@ int launch_dmma(qg::DmmaArgs &a, DmmaKernel kernel, void *sk_scratch, cudaStream
   // except for short-K full grids: at c4 (16 k-tiles per tile) the C boxes'
   // TMA requests compete with the A/B stream (DMMA-active 94.7% vs 96.0%,
   // 250.1 vs 247.4 ms), while c2 / c3 / QHERK gain
-  a.c_ring = QG_C_RING && (a.tri != 0 || a.KT >= QG_C_RING_MIN_KT) && c_is_local(a.C);
+  a.c_ring = QG_C_RING && ((QG_RING_TRI && a.tri != 0) || a.KT >= QG_C_RING_MIN_KT) && c_is_local(a.C);
   if (a.c_ring) {
     const int e = encode_c(&a.tmC, a.C, a.ldc, a.M, a.N);
     if (e) return e;
