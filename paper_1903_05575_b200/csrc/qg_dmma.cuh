@@ -18,17 +18,19 @@
 // CTA: 64x64 output quaternions, 8 consumer warps (2 in m x 4 in n, each a
 // 32x16 warp tile = 4x2 m8n8 tiles x 4 components = 64 f64 accumulators per
 // lane) + a producer warpgroup, one lane of which fills a 3-stage shared-memory
-// ring completing on mbarriers -- with 1-D bulk copies of packed chunks
-// (qg_pack.cuh FragLayout; SASS UBLKCP), or (the direct path, kFeedTma) with
-// TMA tensor-map loads of the user's interleaved tiles, de-interleaved by the
-// consumers' fragment addresses.  Epilogue: alpha (x) acc + beta (x) C, left
-// products, masked at the M/N edges, C re-interleaved in registers
-// (each lane owns whole quaternions).
+// ring completing on mbarriers -- with TMA tensor-map loads of the user's
+// interleaved tiles (the direct path, the default: kFeedTma128 4-quaternion
+// groups or kFeedTma 32-byte tiles), de-interleaved by the consumers' fragment
+// addresses, or with 1-D bulk copies of packed chunks (qg_pack.cuh FragLayout;
+// SASS UBLKCP).  Epilogue: alpha (x) acc + beta (x) C, left products
+// (P:493-500), masked at the M/N edges, each lane owning whole quaternions; in
+// the direct kernels the C tile travels through the same ring by TMA
+// (produce_c_stage).
 //
 // Schedule: persistent (one CTA per SM), "data-parallel + stream-K" hybrid.
-// Whole tiles are dealt round-robin while at least two full waves remain; the
-// remaining tiles' k-iterations are split evenly over all CTAs (stream-K), so
-// no SM idles in a partial last wave (c2: 256 tiles on 148 SMs).  A tile split
+// Whole tiles are dealt round-robin for every full wave; the remainder's
+// k-iterations are split evenly over all CTAs (stream-K), so no SM idles in a
+// partial last wave (c2: 256 tiles on 148 SMs).  A tile split
 // across CTAs is finished by the CTA holding its k = 0 segment (the "owner"):
 // the others park their partial accumulators in the workspace and bump the
 // tile's arrival counter; the owner adds them and runs the epilogue (the host
