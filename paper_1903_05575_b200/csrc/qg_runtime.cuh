@@ -288,6 +288,10 @@ int persistent_ctas() {
 // Full waves folded into the stream-K part (besides the partial last wave):
 // 0 = data-parallel for every full wave, stream-K over the remainder only
 // (c2: 35.32-35.51 vs 35.24-35.41 TFLOP/s graph-replayed with 1).
+#ifndef QG_G4_KROWS
+#define QG_G4_KROWS 1  // group tiles also for k-contiguous op(A) x rows-contiguous op(B)
+                        // (0.6-0.9% slower before the C ring, 0-0.5% faster with it)
+#endif
 #ifndef QG_RING_TRI
 #define QG_RING_TRI 1  // QHERK launches take the ring whatever their K (c4 QHERK 125.0 vs 125.8 ms)
 #endif
@@ -325,7 +329,7 @@ using DmmaKernel = void (*)(const qg::DmmaArgs);  // (__grid_constant__ is not p
 // op(B), kRC = 2: see launch_mainloop_direct; no such instantiation.)
 template <int F, bool CA, bool CB, int RC>
 DmmaKernel tma_inst() {
-  if constexpr (F == qg::kFeedTma128 && RC == 2) return nullptr;
+  if constexpr (F == qg::kFeedTma128 && RC == 2 && !QG_G4_KROWS) return nullptr;
   else return qg::qgemm_dmma_kernel<F, CA, CB, RC>;
 }
 template <int F>
@@ -519,12 +523,12 @@ int launch_mainloop_direct(int feed, const double *A, int64_t lda, int a_rc, int
   a.A = A; a.B = B; a.lda = lda; a.ldb = ldb; a.K = K; a.a_rc = a_rc; a.b_rc = b_rc;
   a.C = C; a.ldc = ldc; a.M = M; a.N = N; a.KT = cdiv(K, qg::kBK); a.sc = sc; a.tri = tri;
   // 4-quaternion-group tiles (conflict-free fragment loads, qg_dmma.cuh
-  // kFeedTma128) where both operands' group extents are whole -- except for a
-  // k-contiguous op(A) (T/H) with a rows-contiguous op(B) (T/H), where the
-  // group tiles measured 0.6-0.9% slower than the 32-byte ones despite zero
-  // bank conflicts (tools/feed_sweep.py, profiles/r01p_feed_sweep_g4.jsonl)
+  // kFeedTma128) where both operands' group extents are whole (for a
+  // k-contiguous op(A) with a rows-contiguous op(B) only since the C tiles go
+  // through the ring: before, the group tiles were 0.6-0.9% slower there,
+  // profiles/r01p_feed_sweep_g4.jsonl; now 0-0.5% faster, QG_G4_KROWS)
   if (feed == qg::kFeedTma && g_path_policy.load(std::memory_order_relaxed) != 4 && g4_ok(a_rc, M, K) &&
-      g4_ok(b_rc, N, K) && (a_rc || !b_rc))
+      g4_ok(b_rc, N, K) && (QG_G4_KROWS || a_rc || !b_rc))
     feed = qg::kFeedTma128;
   if (feed == qg::kFeedTma128) {
     int rc = encode_view_g4(&a.tmA, A, lda, a_rc, M, K);
