@@ -65,6 +65,15 @@ def test_host_big_last_chunk_and_split_last_panel(opA, opB, precision):
         assert qg.last_launch_count() == 3 + 1 + 3 + 2
 
 
+@pytest.mark.parametrize("opA,opB", [("N", "N"), ("T", "H"), ("H", "N")])
+def test_host_ragged_k_direct_chunks(opA, opB):
+    """K = 1001 (not a multiple of 4): the direct chunk mainloops fall back to the
+    32-byte tiles where an operand is k-contiguous; ragged last chunk, M, N not
+    multiples of 4 either; exact-integer inputs -> bitwise."""
+    pr = make_problem(203, 517, 1001, opA, opB, (2, -1, 0, 3), (1, 0, -2, 1), seed=25, dist="int8")
+    assert_parity(pr, run_host(pr), oracle_full(pr), exact=True)
+
+
 @pytest.mark.parametrize("opA,opB", [("N", "H"), ("T", "N"), ("H", "T")])
 def test_host_f32_chunked(opA, opB):
     pr = make_problem(260, 700, 900, opA, opB, QALPHA, QBETA, seed=22, dist="normal")
