@@ -348,21 +348,22 @@ data = []
 for (oa, ob), s in zip(ops, streams):
     A = torch.randn(n, n, 4, dtype=torch.float64, device="cuda")
     B = torch.randn(n, n, 4, dtype=torch.float64, device="cuda")
-    C = torch.zeros(n, n, 4, dtype=torch.float64, device="cuda")
-    data.append((oa, ob, A, B, C, s))
+    C0 = torch.randn(n, n, 4, dtype=torch.float64, device="cuda")
+    data.append((oa, ob, A, B, C0, torch.empty_like(C0), s))
 torch.cuda.synchronize()
 ref = []
-for oa, ob, A, B, C, s in data:  # serial reference run
-    C.zero_()
-    qg.qgemm(oa, ob, 1.0, A, B, 0.0, C)
+for oa, ob, A, B, C0, C, s in data:  # serial reference run (beta != 0: C goes through the ring)
+    C.copy_(C0)
+    qg.qgemm(oa, ob, 1.0, A, B, 0.5, C)
     ref.append(C.clone())
 torch.cuda.synchronize()
 for it in range(20):  # the three persistent grids in flight together
-    for oa, ob, A, B, C, s in data:
+    for oa, ob, A, B, C0, C, s in data:
         with torch.cuda.stream(s):
-            qg.qgemm(oa, ob, 1.0, A, B, 0.0, C)
+            C.copy_(C0)
+            qg.qgemm(oa, ob, 1.0, A, B, 0.5, C)
 torch.cuda.synchronize()
-for (oa, ob, A, B, C, s), r in zip(data, ref):
+for (oa, ob, A, B, C0, C, s), r in zip(data, ref):
     assert torch.equal(C, r), (oa, ob)  # same tile config -> bitwise
 print("OK")
 """
