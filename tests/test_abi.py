@@ -211,3 +211,17 @@ def test_small_path_validates_identically(lib, kw, code):
     lib.qgemm_set_path_policy(2)
     assert _call(lib, ws=None, wsb=0, **kw) == code
     assert lib.qgemm_last_launch_count() == 0
+
+
+def test_host_workspace_c3_plan(lib):
+    """qgemm_host at c3 (FP64, auto = direct chunks): caller's C + accumulator C
+    (2 x 2 GiB) + 2 staging slots per operand for the largest K-chunk (4096 k:
+    chunks 256, 1024, 2048, 768, 4096 after the longest-last reorder) + the
+    stream-K scratch; no packed buffers (the chunks are read in place)."""
+    lib.qgemm_set_path_policy(0)
+    n = 8192
+    sk = 256 * 131072 + 2048
+    assert lib.qgemm_host_workspace_bytes(b"N", b"H", n, n, n, 0) == 2 * n * n * 32 + 4 * n * 4096 * 32 + sk
+    old = lib.qgemm_set_path_policy(1)  # packed chunks: + 2 packed chunks per operand
+    assert lib.qgemm_host_workspace_bytes(b"N", b"H", n, n, n, 0) == 2 * n * n * 32 + 8 * n * 4096 * 32 + sk
+    lib.qgemm_set_path_policy(old)
