@@ -276,7 +276,7 @@ struct Producer {
   int64_t fills;
   int64_t c_pref_kt;  // k-tile at which to L2-prefetch the unit's C tile (-1: none)
   int c_left;         // QG_C_RING: C stages still to issue for the current unit
-  bool c_load;        // ... and whether they load C (beta != 0, or QHERK)
+  bool c_load;        // ... and whether they load C (beta != 0)
 };
 
 // ---- C through the ring (QG_C_RING): a unit that runs the epilogue is
@@ -288,8 +288,8 @@ struct Producer {
 // the M / N edges): the epilogue's global traffic runs at TMA rates instead of
 // 128-bit per-lane loads and stores with 64 KB in flight per batch.
 // Without a C read (beta = 0, not QHERK) there are no C stages: the plain
-// per-lane store epilogue is faster there.  QHERK always loads C, so the
-// untouched triangle of a diagonal tile is stored back unchanged.
+// per-lane store epilogue is faster there.  QHERK's off-diagonal tiles lie
+// wholly inside its triangle; its diagonal tiles never take the ring.
 constexpr uint32_t kCBoxBytes = 16u * 64u * 32u;  // 32 KB = one slot half
 __device__ __forceinline__ void produce_c_stage(Producer &p, const DmmaArgs &args, double *sA, double *sB,
                                                 uint64_t *full, uint64_t *empty) {
@@ -300,17 +300,25 @@ __device__ __forceinline__ void produce_c_stage(Producer &p, const DmmaArgs &arg
     const int n0 = int(p.nt * kBR), r0 = int(p.mt * kBR) + 16 * h;
     tma_load_3d(sA + p.slot * kChunkElems, &args.tmC, 0, n0, r0, &full[p.slot]);
     tma_load_3d(sB + p.slot * kChunkElems, &args.tmC, 0, n0, r0 + 32, &full[p.slot]);
-  } else {
+  } else {  // beta = 0 (QHERK off-diagonal tile): the box is overwritten whole
     mbar_arrive(&full[p.slot]);
   }
   if (++p.slot == kStages) { p.slot = 0; p.phase ^= 1u; }
   --p.c_left;
   ++p.fills;
 }
+// Whether a tile's epilogue takes the ring: beta != 0 or QHERK, except QHERK's
+// diagonal tiles -- a TMA store writes the whole box back, so the strict other
+// triangle (which qherk must never touch, qgemm.h) would be rewritten with the
+// values loaded earlier, losing a concurrent writer's update; those few tiles
+// (MT of MT(MT+1)/2) take the per-lane masked store epilogue instead.
+__device__ __forceinline__ bool ring_epilogue(const DmmaArgs &a, int64_t mt, int64_t nt) {
+  return a.c_ring && (!a.sc.beta_zero || a.tri != 0) && !(a.tri != 0 && mt == nt);
+}
 template <bool kRing>
 __device__ __forceinline__ void producer_unit_c(Producer &p, const DmmaArgs &a, const Unit &u) {
-  p.c_load = !a.sc.beta_zero || a.tri != 0;
-  p.c_left = (kRing && a.c_ring && u.kb == 0 && p.c_load) ? 2 : 0;
+  p.c_load = !a.sc.beta_zero;
+  p.c_left = (kRing && u.kb == 0 && ring_epilogue(a, p.mt, p.nt)) ? 2 : 0;
 }
 
 // L2 prefetch of the C tile (mt, nt) by the TMA engine: one bulk prefetch per
@@ -718,8 +726,9 @@ __global__ void __launch_bounds__(kDmmaThreads, 1) qgemm_dmma_kernel(const __gri
     // D fragment of m8n8k4: lane holds D[lane/4][2*(lane%4) + e], e = 0, 1.
     int64_t mt, nt;
     work_tile(args, u.t, mt, nt);
-    // (beta = 0 outside QHERK: no C read -- the plain store path below is faster)
-    if (kRing && args.c_ring && (!args.sc.beta_zero || args.tri != 0)) {
+    // (beta = 0 outside QHERK: no C read -- the plain store path below is faster;
+    // QHERK's diagonal tiles: masked per-lane stores, see ring_epilogue)
+    if (kRing && ring_epilogue(args, mt, nt)) {
       // C tile through the ring (produce_c_stage): read, update in place, TMA store.
       int slots[2];
 #pragma unroll
@@ -736,10 +745,6 @@ __global__ void __launch_bounds__(kDmmaThreads, 1) qgemm_dmma_kernel(const __gri
               const int ii = 2 * h + i2;
               const int rl = i2 * 8 + (lane >> 2);                    // row in the 16-row box
               const int cl = (wn * 2 + jj) * 8 + 2 * (lane & 3) + e;  // column in the tile
-              const int64_t row = mt * kBR + (wm * 4 + ii) * 8 + (lane >> 2);
-              const int64_t col = nt * kBR + cl;
-              const bool ok = args.tri == 0 || (args.tri == 1 ? row >= col : row <= col);
-              if (!ok) continue;  // QHERK: the other triangle goes back as loaded
               const uint32_t lin = uint32_t(rl * 64 + cl) * 32u;
               double2 *q0 = reinterpret_cast<double2 *>(box + (lin ^ (((lin >> 7) & 1u) << 4)));
               double2 *q1 = reinterpret_cast<double2 *>(box + ((lin + 16u) ^ ((((lin + 16u) >> 7) & 1u) << 4)));
@@ -754,7 +759,6 @@ __global__ void __launch_bounds__(kDmmaThreads, 1) qgemm_dmma_kernel(const __gri
 #pragma unroll
                 for (int k = 0; k < 4; ++k) out[k] += bc[k];
               }
-              if (args.tri != 0 && row == col) out[1] = out[2] = out[3] = 0.0;  // real diagonal (R18)
               *q0 = make_double2(out[0], out[1]);
               *q1 = make_double2(out[2], out[3]);
             }

@@ -57,6 +57,10 @@ struct HostPlan {
   size_t off_cold = 0;      // device copy of the caller's C (beta != 0); off_C = 0
   size_t off_sa[2], off_sb[2], off_pa[2], off_pb[2], off_sk = 0, total = 0;
   std::vector<int64_t> kb;  // chunk p covers k in [kb[p], kb[p+1])
+  // the last chunk's launches: (first column, width) per column panel -- the very
+  // last panel in QG_HOST_LAST_SPLIT pieces (multiples of 128 columns: a packed
+  // FP32 B panel starts on a 128-column tile) so less of its download is exposed
+  std::vector<std::pair<int64_t, int64_t>> panels;
   int64_t k_begin(int64_t p) const { return kb[size_t(p)]; }
   int64_t k_len(int64_t p) const { return kb[size_t(p) + 1] - kb[size_t(p)]; }
 };
@@ -101,6 +105,20 @@ HostPlan<T> host_plan(int oa, int ob, int64_t M, int64_t N, int64_t K) {
     }
     h.Nj = std::min<int64_t>(cdiv(N, rows) * rows, std::max<int64_t>(256, cdiv(cdiv(N, QG_HOST_PANELS), rows) * rows));
     h.P = cdiv(N, h.Nj);
+    for (int64_t j = 0; j < h.P; ++j) {
+      const int64_t n0 = j * h.Nj, nj = std::min<int64_t>(N, n0 + h.Nj) - n0;
+      const int64_t piece = (j == h.P - 1) ? std::max<int64_t>(128, cdiv(cdiv(nj, QG_HOST_LAST_SPLIT), 128) * 128) : nj;
+      for (int64_t c = 0; c < nj; c += piece) h.panels.emplace_back(n0 + c, std::min(piece, nj - c));
+    }
+  }
+  // stream-K / split-K scratch for EVERY mainloop width launched: N (chunks
+  // before the last) and each panel / piece width of the last chunk.  (The FP32
+  // split count is not monotone in the width: a narrow piece has fewer tile
+  // pairs than a wave and splits K where N and Nj did not.)
+  size_t sk_need = 0;
+  if (!h.small && K > 0) {
+    sk_need = sk_reserve<T>(M, N, cdiv(K, kq));
+    for (const auto &pn : h.panels) sk_need = std::max(sk_need, sk_reserve<T>(M, pn.second, cdiv(K, kq)));
   }
   const size_t csz = align256(size_t(M) * size_t(N) * qb);  // C, compact ld = M
   size_t off = csz;
@@ -116,12 +134,12 @@ HostPlan<T> host_plan(int oa, int ob, int64_t M, int64_t N, int64_t K) {
     const size_t pb = align256(size_t(cdiv(N, Geo<T>::rows)) * size_t(ktc) * Geo<T>::chunk);
     for (int i = 0; i < 2; ++i) { h.off_pa[i] = off; if (i < nbuf) off += pa; }
     for (int i = 0; i < 2; ++i) { h.off_pb[i] = off; if (i < nbuf) off += pb; }
-    h.off_sk = off;  // (the last chunk's column panels may split differently: reserve for both)
-    off += std::max(sk_reserve<T>(M, N, cdiv(K, kq)), sk_reserve<T>(M, h.Nj, cdiv(K, kq)));
+    h.off_sk = off;
+    off += sk_need;
   } else if (!h.small && K > 0) {  // direct: stream-K scratch only
     for (int i = 0; i < 2; ++i) h.off_pa[i] = h.off_pb[i] = off;
     h.off_sk = off;
-    off += std::max(sk_reserve<T>(M, N, cdiv(K, kq)), sk_reserve<T>(M, h.Nj, cdiv(K, kq)));
+    off += sk_need;
   } else {
     for (int i = 0; i < 2; ++i) h.off_pa[i] = h.off_pb[i] = off;
     h.off_sk = off;
@@ -315,16 +333,8 @@ int qgemm_host_impl(char transA, char transB, int64_t M, int64_t N, int64_t K, c
       continue;
     }
     if (!folded) QH_TRY(int(cudaStreamWaitEvent(S, c_up, 0)));
-    // last chunk: per column panel, each downloaded at once; the very last panel
-    // in QG_HOST_LAST_SPLIT pieces (multiples of 128 columns: a packed FP32 B
-    // panel starts on a 128-column tile) so less is exposed
-    std::vector<std::pair<int64_t, int64_t>> panels;
-    for (int64_t j = 0; j < h.P; ++j) {
-      const int64_t n0 = j * h.Nj, nj = std::min<int64_t>(N, n0 + h.Nj) - n0;
-      const int64_t piece = (j == h.P - 1) ? std::max<int64_t>(128, cdiv(cdiv(nj, QG_HOST_LAST_SPLIT), 128) * 128) : nj;
-      for (int64_t c = 0; c < nj; c += piece) panels.emplace_back(n0 + c, std::min(piece, nj - c));
-    }
-    for (const auto &pn : panels) {
+    // last chunk: per column panel (h.panels), each downloaded at once
+    for (const auto &pn : h.panels) {
       const int64_t n0 = pn.first, nj = pn.second;
       T *Cdj = Cd + 4 * (n0 * M);
       QH_TRY(mainloop(n0, nj, Cdj, scp));

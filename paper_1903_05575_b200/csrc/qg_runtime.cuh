@@ -431,8 +431,11 @@ int encode_view_g4(CUtensorMap *tm, const double *X, int64_t ldx, int rc, int64_
 bool c_is_local(const void *C) {
   cudaPointerAttributes at{};
   int dev = 0;
+  // a failed query leaves an error behind: clear only that one, never an error
+  // the caller had pending before this call
+  const bool pending = cudaPeekAtLastError() != cudaSuccess;
   if (cudaPointerGetAttributes(&at, C) != cudaSuccess || cudaGetDevice(&dev) != cudaSuccess) {
-    cudaGetLastError();  // (clear a sticky-free error from the query)
+    if (!pending) cudaGetLastError();
     return false;
   }
   return at.type == cudaMemoryTypeDevice && at.device == dev;
@@ -454,12 +457,14 @@ int encode_c(CUtensorMap *tm, const double *C, int64_t ldc, int64_t M, int64_t N
 }
 
 // Schedule + stream-K scratch + launch of a filled-in DmmaArgs (operands set).
-int launch_dmma(qg::DmmaArgs &a, DmmaKernel kernel, void *sk_scratch, cudaStream_t st) {
-  // the epilogue's C tiles go through the ring (qg_dmma.cuh produce_c_stage) --
-  // except for short-K full grids: at c4 (16 k-tiles per tile) the C boxes'
-  // TMA requests compete with the A/B stream (DMMA-active 94.7% vs 96.0%,
-  // 250.1 vs 247.4 ms), while c2 / c3 / QHERK gain
-  a.c_ring = QG_C_RING && ((QG_RING_TRI && a.tri != 0) || a.KT >= QG_C_RING_MIN_KT) && c_is_local(a.C);
+int launch_dmma(qg::DmmaArgs &a, DmmaKernel kernel, bool direct, void *sk_scratch, cudaStream_t st) {
+  // the direct kernels' epilogue C tiles go through the ring (qg_dmma.cuh
+  // produce_c_stage) -- except for short-K full grids: at c4 (16 k-tiles per
+  // tile) the C boxes' TMA requests compete with the A/B stream (DMMA-active
+  // 94.7% vs 96.0%, 250.1 vs 247.4 ms), while c2 / c3 / QHERK gain (DESIGN.md
+  // §6).  The packed kernel never takes the ring: no pointer query, no map.
+  a.c_ring = direct && QG_C_RING && ((QG_RING_TRI && a.tri != 0) || a.KT >= QG_C_RING_MIN_KT) &&
+             c_is_local(a.C);
   if (a.c_ring) {
     const int e = encode_c(&a.tmC, a.C, a.ldc, a.M, a.N);
     if (e) return e;
@@ -510,7 +515,7 @@ int launch_mainloop(const double *Ap, const double *Bp, double *C, int64_t ldc, 
                     int64_t KT, const qg::Scalars<double> &sc, void *sk_scratch, cudaStream_t st, int tri = 0) {
   qg::DmmaArgs a{};
   a.Ap = Ap; a.Bp = Bp; a.C = C; a.ldc = ldc; a.M = M; a.N = N; a.KT = KT; a.sc = sc; a.tri = tri;
-  return launch_dmma(a, dmma_kernel(qg::kFeedPacked, false, false), sk_scratch, st);
+  return launch_dmma(a, dmma_kernel(qg::kFeedPacked, false, false), false, sk_scratch, st);
 }
 
 // Direct path: op(A), op(B) read in place by the producer warpgroup (no pack
@@ -539,7 +544,7 @@ int launch_mainloop_direct(int feed, const double *A, int64_t lda, int a_rc, int
     if (!rc) rc = encode_view(&a.tmB, B, ldb, b_rc, N, K);
     if (rc) return rc;
   }
-  return launch_dmma(a, dmma_kernel(feed, a_cj != 0, b_cj != 0, a_rc, b_rc), sk_scratch, st);
+  return launch_dmma(a, dmma_kernel(feed, a_cj != 0, b_cj != 0, a_rc, b_rc), true, sk_scratch, st);
 }
 
 // 2-D view of a packed FP32 chunk array for the pair kernel's TMA: rows of

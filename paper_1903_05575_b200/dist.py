@@ -35,6 +35,12 @@ import torch.distributed as dist
 TILE = 64
 
 
+def _ld(t: torch.Tensor, name: str) -> int:
+    """Leading dimension of a (ncols, rows, 4) view (qgemm.leading_dim; no CUDA needed)."""
+    from .qgemm import leading_dim
+    return leading_dim(t, name)
+
+
 def rows_for_rank(M: int, world: int, rank: int, tile: int = TILE) -> tuple[int, int]:
     """[r0, r1) of the row block of `rank`: whole tiles split as evenly as possible."""
     tiles = (M + tile - 1) // tile
@@ -162,8 +168,15 @@ def qgemm_rowsharded_p2p(transA: str, transB: str, alpha, A_local: torch.Tensor,
     assert peer.ncols == N and peer.ldc >= M
     if broadcast_b:
         dist.broadcast(B, src=root, group=group)
+    else:
+        # peers read (beta != 0) and write root's C: order them after root's
+        # earlier work on C (the broadcast does that when it runs)
+        flag = torch.zeros(1, dtype=torch.float32, device=A_local.device)
+        dist.all_reduce(flag, group=group)
     if m_loc > 0:
-        lda = A_local.shape[1]
+        # A_local may be a row-block view of a larger stored A (c4: rows
+        # [r0, r1) of the broadcast A, lda = M): ld from the strides, not the shape
+        lda, ldb = _ld(A_local, "A_local"), _ld(B, "B")
         if local_gemm_ptr is None:
             from .qgemm import get_workspace, qgemm_ptr, workspace_bytes
             dt = A_local.dtype
@@ -174,11 +187,11 @@ def qgemm_rowsharded_p2p(transA: str, transB: str, alpha, A_local: torch.Tensor,
                 ws = get_workspace(need, A_local.device, cur) if need else None
             st = cur.cuda_stream
             qgemm_ptr(transA, transB, m_loc, N, K, alpha, A_local.data_ptr(), lda, B.data_ptr(),
-                      B.shape[1], beta, peer.row_addr(r0), peer.ldc,
+                      ldb, beta, peer.row_addr(r0), peer.ldc,
                       ws.data_ptr() if ws is not None else 0,
                       ws.numel() * ws.element_size() if ws is not None else 0, st, dtype=dt)
         else:
-            local_gemm_ptr(transA, transB, m_loc, N, K, alpha, A_local, lda, B, B.shape[1], beta,
+            local_gemm_ptr(transA, transB, m_loc, N, K, alpha, A_local, lda, B, ldb, beta,
                            peer.row_addr(r0), peer.ldc)
     if barrier:
         flag = torch.zeros(1, dtype=torch.float32, device=A_local.device)

@@ -36,13 +36,32 @@ def _ptr(t: torch.Tensor | None):
     return None if t is None else ctypes.c_void_p(t.data_ptr())
 
 
+def leading_dim(t: torch.Tensor, name: str = "X") -> int:
+    """Leading dimension (in quaternions) of a column-major (ncols, rows, 4) view.
+
+    A contiguous tensor has ld = shape[1]; a row-block view of a larger matrix,
+    X[:, r0:r1, :] (what the row-sharded driver hands each rank), keeps the
+    parent's column stride, so ld = stride(0) / 4.  Anything else (a
+    non-interleaved component stride, transposed or overlapping columns) is
+    rejected: the kernels address element (i, j) at base + 4 (i + j ld)."""
+    if t.dim() != 3 or t.shape[2] != 4:
+        raise ValueError(f"{name}: expected an (ncols, rows, 4) tensor")
+    if t.stride(2) != 1 or (t.shape[1] > 1 and t.stride(1) != 4):
+        raise ValueError(f"{name}: components and rows must be contiguous (strides (4 ld, 4, 1))")
+    if t.shape[0] <= 1:
+        return max(1, t.shape[1])
+    s0 = t.stride(0)
+    if s0 % 4 or s0 // 4 < t.shape[1]:
+        raise ValueError(f"{name}: column stride {s0} is not 4 * ld with ld >= {t.shape[1]}")
+    return s0 // 4
+
+
 def _check(t: torch.Tensor, name: str, dtype):
     if t.dtype != dtype:
         raise TypeError(f"{name}: expected {dtype}, got {t.dtype}")
     if not t.is_cuda:
         raise TypeError(f"{name}: must be a CUDA tensor (no CPU path exists)")
-    if t.dim() != 3 or t.shape[2] != 4 or not t.is_contiguous():
-        raise ValueError(f"{name}: expected a contiguous (ncols, ld, 4) tensor")
+    leading_dim(t, name)
 
 
 def infer_dims(transA: str, transB: str, A: torch.Tensor, B: torch.Tensor, C: torch.Tensor):
@@ -83,9 +102,9 @@ def get_workspace(nbytes: int, device, stream: torch.cuda.Stream | None = None) 
 def _call(fn, name, transA, transB, M, N, K, alpha, A, B, beta, C, dtype, workspace, ws_bytes,
           stream):
     al, be = _q4(alpha, dtype), _q4(beta, dtype)
-    lda = A.shape[1] if A is not None else 1
-    ldb = B.shape[1] if B is not None else 1
-    ldc = C.shape[1]
+    lda = leading_dim(A, "A") if A is not None else 1
+    ldb = leading_dim(B, "B") if B is not None else 1
+    ldc = leading_dim(C, "C")
     args = [transA.encode(), transB.encode(), M, N, K, ctypes.cast(al, ctypes.c_void_p), _ptr(A),
             lda, _ptr(B), ldb, ctypes.cast(be, ctypes.c_void_p), _ptr(C), ldc]
     if workspace is not Ellipsis:
@@ -108,7 +127,9 @@ def qgemm(transA: str, transB: str, alpha, A: torch.Tensor, B: torch.Tensor, bet
 def qgemm_f32(transA: str, transB: str, alpha, A: torch.Tensor, B: torch.Tensor, beta,
               C: torch.Tensor, M: int | None = None, N: int | None = None, K: int | None = None,
               workspace: torch.Tensor | None = None, stream: torch.cuda.Stream | None = None):
-    """FP32 variant (float storage, FP32 FMA arithmetic)."""
+    """FP32 variant: float storage, 3xTF32 products on the tcgen05 tensor cores with
+    FP32 accumulation, or FP64 DMMA on the widened values in the
+    one-launch small kernel; result rounded to FP32 once on store."""
     return _qgemm_typed(load().qgemm_f32, "qgemm_f32", torch.float32, transA, transB, alpha, A, B,
                         beta, C, M, N, K, workspace, stream)
 
@@ -260,8 +281,9 @@ def qherk(uplo: str, trans: str, alpha: float, A: torch.Tensor, beta: float, C: 
     if workspace is None:
         workspace = get_workspace(need, C.device, stream) if need else None
     nbytes = workspace.numel() * workspace.element_size() if workspace is not None else 0
-    rc = lib.qherk(uplo.encode(), trans.encode(), N, K, float(alpha), _ptr(A), A.shape[1],
-                   float(beta), _ptr(C), C.shape[1], _ptr(workspace), nbytes, ctypes.c_void_p(st))
+    rc = lib.qherk(uplo.encode(), trans.encode(), N, K, float(alpha), _ptr(A), leading_dim(A, "A"),
+                   float(beta), _ptr(C), leading_dim(C, "C"), _ptr(workspace), nbytes,
+                   ctypes.c_void_p(st))
     if rc != 0:
         err = QgemmError("qherk", rc)
         if rc < 0:

@@ -11,7 +11,7 @@ from __future__ import annotations
 import numpy as np
 import torch
 
-from .inputs import counter_uniform
+from .inputs import counter_uniform  # noqa: F401  (the numpy twin; tests compare the two)
 
 _M64 = (1 << 64) - 1
 
@@ -47,6 +47,35 @@ def counter_uniform_t(seed: int, mid: int, flat: torch.Tensor) -> torch.Tensor:
     return 2.0 * u - 1.0
 
 
+def counter_normal_t(seed: int, mid: int, flat: torch.Tensor) -> torch.Tensor:
+    """torch twin of synth.inputs.counter_normal (Box-Muller; device log/cos)."""
+    u1 = 0.5 * (counter_uniform_t(seed, mid, 2 * flat) + 1.0)
+    u2 = 0.5 * (counter_uniform_t(seed, mid, 2 * flat + 1) + 1.0)
+    return torch.sqrt(-2.0 * torch.log1p(-u1)) * torch.cos((2.0 * np.pi) * u2)
+
+
+def counter_block(seed: int, mid: int, ld: int, r0: int, nrows: int, c0: int, ncols: int,
+                  device, dist: str = "uniform", dtype=torch.float64,
+                  chunk_cols: int | None = None) -> torch.Tensor:
+    """Rows [r0, r0+nrows) x columns [c0, c0+ncols) of the global stored matrix
+    (leading dimension ld) whose scalar (i, j, c) is the counter draw at flat
+    index 4 (i + j ld) + c, generated on `device` as a compact (ncols, nrows, 4)
+    tensor: a rank's row block of a sharded matrix, or a column panel, without
+    materialising the rest (synth.inputs.counter_block_host is the numpy twin)."""
+    out = torch.empty((ncols, nrows, 4), dtype=dtype, device=device)
+    if ncols == 0 or nrows == 0:
+        return out
+    gen = counter_uniform_t if dist == "uniform" else counter_normal_t
+    step = chunk_cols or max(1, (1 << 25) // max(1, 4 * nrows))
+    i = torch.arange(r0, r0 + nrows, dtype=torch.int64, device=device).view(1, -1, 1)
+    c = torch.arange(4, dtype=torch.int64, device=device).view(1, 1, 4)
+    for j0 in range(0, ncols, step):
+        j1 = min(ncols, j0 + step)
+        j = torch.arange(c0 + j0, c0 + j1, dtype=torch.int64, device=device).view(-1, 1, 1)
+        out[j0:j1] = gen(seed, mid, 4 * (i + j * ld) + c).to(dtype)
+    return out
+
+
 def counter_matrix(seed: int, mid: int, rows: int, cols: int, device, dtype=torch.float64,
                    chunk: int = 1 << 26) -> torch.Tensor:
     """Stored rows x cols matrix (cols, rows, 4) (ld = rows) from the counter generator."""
@@ -60,12 +89,15 @@ def counter_matrix(seed: int, mid: int, rows: int, cols: int, device, dtype=torc
     return out
 
 
-def counter_hermitian(seed: int, mid: int, n: int, device, chunk_cols: int = 512) -> torch.Tensor:
+def counter_hermitian(seed: int, mid: int, n: int, device, chunk_cols: int = 512, r0: int = 0,
+                      nrows: int | None = None) -> torch.Tensor:
     """C = (X + X^H)/2 with X the counter matrix (seed, mid), n x n, ld = n
     (reading R14).  Entry (i, j): (X_ij + conj(X_ji)) / 2, computed from the
-    counter directly (no X materialised)."""
-    out = torch.empty((n, n, 4), dtype=torch.float64, device=device)
-    i = torch.arange(n, dtype=torch.int64, device=device).view(1, n, 1)
+    counter directly (no X materialised).  Rows [r0, r0 + nrows) only (default:
+    all), as a compact (n, nrows, 4) tensor: a rank's row block."""
+    nrows = n - r0 if nrows is None else nrows
+    out = torch.empty((n, nrows, 4), dtype=torch.float64, device=device)
+    i = torch.arange(r0, r0 + nrows, dtype=torch.int64, device=device).view(1, nrows, 1)
     c = torch.arange(4, dtype=torch.int64, device=device).view(1, 1, 4)
     sign = torch.tensor([1.0, -1.0, -1.0, -1.0], dtype=torch.float64, device=device)
     for j0 in range(0, n, chunk_cols):

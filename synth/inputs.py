@@ -102,6 +102,31 @@ def counter_uniform(seed: int, matrix_id: int, flat_index: np.ndarray) -> np.nda
     return 2.0 * u - 1.0
 
 
+def counter_normal(seed: int, matrix_id: int, flat_index: np.ndarray) -> np.ndarray:
+    """Standard normal value of scalar `flat_index` of matrix `matrix_id`:
+    Box-Muller on two counter draws (u1, u2) at counters 2f and 2f+1,
+    z = sqrt(-2 ln(1 - u1)) cos(2 pi u2)  (1 - u1 in (0, 1], so the log is finite).
+    Its torch twin (synth.gpu_gen.counter_normal_t) uses the device's log/cos:
+    equal to a few ulp, not bitwise."""
+    f = np.asarray(flat_index, dtype=np.uint64)
+    with np.errstate(over="ignore"):
+        u1 = 0.5 * (counter_uniform(seed, matrix_id, f * np.uint64(2)) + 1.0)
+        u2 = 0.5 * (counter_uniform(seed, matrix_id, f * np.uint64(2) + np.uint64(1)) + 1.0)
+    return np.sqrt(-2.0 * np.log1p(-u1)) * np.cos(2.0 * np.pi * u2)
+
+
+def counter_block_host(seed: int, matrix_id: int, ld: int, r0: int, nrows: int, c0: int,
+                       ncols: int, dist: str = "uniform") -> np.ndarray:
+    """Rows [r0, r0+nrows) x columns [c0, c0+ncols) of the stored matrix whose
+    scalar (i, j, c) is the counter draw at flat index 4 (i + j ld) + c, as a
+    compact (ncols, nrows, 4) array (ld = nrows)."""
+    i = np.arange(r0, r0 + nrows, dtype=np.int64).reshape(1, -1, 1)
+    j = np.arange(c0, c0 + ncols, dtype=np.int64).reshape(-1, 1, 1)
+    c = np.arange(4, dtype=np.int64).reshape(1, 1, 4)
+    flat = 4 * (i + j * ld) + c
+    return (counter_uniform if dist == "uniform" else counter_normal)(seed, matrix_id, flat)
+
+
 @dataclass
 class Problem:
     """One QGEMM call: C <- alpha op(A) op(B) + beta C (stored numpy arrays)."""

@@ -225,3 +225,23 @@ def test_host_workspace_c3_plan(lib):
     old = lib.qgemm_set_path_policy(1)  # packed chunks: + 2 packed chunks per operand
     assert lib.qgemm_host_workspace_bytes(b"N", b"H", n, n, n, 0) == 2 * n * n * 32 + 8 * n * 4096 * 32 + sk
     lib.qgemm_set_path_policy(old)
+
+
+@pytest.mark.parametrize("N", [8192, 1024])
+def test_host_workspace_f32_covers_every_panel_split(lib, N):
+    """qgemm_host_f32 (packed FP32 chunks, M = K = 8192): the last chunk runs per
+    column panel and its last panel in 128-column pieces; a 128-wide piece has
+    32 tile pairs (< one wave of 74) and splits K twice, so the plan must reserve
+    its split-K partials (32 pairs x 2 splits x 512 KiB = 32 MiB) even though the
+    full width and the panel width do not split.  (The reserve used to cover only
+    the full and the panel width: an out-of-bounds write of 32 MiB.)"""
+    lib.qgemm_set_path_policy(0)
+    M = K = 8192
+    qb = 16
+    kc = 4096                                    # chunks 256, 1024, 2048, 768, 4096
+    stage = 2 * M * kc * qb + 2 * N * kc * qb
+    ktc = kc // 8                                # FP32 k-tiles per chunk (8 k per tile)
+    packed = 2 * (2 * (M // 256)) * ktc * 32768 + 2 * (N // 128) * ktc * 32768
+    part = 32 * 2 * 2 * 65536 * 4                # pairs x S x 2 CTAs x 4x128x128 floats
+    want = 2 * M * N * qb + stage + packed + part
+    assert lib.qgemm_host_workspace_bytes(b"N", b"H", M, N, K, 1) == want

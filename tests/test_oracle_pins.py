@@ -363,3 +363,26 @@ def test_counter_generator_torch_cpu_matches_numpy():
     LH = L.transpose(1, 0, 2).copy()
     LH[..., 1:] *= -1
     np.testing.assert_array_equal(L, LH)
+
+
+def test_counter_block_generators():
+    """synth: a row/column block of the global counter matrix (a rank's shard) is
+    the slice of the whole matrix; torch and numpy twins agree (uniform bitwise,
+    Box-Muller normal to rounding); the normal draws have N(0,1) moments; a row
+    block of the Hermitian initialiser is the slice of the whole one."""
+    import torch
+    from synth.gpu_gen import counter_block, counter_hermitian, counter_matrix
+    from synth.inputs import counter_block_host
+    full = counter_matrix(4, 2, 50, 30, "cpu").numpy()
+    blk = counter_block(4, 2, 50, 7, 20, 3, 11, "cpu", chunk_cols=4).numpy()
+    np.testing.assert_array_equal(blk, full[3:14, 7:27, :])
+    np.testing.assert_array_equal(blk, counter_block_host(4, 2, 50, 7, 20, 3, 11))
+    zt = counter_block(1, 9, 300, 0, 300, 0, 200, "cpu", dist="normal").numpy()
+    zh = counter_block_host(1, 9, 300, 0, 300, 0, 200, dist="normal")
+    assert np.abs(zt - zh).max() <= 1e-14 * max(1.0, np.abs(zh).max())
+    assert abs(zh.mean()) < 0.01 and abs(zh.var() - 1.0) < 0.01
+    assert np.isfinite(zh).all()
+    H = counter_hermitian(5, 2, 30, "cpu").numpy()
+    Hr = counter_hermitian(5, 2, 30, "cpu", chunk_cols=4, r0=9, nrows=13).numpy()
+    np.testing.assert_array_equal(Hr, H[:, 9:22, :])
+    del torch
