@@ -192,6 +192,24 @@ int qgemm_naive(char transA, char transB, int64_t M, int64_t N, int64_t K,
                 const double *B, int64_t ldb, const double beta[4],
                 double *C, int64_t ldc, void *stream);
 
+/* Pack A / pack B alone (test hook for SURVEY.md §8(a) rows a2/a3; the packed
+ * path of qgemm() runs the same kernel, Alg. 4 PACK1 / Alg. 5 PACK2,
+ * P:1164-1202).  Packs the R x K panel X~ of op(X) into FP64 chunks:
+ *   operand 0 (A): X~(r, k) = op(X)(r, k), op(X) is R x K (X stored R x K for
+ *                  trans 'N', K x R for 'T'/'H');
+ *   operand 1 (B): X~(r, k) = op(X)(k, r), op(X) is K x R (X stored K x R for
+ *                  'N', R x K for 'T'/'H');
+ * trans 'H' (alias 'C') conjugates (components 1..3 negated).
+ * out: ceil(R/64) * ceil(K/16) chunks of 64 x 16 quaternions, chunk index
+ * rt * ceil(K/16) + kt; inside a chunk, component c of X~(64 rt + r, 16 kt + k)
+ * is the double at offset ((((k/4)*8 + r/8)*2 + c/2)*32 + 4(r%8) + k%4)*2 + c%2
+ * (the DMMA m8n8k4 fragment order); rows r >= R and k >= K are 0 (Alg. 2
+ * padding).  Device pointers X (16-byte aligned) and out; enqueued
+ * on `stream`.  Errors: trans=-1 operand=-2 R=-3 K=-4 X=-5 ldx=-6 out=-7
+ * out_bytes=-8 (too small); >0 cudaError_t.  R == 0 or K == 0: no-op. */
+int qgemm_pack_panel(char trans, int operand, int64_t R, int64_t K, const double *X, int64_t ldx,
+                     double *out, size_t out_bytes, void *stream);
+
 /* Path policy (process-wide): 0 = auto (default), 1 = always the packed
  * path (pack launch + persistent mainloop), 2 = always the one-launch small
  * kernel, 3 = direct (FP64: the persistent mainloop fed by TMA straight from

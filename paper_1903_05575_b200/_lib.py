@@ -16,7 +16,7 @@ EXPORTS = ("qgemm", "qgemm_f32", "qgemm_workspace_bytes", "qgemm_workspace_min_b
            "qgemm_naive", "qherk", "qherk_workspace_bytes", "qgemm_last_launch_count",
            "qgemm_set_path_policy", "qgemm_host", "qgemm_host_f32", "qgemm_host_workspace_bytes",
            "qgemm_ipc_handle", "qgemm_ipc_open", "qgemm_ipc_close",
-           "qgemm_timing_enable", "qgemm_timing_collect", "qgemm_version")
+           "qgemm_timing_enable", "qgemm_timing_collect", "qgemm_version", "qgemm_pack_panel")
 
 _lib = None
 
@@ -82,6 +82,8 @@ def load():
     lib.qherk.restype = ctypes.c_int
     lib.qherk_workspace_bytes.argtypes = [c, c, i64, i64]
     lib.qherk_workspace_bytes.restype = sz
+    lib.qgemm_pack_panel.argtypes = [c, ctypes.c_int, i64, i64, vp, i64, vp, sz, vp]
+    lib.qgemm_pack_panel.restype = ctypes.c_int
     lib.qgemm_timing_enable.argtypes = [ctypes.c_int]
     lib.qgemm_timing_enable.restype = None
     lib.qgemm_timing_collect.argtypes = [ctypes.POINTER(ctypes.c_double),

@@ -834,6 +834,11 @@ __global__ void __launch_bounds__(kDmmaThreads, 1) qgemm_dmma_kernel(const __gri
     QG_TR(5);
   }
   if (kRing && args.c_ring && tid == 0) asm volatile("cp.async.bulk.wait_group 0;\n" ::: "memory");
+  // Per-lane C stores may target another GPU's memory (the multi-GPU driver's
+  // epilogue stores into root's C over NVLink, dist.qgemm_rowsharded_p2p):
+  // make them visible at system scope before this CTA retires, so whatever the
+  // rank signals next (the completion all_reduce) is ordered after them.
+  if (!(kRing && args.c_ring)) asm volatile("fence.acq_rel.sys;\n" ::: "memory");
   QG_TR(6);
 }
 

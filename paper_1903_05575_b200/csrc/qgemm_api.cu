@@ -220,6 +220,29 @@ int qgemm_naive(char transA, char transB, int64_t M, int64_t N, int64_t K, const
   return int(cudaGetLastError());
 }
 
+int qgemm_pack_panel(char trans, int operand, int64_t R, int64_t K, const double *X, int64_t ldx, double *out,
+                     size_t out_bytes, void *stream) {
+  g_last_launches = 0;
+  const int op = op_code(trans);
+  if (op < 0) return -1;
+  if (operand != 0 && operand != 1) return -2;
+  if (R < 0) return -3;
+  if (K < 0) return -4;
+  // operand A: op N reads rows contiguously; operand B: op T/H does (qg_pack.cuh)
+  const int rc = operand == 0 ? (op == 0) : (op != 0);
+  if (ldx < std::max<int64_t>(1, rc ? R : K)) return -6;
+  if (R == 0 || K == 0) return 0;
+  if (X == nullptr || (reinterpret_cast<uintptr_t>(X) & 15u)) return -5;
+  const int64_t KT = cdiv(K, qg::kBK);
+  const size_t need = size_t(cdiv(R, qg::kBR)) * size_t(KT) * size_t(qg::kChunkElems) * sizeof(double);
+  if (out == nullptr || (reinterpret_cast<uintptr_t>(out) & 15u)) return -7;
+  if (out_bytes < need) return -8;
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  qg::PackJob<double> none{};
+  none.blocks = 0;
+  return launch_pack2<double>(pack_job<double>(X, ldx, rc, op == 2, R, 0, K, KT, out, operand == 0), none, st);
+}
+
 int qherk(char uplo, char trans, int64_t N, int64_t K, double alpha, const double *A, int64_t lda, double beta,
           double *C, int64_t ldc, void *workspace, size_t workspace_bytes, void *stream) {
   return qherk_impl(uplo, trans, N, K, alpha, A, lda, beta, C, ldc, workspace, workspace_bytes, stream);

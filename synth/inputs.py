@@ -115,16 +115,23 @@ def counter_normal(seed: int, matrix_id: int, flat_index: np.ndarray) -> np.ndar
     return np.sqrt(-2.0 * np.log1p(-u1)) * np.cos(2.0 * np.pi * u2)
 
 
-def counter_block_host(seed: int, matrix_id: int, ld: int, r0: int, nrows: int, c0: int,
-                       ncols: int, dist: str = "uniform") -> np.ndarray:
-    """Rows [r0, r0+nrows) x columns [c0, c0+ncols) of the stored matrix whose
-    scalar (i, j, c) is the counter draw at flat index 4 (i + j ld) + c, as a
-    compact (ncols, nrows, 4) array (ld = nrows)."""
-    i = np.arange(r0, r0 + nrows, dtype=np.int64).reshape(1, -1, 1)
-    j = np.arange(c0, c0 + ncols, dtype=np.int64).reshape(-1, 1, 1)
+def counter_gather_host(seed: int, matrix_id: int, ld: int, rows, cols,
+                        dist: str = "uniform") -> np.ndarray:
+    """Entries (rows x cols) of the stored matrix whose scalar (i, j, c) is the
+    counter draw at flat index 4 (i + j ld) + c, as a compact (len(cols),
+    len(rows), 4) array: the sampled rows / columns a parity check needs."""
+    i = np.asarray(rows, dtype=np.int64).reshape(1, -1, 1)
+    j = np.asarray(cols, dtype=np.int64).reshape(-1, 1, 1)
     c = np.arange(4, dtype=np.int64).reshape(1, 1, 4)
     flat = 4 * (i + j * ld) + c
     return (counter_uniform if dist == "uniform" else counter_normal)(seed, matrix_id, flat)
+
+
+def counter_block_host(seed: int, matrix_id: int, ld: int, r0: int, nrows: int, c0: int,
+                       ncols: int, dist: str = "uniform") -> np.ndarray:
+    """Rows [r0, r0+nrows) x columns [c0, c0+ncols) (counter_gather_host)."""
+    return counter_gather_host(seed, matrix_id, ld, np.arange(r0, r0 + nrows),
+                               np.arange(c0, c0 + ncols), dist)
 
 
 @dataclass

@@ -245,3 +245,23 @@ def test_host_workspace_f32_covers_every_panel_split(lib, N):
     part = 32 * 2 * 2 * 65536 * 4                # pairs x S x 2 CTAs x 4x128x128 floats
     want = 2 * M * N * qb + stage + packed + part
     assert lib.qgemm_host_workspace_bytes(b"N", b"H", M, N, K, 1) == want
+
+
+@pytest.mark.parametrize("args,code", [
+    ((b"X", 0, 64, 16, 0x1000, 64, 0x2000, 1 << 20), -1),
+    ((b"N", 2, 64, 16, 0x1000, 64, 0x2000, 1 << 20), -2),
+    ((b"N", 0, -1, 16, 0x1000, 64, 0x2000, 1 << 20), -3),
+    ((b"N", 0, 64, -1, 0x1000, 64, 0x2000, 1 << 20), -4),
+    ((b"N", 0, 64, 16, 0x1008, 64, 0x2000, 1 << 20), -5),
+    ((b"N", 0, 64, 16, 0x1000, 63, 0x2000, 1 << 20), -6),
+    ((b"T", 0, 64, 16, 0x1000, 15, 0x2000, 1 << 20), -6),
+    ((b"N", 1, 64, 16, 0x1000, 15, 0x2000, 1 << 20), -6),
+    ((b"N", 0, 64, 16, 0x1000, 64, None, 1 << 20), -7),
+    ((b"N", 0, 64, 16, 0x1000, 64, 0x2000, 64 * 16 * 32 - 1), -8),
+    ((b"N", 0, 0, 16, None, 64, None, 0), 0),
+])
+def test_pack_panel_validation(lib, args, code):
+    """qgemm_pack_panel (the a2/a3 test hook): every error code, nothing enqueued."""
+    tr, operand, R, K, X, ldx, out, nbytes = args
+    assert lib.qgemm_pack_panel(tr, operand, R, K, X, ldx, out, nbytes, None) == code
+    assert lib.qgemm_last_launch_count() == 0

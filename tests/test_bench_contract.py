@@ -33,7 +33,7 @@ def test_reference_arm_json_line():
 
 @pytest.mark.gpu
 def test_our_arm_json_line():
-    line = _run(["--size", "1024", "--steps", "3", "--warmup", "3", "--no-cpu"])
+    line = _run(["--size", "1024", "--steps", "3", "--warmup", "3", "--no-cpu", "--no-sharded"])
     for key in ("metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step", "higher_is_better",
                 "scaling", "vs_baseline", "dtype", "data", "config", "roofline", "e2e", "gpu_launches",
                 "clocks"):
@@ -47,3 +47,18 @@ def test_our_arm_json_line():
     assert e["h2d_bytes_per_step"] == 3 * 1024 * 1024 * 32 and e["d2h_bytes_per_step"] == 1024 * 1024 * 32
     assert "workload" in line["config"] and "sm_mhz" in line["clocks"]
     assert line["variants"]["c3_fp32"]["value"] > 1.0
+    # the headline workload re-run once from fresh inputs and checked against the oracle
+    assert line["parity"]["ok"] is True and line["parity_ok"] is True
+    assert line["parity"]["max_err"] <= line["parity"]["tol"]
+    assert line["paper_cpu"]["serial_peak_gflops"] == 24.0
+
+
+def test_reference_arm_and_cpu_baseline_use_one_sampler():
+    """the reference arm and cpu_baseline time the same oracle block
+    sampler (square blocks of c3's C, full K), so their rates agree."""
+    sys.path.insert(0, ROOT)
+    import bench
+    side = bench.oracle_block_side(256, 0.2)
+    assert 128 <= side <= 256 and side % 16 == 0
+    dt, fl = bench.oracle_block(256, 128, 128)
+    assert fl == 32.0 * 128 * 128 * 256 and dt > 0

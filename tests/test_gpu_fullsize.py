@@ -96,16 +96,65 @@ def test_c4_full_size_every_entry_vs_oracle():
     _free()
 
 
+@pytest.fixture(scope="module")
+def c5_reference():
+    """The oracle's side of c5's parity check, computed once:
+    64 full rows and 64 full columns of C = A B (alpha = 1, beta = 0) and the
+    right-hand side A (B X) of a block Freivalds check (tests/freivalds.py, column
+    blocks of 512).  Inputs: rows of A / columns of B from the host counter
+    generator; whole column panels of A and B regenerated panel by panel on the
+    device by the torch twin (bitwise equal, test_counter_generator_device_matches_host;
+    fresh tensors, not the buffers the kernel ran on) and copied to the host."""
+    from synth.gpu_gen import counter_block
+    from tests.freivalds import draw_x
+    n, bs, kc = 32768, 512, 1024
+    rng = np.random.default_rng(5)
+    rows = np.sort(np.concatenate([[0, n - 1], rng.choice(np.arange(1, n - 1), 62, replace=False)]))
+    cols = np.sort(np.concatenate([[0, n - 1], rng.choice(np.arange(1, n - 1), 62, replace=False)]))
+    x = draw_x(n, seed=11)
+    A_S = host_rows_N(0, 1, n, rows, n)                 # op(A) rows S: stored (K, 64, 4)
+    B_cols = host_cols(0, 2, n, cols, n)                # op(B) columns: stored (64, K, 4)
+    nb = n // bs
+    Y = np.zeros((nb, n, 4))                            # op(B) X, stored (nb, K, 4)
+    ref_rows = np.zeros((n, rows.size, 4))              # rows S of C, stored (N, 64, 4)
+    for v in range(nb):                                 # one pass over column panels of B
+        j0 = v * bs
+        Bp = counter_block(0, 2, n, 0, n, j0, bs, "cuda").cpu().numpy()   # (bs, K, 4)
+        Y[v] = oracle.qgemv("N", n, bs, Bp, x[j0:j0 + bs])
+        oracle.qgemm("N", "N", rows.size, bs, n, 1, A_S, Bp, 0, ref_rows[j0:j0 + bs])
+        del Bp
+    rhs = np.ascontiguousarray(np.concatenate([B_cols, Y], axis=0))   # (64 + nb, K, 4)
+    out = np.zeros((rhs.shape[0], n, 4))                # A [B_cols | Y], accumulated over k-panels
+    for k0 in range(0, n, kc):                          # one pass over column panels of A
+        Ap = counter_block(0, 1, n, 0, n, k0, kc, "cuda").cpu().numpy()   # (kc, M, 4)
+        oracle.qgemm("N", "N", n, rhs.shape[0], kc, 1, Ap, np.ascontiguousarray(rhs[:, k0:k0 + kc]),
+                     1, out)
+        del Ap
+    torch.cuda.empty_cache()
+    ref_cols, AY = out[:cols.size], out[cols.size:]
+    tol = 1e-12 * n * 1.0 * 1.0                         # max|A|, max|B| <= 1 (uniform[-1,1))
+    return dict(n=n, bs=bs, rows=rows, cols=cols, x=x, ref_rows=ref_rows, ref_cols=ref_cols,
+                AY=AY, tol=tol)
+
+
 @pytest.mark.parametrize("mode", ["packed_kpanels", "auto_direct"])
-def test_c5_full_size_kpanel_nan_c(mode):
+def test_c5_full_size_rows_cols_freivalds(mode, c5_reference):
     """c5: M = N = K = 32768, N/N, alpha = 1, beta = 0 with C NaN-filled; either the
     packed path with a 16 GB workspace (K-panel loop) or the auto path (TMA-fed
-    mainloop, one launch, stream-K scratch only); 66 x 66 sampled entries (incl.
-    first/last row/column) from the oracle on host-regenerated rows of A / columns of B."""
-    n = 32768
+    mainloop, one launch, stream-K scratch only).  Checked:
+      * every entry finite (beta = 0: C never read, R3);
+      * 64 full rows and 64 full columns (incl. the first and last) against the
+        oracle within the per-entry tolerance;
+      * block Freivalds over the whole C, below a bound calibrated on the 64 known
+        rows (tests/freivalds.py) that is itself < 5 x tol;
+      * negative control: one unsampled entry moved by 10 x tol fails it."""
+    from tests.freivalds import Check, qnorm
+    ref = c5_reference
+    n, bs, rows, cols, tol = ref["n"], ref["bs"], ref["rows"], ref["cols"], ref["tol"]
     A = counter_matrix(0, 1, n, n, "cuda")
     B = counter_matrix(0, 2, n, n, "cuda")
     C = torch.full((n, n, 4), float("nan"), dtype=torch.float64, device="cuda")
+    ws = None
     if mode == "packed_kpanels":
         ws_bytes = 16 * 10 ** 9
         old = qg.set_path_policy(qg.PATH_PACKED)
@@ -118,22 +167,33 @@ def test_c5_full_size_kpanel_nan_c(mode):
         finally:
             qg.set_path_policy(old)
     else:
-        ws = None
         qg.qgemm("N", "N", 1.0, A, B, 0.0, C)
         torch.cuda.synchronize()
         assert qg.last_launch_count() == 1         # no pack, no K-panels
+    del A, B, ws
+    torch.cuda.empty_cache()
     assert bool(torch.isfinite(C).all())          # beta = 0: C never read (R3)
-    rng = np.random.default_rng(5)
-    rows = np.concatenate([[0, n - 1], rng.integers(0, n, 64)])
-    cols = np.concatenate([[0, n - 1], rng.integers(0, n, 64)])
-    A_rows = host_rows_N(0, 1, n, rows, n)     # op(A) rows: stored (K, |R|, 4)
-    B_cols = host_cols(0, 2, n, cols, n)       # op(B) columns: stored (|S|, K, 4)
-    ref = np.zeros((cols.size, rows.size, 4))
-    oracle.qgemm("N", "N", rows.size, cols.size, n, 1, np.ascontiguousarray(A_rows), B_cols, 0, ref)
-    got = C[torch.from_numpy(cols).cuda()][:, torch.from_numpy(rows).cuda()].cpu().numpy()
-    tol = 1e-12 * n * max(np.abs(A_rows).max(), 1e-300) * np.abs(B_cols).max()
-    # max over the sampled operands is <= the global max: a stricter tolerance
-    err = float(np.abs(got - ref).max())
+    got_rows = C[:, torch.from_numpy(rows).cuda(), :].cpu().numpy()     # (N, 64, 4)
+    got_cols = C[torch.from_numpy(cols).cuda()].cpu().numpy()           # (64, M, 4)
+    err = max(float(np.abs(got_rows - ref["ref_rows"]).max()),
+              float(np.abs(got_cols - ref["ref_cols"]).max()))
     assert err <= tol, (err, tol)
-    del A, B, C, ws
+    chk = Check(n, n, bs, ref["x"], ref["AY"])     # beta = 0: no C0 X term
+    bound = chk.bound(ref["ref_rows"], got_rows, rows)
+    assert bound < 5 * tol, (bound, tol)
+    bad_j, bad_i = 20000, 12345                    # neither sampled (asserted below)
+    assert bad_i not in rows and bad_j not in cols
+    worst, worst_bad = 0.0, 0.0
+    for v in range(n // bs):                       # C X panel by panel (C copied to the host)
+        j0 = v * bs
+        Cp = C[j0:j0 + bs].cpu().numpy()
+        r = oracle.qgemv("N", n, bs, Cp, ref["x"][j0:j0 + bs]) - ref["AY"][v]
+        worst = max(worst, float(qnorm(r).max()))
+        if j0 <= bad_j < j0 + bs:
+            Cp[bad_j - j0, bad_i, 0] += 10 * tol
+            rb = oracle.qgemv("N", n, bs, Cp, ref["x"][j0:j0 + bs]) - ref["AY"][v]
+            worst_bad = float(qnorm(rb).max())
+    assert worst <= bound, (worst, bound, tol)
+    assert worst_bad > bound, (worst_bad, bound, tol)
+    del C
     _free()

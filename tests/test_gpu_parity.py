@@ -224,30 +224,53 @@ def test_b_is_a_hermitian_rank_k_shape(path):
 @pytest.mark.parametrize("precision", ["f64", "f32"])
 def test_c3_full_size_sampled_and_freivalds(precision):
     """c3 (8192^3, N/H, alpha = beta = 1, N(0,1)) in the bench's launch
-    configuration: 2 full rows + 2 full columns + 256 random entries from the
-    oracle one by one, plus a Freivalds check of the whole C."""
+    configuration:
+      * 16 full rows (every 512th row) and 2 full columns of C from the oracle,
+        entry by entry within the per-entry tolerance;
+      * a block Freivalds check of the WHOLE C (tests/freivalds.py: right vectors
+        supported on column blocks of 64 (FP64) / 16 (FP32) columns), passing
+        below a bound calibrated on the 16 known rows (20 x the correct-C
+        residual), which must itself be < 5 x tol so that any single entry off
+        by 10 x tol is caught;
+      * negative control: the same check on C with ONE unsampled entry moved by
+        10 x tol must fail."""
+    from tests.freivalds import Check, columns_of, draw_x, qnorm, times_x
+    from tests.gpu_helpers import tol_for
     cfg = CONFIGS["c3"]
     n = cfg["M"]
     pr = make_problem(n, n, n, "N", "H", cfg["alpha"], cfg["beta"], seed=0, dist="normal")
-    got = run_gpu(pr, precision)
-    rng = np.random.default_rng(42)
-    rows = np.concatenate([np.full(n, 17), np.full(n, n - 1), np.arange(n), np.arange(n),
-                           rng.integers(0, n, 256)])
-    cols = np.concatenate([np.arange(n), np.arange(n), np.full(n, 5), np.full(n, n - 2),
-                           rng.integers(0, n, 256)])
-    ref = oracle.qgemm_entries("N", "H", n, n, n, pr.alpha, pr.A, pr.B, pr.beta, pr.C, rows, cols)
-    from tests.gpu_helpers import tol_for
+    got = run_gpu(pr, precision)                      # (n, n, 4): columns of C
     tol = tol_for(pr, precision)
-    err = np.abs(got[cols, rows, :] - ref).max()
-    assert err <= tol, (err, tol)
-    # Freivalds: C x == alpha op(A) (op(B) x) + beta C0 x, x multiplied on the right
-    x = np.random.default_rng(7).standard_normal((n, 4))
-    lhs = oracle.qgemv("N", n, n, np.ascontiguousarray(got), x)
-    y = oracle.qgemv("H", n, n, pr.B, x)
-    rhs = oracle.qgemv("N", n, n, pr.A, y) + oracle.qgemv("N", n, n, pr.C, x)
-    # each entry of C x sums n products of an entry error (<= tol) and |x|
-    bound = tol * np.abs(x).sum() * 4
-    assert np.abs(lhs - rhs).max() <= bound
+    rows = np.arange(0, n, 512) + 17                  # 16 full rows
+    A_S = np.ascontiguousarray(pr.A[:, rows, :])      # op(A) rows S (stored (K, |S|, 4))
+    ref_rows = np.ascontiguousarray(pr.C[:, rows, :])
+    oracle.qgemm("N", "H", rows.size, n, n, pr.alpha, A_S, pr.B, pr.beta, ref_rows)
+    got_rows = np.ascontiguousarray(got[:, rows, :])
+    err_rows = float(np.abs(got_rows - ref_rows).max())
+    assert err_rows <= tol, (err_rows, tol)
+    cols = np.array([5, n - 2])
+    ref_cols = np.ascontiguousarray(pr.C[cols])
+    B_cols = np.ascontiguousarray(pr.B[:, cols, :])   # op(B) = B^H: columns = rows of stored B
+    oracle.qgemm("N", "H", n, cols.size, n, pr.alpha, pr.A, B_cols, pr.beta, ref_cols)
+    err_cols = float(np.abs(got[cols] - ref_cols).max())
+    assert err_cols <= tol, (err_cols, tol)
+    # block Freivalds over the whole C
+    bs = 64 if precision == "f64" else 16
+    x = draw_x(n, seed=7)
+    Y = times_x(lambda j0, j1: (pr.B[:, j0:j1, :], "H"), n, n, x, bs)   # op(B) X: (nb, K, 4)
+    AY = np.zeros((Y.shape[0], n, 4))
+    oracle.qgemm("N", "N", n, Y.shape[0], n, 1, pr.A, Y, 0, AY)
+    C0X = times_x(columns_of(pr.C), n, n, x, bs)
+    chk = Check(n, n, bs, x, AY + C0X)                # alpha = beta = 1
+    bound = chk.bound(ref_rows, got_rows, rows)
+    assert bound < 5 * tol, (bound, tol)              # power: 10 x tol on one entry is visible
+    res = float(qnorm(chk.residual(columns_of(got))).max())
+    assert res <= bound, (res, bound, tol)
+    # negative control: one entry (row not sampled, column not sampled) moved by 10 tol
+    bad = got.copy()
+    bad[4321, 2345, 0] += 10 * tol
+    res_bad = float(qnorm(chk.residual(columns_of(bad))).max())
+    assert res_bad > bound, (res_bad, bound, tol)
 
 
 # ---------------------------------------------------------------- small-problem path
