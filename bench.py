@@ -661,9 +661,9 @@ def measure_c5_weak(ctx, m_loc, n, warmup, steps, check):
            "steps": steps, "n_gpus": world,
            "per_gpu_tflops": fl / world * steps / (ms / 1e3) / 1e12,
            "mainloop_ms_per_step_rank0": main_ms / max(1, steps),
-           "timed": "NCCL broadcast(B) + local qgemm" + (
+           "timed": ("NCCL broadcast(B) + local qgemm" + (
                " with epilogue stores into root's C over peer memory + completion all_reduce"
-               if peer is not None else " + NCCL gather of C" if world > 1 else ""),
+               if peer is not None else " + NCCL gather of C")) if world > 1 else "qgemm",
            "launches_per_step": launches / max(1, steps)}
     del B
     torch.cuda.empty_cache()
@@ -721,7 +721,8 @@ def measure_c4_sharded(ctx, n, K, warmup, steps, check):
                        f"A_r a strided view, lda = {n}), C Hermitian-initialised, over {world} GPU(s)",
            "value": fl * steps / (ms / 1e3) / 1e12, "unit": "TFLOP/s", "ms_per_step": ms / steps,
            "steps": steps, "n_gpus": world,
-           "timed": "NCCL broadcast(A) + local qgemm per step (gather timed separately)",
+           "timed": "NCCL broadcast(A) + local qgemm per step (gather timed separately)"
+                    if world > 1 else "qgemm",
            "launches_per_step": launches / max(1, steps)}
     # collection: gather of every row block into root's column-major C (once, timed)
     C_full = None

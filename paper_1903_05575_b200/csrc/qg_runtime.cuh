@@ -691,6 +691,20 @@ int num_sms() {
 #define QG_SMALL_CTAS_PER_SM (16 / QG_SMALL_WARPS)  // resident at <= 128 registers
 #endif
 
+#ifndef QG_SMALL_PDL
+#define QG_SMALL_PDL 1
+#endif
+// Programmatic dependent launch for the one-launch small kernel: default
+// QG_SMALL_PDL, overridable at run time with the environment variable
+// QG_SMALL_PDL=0/1 (read once; for A/B measurements).
+bool small_pdl() {
+  static const int v = [] {
+    const char *e = std::getenv("QG_SMALL_PDL");
+    return e ? (e[0] != '0') : QG_SMALL_PDL;
+  }();
+  return v != 0;
+}
+
 template <typename T>
 int launch_small(const T *A, int64_t lda, int a_rc, int a_cj, const T *B, int64_t ldb, int b_rc, int b_cj, T *C,
                  int64_t ldc, int64_t M, int64_t N, int64_t K, const T *alpha, const T *beta, cudaStream_t st) {
@@ -727,22 +741,28 @@ int launch_small(const T *A, int64_t lda, int a_rc, int a_cj, const T *B, int64_
   if (blocks * Z > INT32_MAX) return int(cudaErrorInvalidConfiguration);
   cudaError_t e = cudaSuccess;
   { int ti = tstart(kSmall, st);
-  if (Z == 1) {
-    qg::qgemm_small_kernel<T, false><<<unsigned(blocks), qg::kSmallThreads, 0, st>>>(a);
-  } else {
-    cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3(unsigned(blocks * Z));
-    cfg.blockDim = dim3(qg::kSmallThreads);
-    cfg.stream = st;
-    cudaLaunchAttribute attr[1];
-    attr[0].id = cudaLaunchAttributeClusterDimension;
-    attr[0].val.clusterDim.x = unsigned(Z);
-    attr[0].val.clusterDim.y = 1;
-    attr[0].val.clusterDim.z = 1;
-    cfg.attrs = attr;
-    cfg.numAttrs = 1;
-    e = cudaLaunchKernelEx(&cfg, qg::qgemm_small_kernel<T, true>, a);
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(unsigned(blocks * Z));
+  cfg.blockDim = dim3(qg::kSmallThreads);
+  cfg.stream = st;
+  cudaLaunchAttribute attr[2];
+  int na = 0;
+  if (Z > 1) {
+    attr[na].id = cudaLaunchAttributeClusterDimension;
+    attr[na].val.clusterDim.x = unsigned(Z);
+    attr[na].val.clusterDim.y = 1;
+    attr[na].val.clusterDim.z = 1;
+    ++na;
   }
+  if (small_pdl()) {  // programmatic dependent launch (qg_small.cuh griddepcontrol)
+    attr[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[na].val.programmaticStreamSerializationAllowed = 1;
+    ++na;
+  }
+  cfg.attrs = attr;
+  cfg.numAttrs = unsigned(na);
+  e = Z == 1 ? cudaLaunchKernelEx(&cfg, qg::qgemm_small_kernel<T, false>, a)
+             : cudaLaunchKernelEx(&cfg, qg::qgemm_small_kernel<T, true>, a);
   tstop(ti, st); }
   if (e != cudaSuccess) return int(e);
   ++g_last_launches;

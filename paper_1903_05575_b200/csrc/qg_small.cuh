@@ -131,6 +131,13 @@ __global__ void __launch_bounds__(kSmallThreads, 512 / kSmallThreads) qgemm_smal
   const T *A = static_cast<const T *>(a.A);
   const T *B = static_cast<const T *>(a.B);
   T *C = static_cast<T *>(a.C);
+  // Programmatic dependent launch (host: QG_SMALL_PDL): let the next kernel of
+  // the stream start launching now, so its CTA dispatch and prologue overlap
+  // this grid; and wait for the previous kernel's completion (and memory) only
+  // here, right before the first global access.  Without the launch attribute
+  // both are no-ops.
+  asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
+  asm volatile("griddepcontrol.wait;\n" ::: "memory");
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int S = a.S, tiles_per_cta = kSmallWarps / S, Z = kZ ? a.Z : 1;
   const int tile = warp / S, part = warp % S;

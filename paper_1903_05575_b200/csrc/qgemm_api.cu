@@ -10,6 +10,7 @@
 #include <atomic>
 #include <climits>
 #include <cstdint>
+#include <cstdlib>
 #include <cstring>
 #include <vector>
 #include <cuda_runtime.h>

@@ -46,6 +46,8 @@ def leading_dim(t: torch.Tensor, name: str = "X") -> int:
     rejected: the kernels address element (i, j) at base + 4 (i + j ld)."""
     if t.dim() != 3 or t.shape[2] != 4:
         raise ValueError(f"{name}: expected an (ncols, rows, 4) tensor")
+    if t.numel() == 0:  # nothing is addressed (strides of empty tensors are arbitrary)
+        return max(1, t.shape[1])
     if t.stride(2) != 1 or (t.shape[1] > 1 and t.stride(1) != 4):
         raise ValueError(f"{name}: components and rows must be contiguous (strides (4 ld, 4, 1))")
     if t.shape[0] <= 1:

@@ -87,9 +87,17 @@ class Check:
         cx = times_x(columns_of(C_rows_st), len(rows), self.n, self.x, self.bs)
         return cx - self.rhs[:, rows, :]
 
-    def bound(self, ref_rows_st: np.ndarray, got_rows_st: np.ndarray, rows: np.ndarray) -> float:
-        """CAL_FACTOR x the largest residual norm on the sampled rows, of the
+    def bound(self, ref_rows_st: np.ndarray, got_rows_st: np.ndarray, rows: np.ndarray,
+              factor: float = CAL_FACTOR) -> float:
+        """`factor` x the largest residual norm on the sampled rows, of the
         oracle's C (the correct-C residual) and of the GPU's verified rows."""
         noise = max(float(qnorm(self.residual_rows(ref_rows_st, rows)).max()),
                     float(qnorm(self.residual_rows(got_rows_st, rows)).max()))
-        return CAL_FACTOR * noise
+        return factor * noise
+
+
+def detects(bound: float, tol: float, factor: float) -> bool:
+    """Power of the check: an entry off by 10 tol moves its residual by >= 10 tol
+    (|x_j| >= 1); the other bs - 1 terms of that residual add at most the noise
+    level ~ bound / factor, so the entry is caught if 10 tol - bound/factor > bound."""
+    return bound * (1.0 + 1.0 / factor) < 10.0 * tol

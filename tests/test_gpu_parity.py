@@ -228,13 +228,16 @@ def test_c3_full_size_sampled_and_freivalds(precision):
       * 16 full rows (every 512th row) and 2 full columns of C from the oracle,
         entry by entry within the per-entry tolerance;
       * a block Freivalds check of the WHOLE C (tests/freivalds.py: right vectors
-        supported on column blocks of 64 (FP64) / 16 (FP32) columns), passing
-        below a bound calibrated on the 16 known rows (20 x the correct-C
-        residual), which must itself be < 5 x tol so that any single entry off
-        by 10 x tol is caught;
+        supported on column blocks of 64 (FP64) / 4 (FP32) columns), passing
+        below a bound calibrated on the 16 known rows (20 x (FP64) / 3 x (FP32)
+        the largest residual there), which must itself be small enough that any
+        single entry off by 10 x tol is caught (freivalds.detects).  FP32: the
+        tcgen05 accumulation (truncating FP32 adds over ~12k MMA steps per output)
+        leaves per-entry errors of a few percent of tol, so its blocks are short
+        and its factor small;
       * negative control: the same check on C with ONE unsampled entry moved by
         10 x tol must fail."""
-    from tests.freivalds import Check, columns_of, draw_x, qnorm, times_x
+    from tests.freivalds import Check, columns_of, detects, draw_x, qnorm, times_x
     from tests.gpu_helpers import tol_for
     cfg = CONFIGS["c3"]
     n = cfg["M"]
@@ -255,15 +258,15 @@ def test_c3_full_size_sampled_and_freivalds(precision):
     err_cols = float(np.abs(got[cols] - ref_cols).max())
     assert err_cols <= tol, (err_cols, tol)
     # block Freivalds over the whole C
-    bs = 64 if precision == "f64" else 16
+    bs, factor = (64, 20.0) if precision == "f64" else (4, 3.0)
     x = draw_x(n, seed=7)
     Y = times_x(lambda j0, j1: (pr.B[:, j0:j1, :], "H"), n, n, x, bs)   # op(B) X: (nb, K, 4)
     AY = np.zeros((Y.shape[0], n, 4))
     oracle.qgemm("N", "N", n, Y.shape[0], n, 1, pr.A, Y, 0, AY)
     C0X = times_x(columns_of(pr.C), n, n, x, bs)
     chk = Check(n, n, bs, x, AY + C0X)                # alpha = beta = 1
-    bound = chk.bound(ref_rows, got_rows, rows)
-    assert bound < 5 * tol, (bound, tol)              # power: 10 x tol on one entry is visible
+    bound = chk.bound(ref_rows, got_rows, rows, factor)
+    assert detects(bound, tol, factor), (bound, tol)  # power: 10 x tol on one entry is visible
     res = float(qnorm(chk.residual(columns_of(got))).max())
     assert res <= bound, (res, bound, tol)
     # negative control: one entry (row not sampled, column not sampled) moved by 10 tol
