@@ -50,7 +50,9 @@
  *           beta=11 C=12 ldc=13 workspace=14 workspace_bytes=15 stream=16;
  *         a C extent overlapping the A or B extent returns -12;
  *         NULL A/B are accepted only when they are not read (K == 0 or alpha == 0);
- *         pointers not aligned to their scalar type return -7/-9/-12/-14.
+ *         A, B and C must be 16-byte aligned (every kernel moves whole
+ *         quaternions with 16-byte vector accesses): otherwise -7/-9/-12;
+ *         the workspace must be 256-byte aligned: otherwise -14.
  *    >0   a cudaError_t raised while enqueueing.
  * Nothing is enqueued when the return value is non-zero.
  *
@@ -217,7 +219,9 @@ int qgemm_pack_panel(char trans, int operand, int64_t R, int64_t K, const double
  * only; FP32 calls take the packed path), 4 = direct restricted to the
  * 32-byte-swizzle tile feed (3 and auto load both operands as conflict-free
  * 4-quaternion-group tiles when the groups are whole: M, resp. N, a multiple
- * of 4 for op(A) = A, resp. op(B) = B^T / B^H, else K).  Auto = small kernel below the
+ * of 4 for op(A) = A, resp. op(B) = B^T / B^H, else K), 5 = as 2 but never the
+ * tile-exact variant of the small kernel (taken when M % 8 == N % 8 == K % 4
+ * == 0 and, for FP64, A, B, C are 32-byte aligned).  Auto = small kernel below the
  * crossover; above it FP64 takes the direct path whenever the group tiles
  * apply (op(A) = A: M % 4 == 0 and N % 4 (op(B) = B^T/B^H) resp. K % 4 == 0),
  * when op(A) is T/H, and otherwise up to M*N*K <= 2^37; else packed; FP32

@@ -25,6 +25,7 @@ from .qgemm import (  # noqa: F401
     PATH_SMALL,
     PATH_DIRECT,
     PATH_DIRECT32,
+    PATH_SMALL_GENERAL,
     timing_collect,
     timing_enable,
     version,

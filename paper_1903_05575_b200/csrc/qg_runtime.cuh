@@ -14,7 +14,8 @@ thread_local int g_last_launches = 0;
 // the persistent mainloop fed by TMA from the interleaved storage, no pack) or
 // the one-launch small kernel.  0 = auto, 1 = always packed, 2 = small kernel
 // whenever the call reads A and B, 3 = direct for FP64 (packed for FP32), 4 =
-// direct with the 32-byte-swizzle tiles only (never kFeedTma128) --
+// direct with the 32-byte-swizzle tiles only (never kFeedTma128), 5 = small
+// kernel, general variant only (never the tile-exact one) --
 // qgemm_set_path_policy; the tests run every shape under each.
 std::atomic<int> g_path_policy{0};
 
@@ -655,7 +656,7 @@ template <typename T>
 bool use_small(int64_t M, int64_t N, int64_t K) {
   const int pol = g_path_policy.load(std::memory_order_relaxed);
   if (pol == 1 || pol == 3 || pol == 4) return false;
-  if (pol == 2) return true;
+  if (pol == 2 || pol == 5) return true;
   constexpr int64_t kCap = int64_t(1) << 28;
   if (M > kCap || N > kCap || K > kCap) return false;  // keeps M*N*K from overflowing below
   const double macs = double(M) * double(N) * double(K);
@@ -697,12 +698,34 @@ int num_sms() {
 // Programmatic dependent launch for the one-launch small kernel: default
 // QG_SMALL_PDL, overridable at run time with the environment variable
 // QG_SMALL_PDL=0/1 (read once; for A/B measurements).
-bool small_pdl() {
+// 0: plain launches; 1: PDL, the next kernel may launch at this one's entry;
+// 2: PDL, triggered after each CTA's stores (tiny kernel; the general small
+// kernel triggers at entry for 1 and 2).
+int small_pdl() {
   static const int v = [] {
     const char *e = std::getenv("QG_SMALL_PDL");
-    return e ? (e[0] != '0') : QG_SMALL_PDL;
+    return e ? std::atoi(e) : QG_SMALL_PDL;
   }();
-  return v != 0;
+  return v;
+}
+
+template <typename T>
+using SmallKernel = void (*)(qg::SmallArgs);
+// Tile-exact small kernel for this op pair (qg_small.cuh qgemm_tiny_kernel).
+template <typename T>
+SmallKernel<T> tiny_kernel(int ops) {
+  switch (ops) {
+    case 0: return qg::qgemm_tiny_kernel<T, 0>;
+    case 1: return qg::qgemm_tiny_kernel<T, 1>;
+    case 2: return qg::qgemm_tiny_kernel<T, 2>;
+    case 4: return qg::qgemm_tiny_kernel<T, 4>;
+    case 5: return qg::qgemm_tiny_kernel<T, 5>;
+    case 6: return qg::qgemm_tiny_kernel<T, 6>;
+    case 12: return qg::qgemm_tiny_kernel<T, 12>;
+    case 13: return qg::qgemm_tiny_kernel<T, 13>;
+    case 14: return qg::qgemm_tiny_kernel<T, 14>;
+    default: return nullptr;
+  }
 }
 
 template <typename T>
@@ -739,10 +762,21 @@ int launch_small(const T *A, int64_t lda, int a_rc, int a_cj, const T *B, int64_
       Z *= 2;
   a.Z = Z;
   if (blocks * Z > INT32_MAX) return int(cudaErrorInvalidConfiguration);
+  // tile-exact shapes (every 8x8 fragment and k4 step in range) take the
+  // specialised kernel; FP64 moves whole quaternions as 256-bit accesses there,
+  // which needs 32-byte aligned bases (FP32: the ABI's 16 bytes suffice)
+  auto aligned = [](const void *p) { return (reinterpret_cast<uintptr_t>(p) & (sizeof(T) == 8 ? 31u : 15u)) == 0; };
+  const bool tiny = Z == 1 && M % 8 == 0 && N % 8 == 0 && K % 4 == 0 && tn <= 65535 && aligned(A) &&
+                    aligned(B) && aligned(C) &&
+                    g_path_policy.load(std::memory_order_relaxed) != 5;
+  const int pdl = small_pdl();
+  a.pdl_trigger = pdl;
+  a.per = cdiv(steps, S);
   cudaError_t e = cudaSuccess;
   { int ti = tstart(kSmall, st);
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(unsigned(blocks * Z));
+  if (tiny) cfg.gridDim = dim3(unsigned(a.m_blocks), unsigned(tn));
   cfg.blockDim = dim3(qg::kSmallThreads);
   cfg.stream = st;
   cudaLaunchAttribute attr[2];
@@ -754,15 +788,18 @@ int launch_small(const T *A, int64_t lda, int a_rc, int a_cj, const T *B, int64_
     attr[na].val.clusterDim.z = 1;
     ++na;
   }
-  if (small_pdl()) {  // programmatic dependent launch (qg_small.cuh griddepcontrol)
+  if (pdl) {  // programmatic dependent launch (qg_small.cuh griddepcontrol)
     attr[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
     attr[na].val.programmaticStreamSerializationAllowed = 1;
     ++na;
   }
   cfg.attrs = attr;
   cfg.numAttrs = unsigned(na);
-  e = Z == 1 ? cudaLaunchKernelEx(&cfg, qg::qgemm_small_kernel<T, false>, a)
-             : cudaLaunchKernelEx(&cfg, qg::qgemm_small_kernel<T, true>, a);
+  if (tiny)
+    e = cudaLaunchKernelEx(&cfg, tiny_kernel<T>(a_rc | (a_cj << 1) | (b_rc << 2) | (b_cj << 3)), a);
+  else
+    e = Z == 1 ? cudaLaunchKernelEx(&cfg, qg::qgemm_small_kernel<T, false>, a)
+               : cudaLaunchKernelEx(&cfg, qg::qgemm_small_kernel<T, true>, a);
   tstop(ti, st); }
   if (e != cudaSuccess) return int(e);
   ++g_last_launches;

@@ -46,6 +46,9 @@ struct SmallArgs {
   int Z;                       // CTAs per 8x8 tile splitting K (a thread-block cluster; S == W when > 1)
   int64_t m_blocks;            // CTAs along M (1-D grid: m fastest)
   Scalars<double> sc;
+  int pdl_trigger;             // tiny kernel, launched with PDL: 1 = let the next kernel launch at
+                               // entry, 2 = after this CTA's stores (0: no PDL attribute)
+  int64_t per;                 // tiny kernel: k4 steps per warp (ceil(K / 4 / S))
 };
 
 template <typename T>
@@ -258,6 +261,166 @@ __global__ void __launch_bounds__(kSmallThreads, 512 / kSmallThreads) qgemm_smal
     T o[4] = {T(out[0]), T(out[1]), T(out[2]), T(out[3])};
     stq(cp, o);
   }
+}
+
+// ---------------------------------------------------------------------------
+// Tile-exact variant (host: M % 8 == N % 8 == K % 4 == 0, no cluster split;
+// c1 and every power-of-two small shape): the same work split and arithmetic as
+// qgemm_small_kernel, with everything the general kernel decides per element
+// moved to compile time or out of the loop -- the op pair (rows-contiguous /
+// conj flags, kOps) is a template parameter, so op H is a sign in the product
+// table (eps(p,s) sigma_A(p) sigma_B(s)) instead of a fix-up per loaded
+// component; no range checks (every fragment is in range); each operand walks
+// one pointer with a fixed per-k4-step stride; FP64 quaternions move as one
+// 256-bit access (LDG/STG.E.ENL2.256; 32-byte aligned A, B, C).  ncu at c1 on
+// the general kernel: 810 issued instructions per warp for 64 DMMAs, ~6.6
+// cycles per issue (fixed-latency "wait" and short-scoreboard stalls) -- the
+// instruction stream, not the DMMA pipe, set the time.
+// kOps: bit 0 op(A) rows contiguous (A = N), bit 1 conj A (H), bit 2 op(B) rows
+// contiguous (B = T/H), bit 3 conj B (H).
+__device__ __forceinline__ void ld_quat_wide(const double *p, double (&q)[4]) {
+  asm volatile("ld.global.nc.v4.f64 {%0, %1, %2, %3}, [%4];\n"
+               : "=d"(q[0]), "=d"(q[1]), "=d"(q[2]), "=d"(q[3])
+               : "l"(p));
+}
+__device__ __forceinline__ void ld_quat_wide(const float *p, double (&q)[4]) {
+  float t[4];
+  asm volatile("ld.global.nc.v4.f32 {%0, %1, %2, %3}, [%4];\n"
+               : "=f"(t[0]), "=f"(t[1]), "=f"(t[2]), "=f"(t[3])
+               : "l"(p));
+#pragma unroll
+  for (int c = 0; c < 4; ++c) q[c] = double(t[c]);
+}
+__device__ __forceinline__ void ld_c_wide(const double *p, double (&q)[4]) {
+  asm volatile("ld.global.v4.f64 {%0, %1, %2, %3}, [%4];\n"
+               : "=d"(q[0]), "=d"(q[1]), "=d"(q[2]), "=d"(q[3])
+               : "l"(p)
+               : "memory");
+}
+__device__ __forceinline__ void ld_c_wide(const float *p, double (&q)[4]) {
+  float t[4];
+  ldq_c(p, t);
+#pragma unroll
+  for (int c = 0; c < 4; ++c) q[c] = double(t[c]);
+}
+__device__ __forceinline__ void st_c_wide(double *p, const double (&q)[4]) {
+  asm volatile("st.global.v4.f64 [%0], {%1, %2, %3, %4};\n" ::"l"(p), "d"(q[0]), "d"(q[1]), "d"(q[2]), "d"(q[3])
+               : "memory");
+}
+__device__ __forceinline__ void st_c_wide(float *p, const double (&q)[4]) {
+  const float t[4] = {float(q[0]), float(q[1]), float(q[2]), float(q[3])};
+  stq(p, t);
+}
+
+// One k4 step with the conj signs folded in: acc^{p^s} += eps(p,s) sa(p) sb(s) A^p B^s.
+template <bool CA, bool CB>
+__device__ __forceinline__ void tiny_step(double (&acc)[4][2], const double (&qa)[4], const double (&qb)[4]) {
+  double nb[4];
+#pragma unroll
+  for (int s = 0; s < 4; ++s) nb[s] = -qb[s];
+#pragma unroll
+  for (int p = 0; p < 4; ++p)
+#pragma unroll
+    for (int s = 0; s < 4; ++s) {
+      const bool neg = hneg(p, s) ^ (CA && p != 0) ^ (CB && s != 0);
+      dmma_8x8x4(acc[p ^ s], qa[p], neg ? nb[s] : qb[s]);
+    }
+}
+
+template <typename T, int kOps>
+__global__ void __launch_bounds__(kSmallThreads, 512 / kSmallThreads) qgemm_tiny_kernel(SmallArgs a) {
+  constexpr bool a_rc = kOps & 1, a_cj = (kOps >> 1) & 1, b_rc = (kOps >> 2) & 1, b_cj = (kOps >> 3) & 1;
+  __shared__ double red[kSmallThreads / 32][32][8];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  // grid (m blocks, n tiles); S a power of two (host), so no divisions here
+  const int S = a.S, lgS = __ffs(S) - 1;
+  const int tile = warp >> lgS, part = warp & (S - 1);
+  const int64_t m0 = (int64_t(blockIdx.x) * (kSmallWarps >> lgS) + tile) * 8;
+  const int64_t n0 = int64_t(blockIdx.y) * 8;
+  const int lr = lane >> 2, lk = lane & 3;
+  const int64_t steps_all = a.K >> 2;
+  // (the last CTA row may hold tiles past M: no loads, no stores, but they take
+  // part in the reduction barrier)
+  const bool live = m0 < a.M;
+  const int64_t s0 = live ? min(steps_all, int64_t(part) * a.per) : 0;
+  const int64_t s1 = live ? min(steps_all, s0 + a.per) : 0;
+  const T *A = static_cast<const T *>(a.A);
+  const T *B = static_cast<const T *>(a.B);
+  T *C = static_cast<T *>(a.C);
+  // this lane's quaternion of op(A) (row m0 + lr) / op(B) (column n0 + lr) at k = 4 s0 + lk,
+  // and the step to the next k4 step
+  const int64_t ka = 4 * s0 + lk;
+  const T *pa = a_rc ? A + 4 * ((m0 + lr) + ka * a.lda) : A + 4 * (ka + (m0 + lr) * a.lda);
+  const T *pb = b_rc ? B + 4 * ((n0 + lr) + ka * a.ldb) : B + 4 * (ka + (n0 + lr) * a.ldb);
+  const int64_t da = a_rc ? 16 * a.lda : 16, db = b_rc ? 16 * a.ldb : 16;
+  T *cp0 = C + 4 * ((m0 + lr) + (n0 + 2 * lk) * a.ldc);
+  // PDL (host QG_SMALL_PDL): the previous kernel's results are visible from here
+  if (a.pdl_trigger == 1) asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
+  asm volatile("griddepcontrol.wait;\n" ::: "memory");
+  if (part == 0 && live && !a.sc.beta_zero) {
+    asm volatile("prefetch.global.L1 [%0];" ::"l"(cp0));
+    asm volatile("prefetch.global.L1 [%0];" ::"l"(cp0 + 4 * a.ldc));
+  }
+
+  double acc[4][2];
+#pragma unroll
+  for (int c = 0; c < 4; ++c) acc[c][0] = acc[c][1] = 0.0;
+  int64_t st = s0;
+  for (; st + kSmallUnroll <= s1; st += kSmallUnroll) {  // loads of 4 steps in flight
+    double qa[kSmallUnroll][4], qb[kSmallUnroll][4];
+#pragma unroll
+    for (int u = 0; u < kSmallUnroll; ++u) {
+      ld_quat_wide(pa + u * da, qa[u]);
+      ld_quat_wide(pb + u * db, qb[u]);
+    }
+#pragma unroll
+    for (int u = 0; u < kSmallUnroll; ++u) tiny_step<a_cj, b_cj>(acc, qa[u], qb[u]);
+    pa += kSmallUnroll * da;
+    pb += kSmallUnroll * db;
+  }
+  for (; st < s1; ++st) {
+    double qa[4], qb[4];
+    ld_quat_wide(pa, qa);
+    ld_quat_wide(pb, qb);
+    tiny_step<a_cj, b_cj>(acc, qa, qb);
+    pa += da;
+    pb += db;
+  }
+
+  if (S > 1) {  // fixed-order reduction of the S partial tiles (deterministic)
+    if (part != 0) {
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        red[warp][lane][2 * c] = acc[c][0];
+        red[warp][lane][2 * c + 1] = acc[c][1];
+      }
+    }
+    __syncthreads();
+    if (part != 0) return;
+    for (int w = 1; w < S; ++w)
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        acc[c][0] += red[warp + w][lane][2 * c];
+        acc[c][1] += red[warp + w][lane][2 * c + 1];
+      }
+  }
+  if (!live) return;
+#pragma unroll
+  for (int i = 0; i < 2; ++i) {
+    T *cp = cp0 + i * 4 * a.ldc;
+    const double t[4] = {acc[0][i], acc[1][i], acc[2][i], acc[3][i]};
+    double out[4];
+    left_scale(a.sc.alpha, a.sc.alpha_real, t, out);
+    if (!a.sc.beta_zero) {
+      double c0[4], bc[4];
+      ld_c_wide(cp, c0);
+      left_scale(a.sc.beta, a.sc.beta_real, c0, bc);
+#pragma unroll
+      for (int k = 0; k < 4; ++k) out[k] += bc[k];
+    }
+    st_c_wide(cp, out);
+  }
+  if (a.pdl_trigger == 2) asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
 }
 
 }  // namespace qg

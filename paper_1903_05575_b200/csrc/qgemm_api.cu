@@ -280,7 +280,7 @@ size_t qgemm_host_workspace_bytes(char transA, char transB, int64_t M, int64_t N
 int qgemm_last_launch_count(void) { return g_last_launches; }
 
 int qgemm_set_path_policy(int policy) {
-  if (policy < 0 || policy > 4) return -1;
+  if (policy < 0 || policy > 5) return -1;
   return g_path_policy.exchange(policy);
 }
 

@@ -296,7 +296,7 @@ def qherk(uplo: str, trans: str, alpha: float, A: torch.Tensor, beta: float, C: 
 
 KINDS = ("pack", "mainloop", "scale", "naive", "small")
 
-PATH_AUTO, PATH_PACKED, PATH_SMALL, PATH_DIRECT, PATH_DIRECT32 = 0, 1, 2, 3, 4
+PATH_AUTO, PATH_PACKED, PATH_SMALL, PATH_DIRECT, PATH_DIRECT32, PATH_SMALL_GENERAL = 0, 1, 2, 3, 4, 5
 
 
 def set_path_policy(policy: int) -> int:
@@ -304,7 +304,8 @@ def set_path_policy(policy: int) -> int:
     small kernel, 3 direct (FP64: persistent mainloop fed by TMA straight from
     the interleaved storage, no pack; FP32 packed), 4 direct with the 32-byte-
     swizzle tile feed only (3 and auto load the operands as 4-quaternion groups
-    where M / N / K allow); returns the old one."""
+    where M / N / K allow), 5 as 2 but never the tile-exact small kernel;
+    returns the old one."""
     old = int(load().qgemm_set_path_policy(int(policy)))
     if old < 0:
         raise ValueError(f"invalid path policy {policy}")

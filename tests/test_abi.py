@@ -148,7 +148,7 @@ def test_workspace_sizes(lib):
 def test_path_policy_setter(lib):
     assert lib.qgemm_set_path_policy(2) == 1
     assert lib.qgemm_set_path_policy(7) == -1  # rejected, unchanged
-    assert lib.qgemm_set_path_policy(5) == -1
+    assert lib.qgemm_set_path_policy(6) == -1
     assert lib.qgemm_set_path_policy(4) == 2
     assert lib.qgemm_set_path_policy(3) == 4
     assert lib.qgemm_set_path_policy(0) == 3

@@ -19,12 +19,14 @@ pytestmark = pytest.mark.gpu
 OPS = [(a, b) for a in "NTH" for b in "NTH"]
 QALPHA = (0.3, -1.2, 0.7, 0.25)
 QBETA = (-0.5, 0.1, -0.9, 0.4)
-# pack launch + persistent mainloop | one-launch small kernel | TMA-fed mainloop (no pack):
-# 4-quaternion-group tiles where the extents allow (else 32-byte tiles) | 32-byte tiles only
-PATHS = [qg.PATH_PACKED, qg.PATH_SMALL, qg.PATH_DIRECT, qg.PATH_DIRECT32]
+# pack launch + persistent mainloop | one-launch small kernel (tile-exact variant where
+# the shape allows) | the small kernel's general variant only | TMA-fed mainloop (no
+# pack): 4-quaternion-group tiles where the extents allow (else 32-byte tiles) | 32-byte
+# tiles only
+PATHS = [qg.PATH_PACKED, qg.PATH_SMALL, qg.PATH_SMALL_GENERAL, qg.PATH_DIRECT, qg.PATH_DIRECT32]
 
 
-@pytest.fixture(params=PATHS, ids=["packed", "small", "direct", "direct32"])
+@pytest.fixture(params=PATHS, ids=["packed", "small", "small_general", "direct", "direct32"])
 def path(request):
     with path_policy(request.param):
         yield request.param
@@ -313,6 +315,42 @@ def test_small_kernel_cluster_split_exact(opA, opB):
     with path_policy(qg.PATH_SMALL):
         got = run_gpu(pr)
     assert_parity(pr, got, oracle_full(pr), exact=True)
+
+
+@pytest.mark.parametrize("opA,opB", OPS)
+@pytest.mark.parametrize("precision", ["f64", "f32"])
+@pytest.mark.parametrize("M,N,K", [(64, 64, 64), (8, 8, 4), (40, 24, 12), (128, 64, 256), (16, 8, 1024)])
+def test_tiny_kernel_exact_every_op_pair(opA, opB, precision, M, N, K):
+    """The tile-exact small kernel (M % 8 == N % 8 == K % 4 == 0: c1's shape and
+    its neighbours; op pair and conj signs compiled in, 256-bit quaternion
+    accesses): bitwise equal to the oracle with exact-integer inputs and
+    quaternion alpha/beta, for every op pair, in both storage precisions --
+    and bitwise equal to the general small kernel (policy 5) on the same call.
+    (40 x 24: the last CTA row holds tiles past M; 16 x 8 x 1024: K split over
+    the warps of a CTA.)"""
+    pr = make_problem(M, N, K, opA, opB, (2, -1, 0, 1), (1, 0, -1, 2), seed=M + N + K, dist="int2")
+    with path_policy(qg.PATH_SMALL):
+        got = run_gpu(pr, precision)
+        assert qg.last_launch_count() == 1
+    with path_policy(qg.PATH_SMALL_GENERAL):
+        gen = run_gpu(pr, precision)
+    assert_parity(pr, got, oracle_full(pr), exact=True)
+    np.testing.assert_array_equal(got, gen)
+
+
+def test_tiny_kernel_misaligned_base_takes_general_kernel():
+    """An FP64 operand 16 but not 32 bytes aligned cannot take the tile-exact
+    kernel's 256-bit accesses: the call falls back to the general small kernel
+    (same result, bitwise with exact-integer inputs)."""
+    pr = make_problem(64, 64, 64, "N", "N", 1, 0, seed=3, dist="int8")
+    A = torch.empty(pr.A.size + 2, dtype=torch.float64, device="cuda")[2:].view(pr.A.shape)
+    A.copy_(torch.from_numpy(pr.A))
+    assert A.data_ptr() % 32 == 16
+    B, C = to_dev(pr.B), to_dev(pr.C)
+    with path_policy(qg.PATH_SMALL):
+        qg.qgemm("N", "N", 1.0, A, B, 0.0, C)
+    torch.cuda.synchronize()
+    assert_parity(pr, C.cpu().numpy(), oracle_full(pr), exact=True)
 
 
 def test_concurrent_streams_do_not_share_workspace():
