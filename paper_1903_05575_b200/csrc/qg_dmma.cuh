@@ -124,6 +124,7 @@ struct alignas(64) DmmaArgs {
   CUtensorMap tmA, tmB;  // TMA feed: 3-D maps (component, view row, k) or (component, k, view row)
   CUtensorMap tmC;       // QG_C_RING: C as (component, column, row), box 4 x 64 x 16, 32-byte swizzle
   int c_ring;            // host: C tiles through the ring for this launch (see launch_dmma)
+  int c_remote;          // host: C is not in this GPU's memory (multi-GPU epilogue stores): no L2 prefetch of C
   const double *Ap;  // packed path: packed A panel, MT x KT chunks
   const double *Bp;  // packed path: packed B panel, NT x KT chunks
   // TMA feed: op(A) / op(B) read in place as R x K views -- X~(r, k) at
@@ -336,7 +337,7 @@ __device__ __forceinline__ void prefetch_c_tile(const DmmaArgs &a, int64_t mt, i
 }
 template <bool kRing>
 __device__ __forceinline__ void producer_unit_prefetch(Producer &p, const DmmaArgs &a, const Unit &u) {
-  p.c_pref_kt = (!(kRing && a.c_ring) && QG_C_PREFETCH_BULK && QG_C_PREFETCH_KT > 0 && u.kb == 0 &&
+  p.c_pref_kt = (!(kRing && a.c_ring) && !a.c_remote && QG_C_PREFETCH_BULK && QG_C_PREFETCH_KT > 0 && u.kb == 0 &&
                  !a.sc.beta_zero)
                     ? (u.ke - QG_C_PREFETCH_KT > u.kb ? u.ke - QG_C_PREFETCH_KT : u.kb)
                     : int64_t(-1);
@@ -588,7 +589,8 @@ __global__ void __launch_bounds__(kDmmaThreads, 1) qgemm_dmma_kernel(const __gri
         for (int c = 0; c < 4; ++c) acc[i][j][c][0] = acc[i][j][c][1] = 0.0;
 
     // k-tile at which to warm L2 with this unit's C tile (beta != 0, epilogue here)
-    const int64_t kt_prefetch = (!(kRing && args.c_ring) && !QG_C_PREFETCH_BULK && QG_C_PREFETCH_KT > 0 && u.kb == 0 &&
+    const int64_t kt_prefetch = (!(kRing && args.c_ring) && !args.c_remote && !QG_C_PREFETCH_BULK &&
+                                 QG_C_PREFETCH_KT > 0 && u.kb == 0 &&
                                  !args.sc.beta_zero)
                                     ? (u.ke - QG_C_PREFETCH_KT > u.kb ? u.ke - QG_C_PREFETCH_KT : u.kb)
                                     : int64_t(-1);

@@ -464,8 +464,12 @@ int launch_dmma(qg::DmmaArgs &a, DmmaKernel kernel, bool direct, void *sk_scratc
   // tile) the C boxes' TMA requests compete with the A/B stream (DMMA-active
   // 94.7% vs 96.0%, 250.1 vs 247.4 ms), while c2 / c3 / QHERK gain (DESIGN.md
   // §6).  The packed kernel never takes the ring: no pointer query, no map.
-  a.c_ring = direct && QG_C_RING && ((QG_RING_TRI && a.tri != 0) || a.KT >= QG_C_RING_MIN_KT) &&
-             c_is_local(a.C);
+  // (one pointer query per launch that reads C or may take the ring; C in
+  // another GPU's memory -- the multi-GPU driver's epilogue stores -- gets
+  // neither the ring nor the L2 prefetch of C tiles)
+  const bool query = (direct && QG_C_RING) || !a.sc.beta_zero;
+  a.c_remote = query ? !c_is_local(a.C) : 0;
+  a.c_ring = direct && QG_C_RING && ((QG_RING_TRI && a.tri != 0) || a.KT >= QG_C_RING_MIN_KT) && !a.c_remote;
   if (a.c_ring) {
     const int e = encode_c(&a.tmC, a.C, a.ldc, a.M, a.N);
     if (e) return e;
@@ -693,7 +697,7 @@ int num_sms() {
 #endif
 
 #ifndef QG_SMALL_PDL
-#define QG_SMALL_PDL 1
+#define QG_SMALL_PDL 2  // c1 2.81 -> 2.37 us back to back vs no PDL; 1 (trigger at entry) slowed 128^3
 #endif
 // Programmatic dependent launch for the one-launch small kernel: default
 // QG_SMALL_PDL, overridable at run time with the environment variable
@@ -772,12 +776,22 @@ int launch_small(const T *A, int64_t lda, int a_rc, int a_cj, const T *B, int64_
   const int pdl = small_pdl();
   a.pdl_trigger = pdl;
   a.per = cdiv(steps, S);
+  if (tiny) {
+    // the tile-exact kernel has kTinyWarps warps per CTA (2 per SM sub-partition:
+    // two warps' DMMA chains interleave): its own split, by the same rule
+    constexpr int WT = qg::kTinyWarps, per_sm = 16 / WT;
+    S = 1;
+    while (S < WT && cdiv(tm, WT / (2 * S)) * tn <= per_sm * sms && steps >= 2 * QG_SMALL_MIN_STEPS * S) S *= 2;
+    a.S = S;
+    a.m_blocks = cdiv(tm, WT / S);
+    a.per = cdiv(steps, S);
+  }
   cudaError_t e = cudaSuccess;
   { int ti = tstart(kSmall, st);
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(unsigned(blocks * Z));
   if (tiny) cfg.gridDim = dim3(unsigned(a.m_blocks), unsigned(tn));
-  cfg.blockDim = dim3(qg::kSmallThreads);
+  cfg.blockDim = dim3(tiny ? qg::kTinyThreads : qg::kSmallThreads);
   cfg.stream = st;
   cudaLaunchAttribute attr[2];
   int na = 0;

@@ -327,15 +327,20 @@ __device__ __forceinline__ void tiny_step(double (&acc)[4][2], const double (&qa
     }
 }
 
+#ifndef QG_TINY_WARPS
+#define QG_TINY_WARPS 8  // warps per CTA of the tile-exact kernel (two per SM sub-partition)
+#endif
+constexpr int kTinyWarps = QG_TINY_WARPS;
+constexpr int kTinyThreads = kTinyWarps * 32;
 template <typename T, int kOps>
-__global__ void __launch_bounds__(kSmallThreads, 512 / kSmallThreads) qgemm_tiny_kernel(SmallArgs a) {
+__global__ void __launch_bounds__(kTinyThreads, 512 / kTinyThreads) qgemm_tiny_kernel(SmallArgs a) {
   constexpr bool a_rc = kOps & 1, a_cj = (kOps >> 1) & 1, b_rc = (kOps >> 2) & 1, b_cj = (kOps >> 3) & 1;
-  __shared__ double red[kSmallThreads / 32][32][8];
+  __shared__ double red[kTinyWarps][32][8];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   // grid (m blocks, n tiles); S a power of two (host), so no divisions here
   const int S = a.S, lgS = __ffs(S) - 1;
   const int tile = warp >> lgS, part = warp & (S - 1);
-  const int64_t m0 = (int64_t(blockIdx.x) * (kSmallWarps >> lgS) + tile) * 8;
+  const int64_t m0 = (int64_t(blockIdx.x) * (kTinyWarps >> lgS) + tile) * 8;
   const int64_t n0 = int64_t(blockIdx.y) * 8;
   const int lr = lane >> 2, lk = lane & 3;
   const int64_t steps_all = a.K >> 2;
