@@ -163,6 +163,24 @@ size_t sk_reserve(int64_t M, int64_t N, int64_t ktiles) {
   return sk_slots_bytes<T>(M, N, ktiles) + align256(size_t(2 * qg::kMaxPersistentCTAs) * sizeof(int));
 }
 
+// Longest K-panel of one launch.  FP32 (tcgen05, FP32 accumulation in TMEM):
+// the tensor core's accumulator adds are truncating, so the error of one
+// launch grows like K^1.5 (each of ~12 K/8 accumulation steps errs by ~u |D|,
+// |D| ~ sqrt(K), with a bias that does not average out; measured
+// tools/f32_accuracy.py: max error / north-star tolerance 0.004 at K = 256,
+// 0.013 at 1024, 0.048 at 4096, 0.087 at 8192 -- the tolerance grows only like
+// sqrt(K)).  Panels of <= 8192 k add their results into C with round-to-nearest
+// FP32 (beta = 1 after the first panel), so beyond one panel the error grows
+// like sqrt(K) as the tolerance does.  FP64 (DMMA, exact FP64 accumulation):
+// no cap.
+#ifndef QG_F32_MAX_PANEL_K
+#define QG_F32_MAX_PANEL_K 8192
+#endif
+template <typename T>
+constexpr int64_t max_panel_kt() {
+  return sizeof(T) == 8 ? INT64_MAX : int64_t(QG_F32_MAX_PANEL_K) / qg::kTcBK;
+}
+
 template <typename T>
 size_t workspace_for(int64_t M, int64_t N, int64_t K, int64_t ktiles) {
   // the stream-K reserve is sized for the whole K (an upper bound for any panel),

@@ -328,12 +328,15 @@ __device__ __forceinline__ void tiny_step(double (&acc)[4][2], const double (&qa
 }
 
 #ifndef QG_TINY_WARPS
-#define QG_TINY_WARPS 8  // warps per CTA of the tile-exact kernel (two per SM sub-partition)
+#define QG_TINY_WARPS 4  // warps per CTA of the tile-exact kernel (c1: 2.37 us back to back vs 2.82 with 8)
+#endif
+#ifndef QG_TINY_DUAL
+#define QG_TINY_DUAL 0  // 1: two accumulator sets (even / odd k4 steps), 8 independent DMMA chains per warp
 #endif
 constexpr int kTinyWarps = QG_TINY_WARPS;
 constexpr int kTinyThreads = kTinyWarps * 32;
 template <typename T, int kOps>
-__global__ void __launch_bounds__(kTinyThreads, 512 / kTinyThreads) qgemm_tiny_kernel(SmallArgs a) {
+__global__ void __launch_bounds__(kTinyThreads, (QG_TINY_DUAL ? 384 : 512) / kTinyThreads) qgemm_tiny_kernel(SmallArgs a) {
   constexpr bool a_rc = kOps & 1, a_cj = (kOps >> 1) & 1, b_rc = (kOps >> 2) & 1, b_cj = (kOps >> 3) & 1;
   __shared__ double red[kTinyWarps][32][8];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -370,6 +373,11 @@ __global__ void __launch_bounds__(kTinyThreads, 512 / kTinyThreads) qgemm_tiny_k
   double acc[4][2];
 #pragma unroll
   for (int c = 0; c < 4; ++c) acc[c][0] = acc[c][1] = 0.0;
+#if QG_TINY_DUAL
+  double acc2[4][2];
+#pragma unroll
+  for (int c = 0; c < 4; ++c) acc2[c][0] = acc2[c][1] = 0.0;
+#endif
   int64_t st = s0;
   for (; st + kSmallUnroll <= s1; st += kSmallUnroll) {  // loads of 4 steps in flight
     double qa[kSmallUnroll][4], qb[kSmallUnroll][4];
@@ -379,10 +387,19 @@ __global__ void __launch_bounds__(kTinyThreads, 512 / kTinyThreads) qgemm_tiny_k
       ld_quat_wide(pb + u * db, qb[u]);
     }
 #pragma unroll
-    for (int u = 0; u < kSmallUnroll; ++u) tiny_step<a_cj, b_cj>(acc, qa[u], qb[u]);
+    for (int u = 0; u < kSmallUnroll; ++u) {
+#if QG_TINY_DUAL
+      if (u & 1) { tiny_step<a_cj, b_cj>(acc2, qa[u], qb[u]); continue; }
+#endif
+      tiny_step<a_cj, b_cj>(acc, qa[u], qb[u]);
+    }
     pa += kSmallUnroll * da;
     pb += kSmallUnroll * db;
   }
+#if QG_TINY_DUAL
+#pragma unroll
+  for (int c = 0; c < 4; ++c) { acc[c][0] += acc2[c][0]; acc[c][1] += acc2[c][1]; }
+#endif
   for (; st < s1; ++st) {
     double qa[4], qb[4];
     ld_quat_wide(pa, qa);
