@@ -157,28 +157,14 @@ size_t tc2_part_bytes(int64_t M, int64_t N, int64_t ktiles) {
   return align256(size_t(pairs) * size_t(S) * 2 * size_t(qg::kTc2PartFloats) * sizeof(float));
 }
 
+// FP32 pair kernel, chunk promotion (qg_tc32_2cta.cuh): one raw 4 x 128 x 128
+// FP32 slot per SM (indexed by %smid; 37.9 MB on 148 SMs).
+size_t tc2_slot_bytes() { return align256(size_t(num_sms()) * size_t(qg::kTc2PartFloats) * sizeof(float)); }
+
 template <typename T>
 size_t sk_reserve(int64_t M, int64_t N, int64_t ktiles) {
-  if (sizeof(T) != 8) return tc2_part_bytes(M, N, ktiles);
+  if (sizeof(T) != 8) return (QG_TC32_2CTA ? tc2_slot_bytes() : 0) + tc2_part_bytes(M, N, ktiles);
   return sk_slots_bytes<T>(M, N, ktiles) + align256(size_t(2 * qg::kMaxPersistentCTAs) * sizeof(int));
-}
-
-// Longest K-panel of one launch.  FP32 (tcgen05, FP32 accumulation in TMEM):
-// the tensor core's accumulator adds are truncating, so the error of one
-// launch grows like K^1.5 (each of ~12 K/8 accumulation steps errs by ~u |D|,
-// |D| ~ sqrt(K), with a bias that does not average out; measured
-// tools/f32_accuracy.py: max error / north-star tolerance 0.004 at K = 256,
-// 0.013 at 1024, 0.048 at 4096, 0.087 at 8192 -- the tolerance grows only like
-// sqrt(K)).  Panels of <= 8192 k add their results into C with round-to-nearest
-// FP32 (beta = 1 after the first panel), so beyond one panel the error grows
-// like sqrt(K) as the tolerance does.  FP64 (DMMA, exact FP64 accumulation):
-// no cap.
-#ifndef QG_F32_MAX_PANEL_K
-#define QG_F32_MAX_PANEL_K 8192
-#endif
-template <typename T>
-constexpr int64_t max_panel_kt() {
-  return sizeof(T) == 8 ? INT64_MAX : int64_t(QG_F32_MAX_PANEL_K) / qg::kTcBK;
 }
 
 template <typename T>
@@ -607,10 +593,13 @@ int launch_mainloop(const float *Ap, const float *Bp, float *C, int64_t ldc, int
     int rc = encode_packed_2d(&t.tmA, Ap, 2 * t.MT2 * KT, 32);
     if (!rc) rc = encode_packed_2d(&t.tmB, Bp, t.NT * KT, 16);
     if (rc) return rc;
-    // fewer tile pairs than a wave: split K (the caller reserved tc2_part_bytes
-    // at sk_scratch), then one reduce + epilogue launch
-    t.S = sk_scratch ? int(tc2_splits(M, N, KT)) : 1;
-    t.part = static_cast<float *>(sk_scratch);
+    // sk_scratch = [per-SM chunk slots][split-K partials] (sk_reserve<float>):
+    // fewer tile pairs than a wave -> split K, then one reduce + epilogue launch
+    t.kc = QG_TC2_CHUNK_KT;
+    t.tmp = static_cast<float *>(sk_scratch);
+    t.nslots = num_sms();
+    t.S = int(tc2_splits(M, N, KT));
+    t.part = reinterpret_cast<float *>(static_cast<char *>(sk_scratch) + tc2_slot_bytes());
     const int64_t grid = 2 * t.MT2 * t.NT * t.S;
     if (grid > INT32_MAX) return int(cudaErrorInvalidConfiguration);
     { int ti = tstart(kMain, st);

@@ -33,7 +33,7 @@ constexpr uint32_t kTc2ABytes = kTcChunkBytes;       // 32 KB: this CTA's 128 ro
 constexpr uint32_t kTc2BBytes = kTcChunkBytes / 2;   // 16 KB: this CTA's 64 columns, 8 planes
 constexpr int kTc2AFloats = kTcChunkFloats;
 constexpr int kTc2BFloats = kTcChunkFloats / 2;
-constexpr size_t kTc2SmemBytes = size_t(kTc2Stages) * (kTc2ABytes + kTc2BBytes) + 256 + 1024;
+constexpr size_t kTc2SmemBytes = size_t(kTc2Stages) * (kTc2ABytes + kTc2BBytes) + 256 + 1024;  // + barriers
 constexpr uint32_t kPeerBitMask = 0xFEFFFFFFu;  // shared::cluster address of the leader's copy
 
 struct alignas(64) Tc2Args {
@@ -44,9 +44,60 @@ struct alignas(64) Tc2Args {
   Scalars<float> sc;
   int S;             // K splits per tile pair (1: the epilogue updates C)
   float *part;       // S > 1: raw accumulators, kTc2PartFloats per CTA, summed by tc2_reduce_kernel
+  int kc;            // k-tiles per TMEM accumulation chunk (promotion, see below)
+  float *tmp;        // chunk promotion: one kTc2PartFloats running-sum slot per SM id (%smid) ...
+  int nslots;        // ... for SM ids < nslots
 };
 // One CTA's raw partial: 4 components x 128 columns x 128 rows, rows fastest.
 constexpr int64_t kTc2PartFloats = 4 * int64_t(kTcBN) * kTcBM;
+
+// ---- Accumulation chunks ("promotion").  The tensor core adds each MMA's
+// products into the TMEM accumulator with truncating FP32 arithmetic, so the
+// error of one accumulation chain grows like (steps) x |D| ~ K^1.5, faster
+// than the north-star tolerance's sqrt(K) (tools/f32_accuracy.py; one 8192-deep
+// chain of uniform data errs by ~7 x tol).  A unit's k-tiles are therefore
+// accumulated in chunks of kc k-tiles (error ~ sqrt(K / kc) kc^1.5: a constant
+// fraction of the tolerance, proportional to kc): after every chunk but the last
+// the epilogue warps read TMEM component by component, release each component
+// to the MMA issuer at once (it waits per component before the next chunk's
+// first MMA into it, so the next chunk overlaps the drain), and add the values
+// into their SM's running-sum slot with round-to-nearest FP32.  The last chunk
+// adds the slot and folds into the target: C <- alpha sum + beta C, or, for a
+// split-K unit, the raw partial.  Each thread only touches its own TMEM lane
+// (row) of the slot, so the slot needs no synchronisation beyond program order;
+// one CTA per SM (shared memory) makes the %smid-indexed slot private to the
+// running CTA (the host sizes the slots by the SM count; a CTA on an SM id past
+// it -- ids need not be contiguous -- folds every chunk into the target
+// straight from TMEM, holding TMEM during the fold).
+#ifndef QG_TC2_CHUNK_KT
+#define QG_TC2_CHUNK_KT 32  // 256 quaternion k per chunk
+#endif
+__device__ __forceinline__ uint32_t smid() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%smid;\n" : "=r"(r));
+  return r;
+}
+// Arrive on the barrier at this smem offset in CTA `rank` of the cluster (release, cluster scope).
+__device__ __forceinline__ void mbar_arrive_cluster(uint64_t *bar, uint32_t rank) {
+  uint32_t remote;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;\n" : "=r"(remote) : "r"(smem_u32(bar)), "r"(rank));
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];\n" ::"r"(remote) : "memory");
+}
+// Wait with cluster-scope acquire (arrivals from the peer CTA).
+__device__ __forceinline__ void mbar_wait_cluster(uint64_t *bar, uint32_t parity) {
+  const long long t0 = clock64();
+  uint32_t done = 0;
+  while (true) {
+    asm volatile(
+        "{\n.reg .pred P1;\nmbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 P1, [%1], %2;\n"
+        "selp.b32 %0, 1, 0, P1;\n}\n"
+        : "=r"(done)
+        : "r"(smem_u32(bar)), "r"(parity)
+        : "memory");
+    if (done) return;
+    if (clock64() - t0 > 20000000000LL) __trap();
+  }
+}
 
 // Tile pair `pid` of the grouped raster (kTc2GroupM pair-rows per group).
 __device__ __forceinline__ void tc2_tile(int64_t pid, int64_t MT2, int64_t NT, int64_t &pm, int64_t &pn) {
@@ -104,7 +155,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kTcThreads, 1)
   uint64_t *full = reinterpret_cast<uint64_t *>(sB + kTc2Stages * kTc2BFloats);  // leader's counts both CTAs
   uint64_t *empty = full + kTc2Stages;
   uint64_t *acc_full = empty + kTc2Stages;
-  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(acc_full + 1);
+  uint64_t *acc_empty = acc_full + 1;  // [4] leader: component c of TMEM drained by both CTAs (chunks)
+  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(acc_empty + 4);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t rank = cluster_rank();
@@ -124,6 +176,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kTcThreads, 1)
       mbar_init(&empty[s], 1);
     }
     mbar_init(acc_full, 1);
+    for (int c = 0; c < 4; ++c) mbar_init(&acc_empty[c], 8);  // 4 epilogue warps x 2 CTAs
     fence_mbar_init();
   }
   if (warp == 0) {
@@ -151,7 +204,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kTcThreads, 1)
     // ---------------- MMA issuer (leader only) ----------------
     int slot = 0;
     uint32_t phase = 0;
+    const int64_t kc = args.kc;
+    uint32_t chunk = 0;
     for (int64_t kt = k0; kt < k1; ++kt) {
+      const bool fresh = (kt - k0) % kc == 0;  // first k-tile of an accumulation chunk
       mbar_wait_guarded(&full[slot], phase);
       tc_fence_after();
       const uint32_t a0 = smem_u32(sA + slot * kTc2AFloats);
@@ -159,6 +215,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kTcThreads, 1)
 #pragma unroll
       for (int c = 0; c < 4; ++c) {
         const uint32_t d = tmem + uint32_t(c * kTcBN);
+        if (fresh && kt > k0) {  // both CTAs' epilogue warps have read component c of the previous chunk
+          mbar_wait_cluster(&acc_empty[c], (chunk - 1) & 1u);
+          tc_fence_after();
+        }
 #pragma unroll
         for (int p = 0; p < 4; ++p) {
           const int s = p ^ c;
@@ -167,61 +227,135 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kTcThreads, 1)
           const uint64_t alo = tc_sdesc(a0 + (p * 2 + 1) * kTcPlaneFloats * 4);
           const uint64_t bhi = tc_sdesc(b0 + (s * 2 + 0) * (kTcPlaneFloats / 2) * 4);
           const uint64_t blo = tc_sdesc(b0 + (s * 2 + 1) * (kTcPlaneFloats / 2) * 4);
-          tc2_mma(d, ahi, bhi, id, (kt > k0 || p > 0) ? 1u : 0u);
+          tc2_mma(d, ahi, bhi, id, (!fresh || p > 0) ? 1u : 0u);
           tc2_mma(d, ahi, blo, id, 1u);
           tc2_mma(d, alo, bhi, id, 1u);
         }
       }
       tc2_commit_both(&empty[slot]);  // both CTAs may refill this stage
       if (++slot == kTc2Stages) { slot = 0; phase ^= 1u; }
+      if ((kt + 1 - k0) % kc == 0 || kt + 1 == k1) {
+        tc2_commit_both(acc_full);  // this chunk's accumulators complete, in both CTAs' TMEM
+        ++chunk;
+      }
     }
-    tc2_commit_both(acc_full);  // accumulators complete, in both CTAs' TMEM
   } else if (warp >= 4) {
     // ---------------- epilogue (both CTAs): TMEM -> registers -> C ----------------
     const int q = warp - 4;
     const int64_t row = mt * kTcBM + q * 32 + lane;
-    mbar_wait_guarded(acc_full, 0);
-    tc_fence_after();
     const uint32_t tbase = tmem + (uint32_t(q * 32) << 16);
     float *part = args.S > 1 ? args.part + ((pid * args.S + ks) * 2 + rank) * kTc2PartFloats : nullptr;
-    for (int n0 = 0; n0 < kTcBN; n0 += 16) {
-      float d[4][16];
-#pragma unroll
-      for (int c = 0; c < 4; ++c) tmem_ld16(tbase + uint32_t(c * kTcBN + n0), d[c]);
-      tmem_ld_wait();
-      if (part) {  // split K: park the raw sums (coalesced over the 32 rows of the warp)
+    const int64_t nchunks = (k1 - k0 + args.kc - 1) / args.kc;
+    // this SM's running-sum slot (planar [c][col][row]); without one (SM id past
+    // the slots) every chunk folds into the target straight from TMEM
+    const uint32_t sm = smid();
+    float *slotp = sm < uint32_t(args.nslots) ? args.tmp + int64_t(sm) * kTc2PartFloats + q * 32 + lane : nullptr;
+    // Fold 16 columns of this thread's row into the target: split-K partial (raw)
+    // or C (alpha; beta on the first contribution, else + C).
+    auto fold16 = [&](int n0, const float (&d)[4][16], bool first_chunk) {
+      if (part) {  // split K: raw sums (coalesced over the 32 rows of the warp)
 #pragma unroll
         for (int c = 0; c < 4; ++c)
 #pragma unroll
-          for (int jj = 0; jj < 16; ++jj)
-            __stcg(part + (int64_t(c) * kTcBN + n0 + jj) * kTcBM + q * 32 + lane, d[c][jj]);
-        continue;
-      }
-      if (row < args.M) {
-        float cold[16][4];
-        if (!args.sc.beta_zero) {
-#pragma unroll
           for (int jj = 0; jj < 16; ++jj) {
-            const int64_t col = pn * kTcBN + n0 + jj;
-            if (col < args.N) ldq_c(args.C + 4 * (row + col * args.ldc), cold[jj]);
+            float *pp = part + (int64_t(c) * kTcBN + n0 + jj) * kTcBM + q * 32 + lane;
+            __stcg(pp, first_chunk ? d[c][jj] : __ldcg(pp) + d[c][jj]);
           }
-        }
+        return;
+      }
+      if (row >= args.M) return;
+      float cold[16][4];
+      if (!args.sc.beta_zero || !first_chunk) {  // (beta = 0: C is never read, R3)
 #pragma unroll
         for (int jj = 0; jj < 16; ++jj) {
           const int64_t col = pn * kTcBN + n0 + jj;
-          if (col >= args.N) continue;
-          const float acc[4] = {d[0][jj], d[1][jj], d[2][jj], d[3][jj]};
-          float out[4];
-          left_scale(args.sc.alpha, args.sc.alpha_real, acc, out);
-          if (!args.sc.beta_zero) {
-            float bc[4];
-            left_scale(args.sc.beta, args.sc.beta_real, cold[jj], bc);
-#pragma unroll
-            for (int k = 0; k < 4; ++k) out[k] += bc[k];
-          }
-          stq(args.C + 4 * (row + col * args.ldc), out);
+          if (col < args.N) ldq_c(args.C + 4 * (row + col * args.ldc), cold[jj]);
         }
       }
+#pragma unroll
+      for (int jj = 0; jj < 16; ++jj) {
+        const int64_t col = pn * kTcBN + n0 + jj;
+        if (col >= args.N) continue;
+        const float acc[4] = {d[0][jj], d[1][jj], d[2][jj], d[3][jj]};
+        float out[4];
+        left_scale(args.sc.alpha, args.sc.alpha_real, acc, out);
+        if (!first_chunk) {
+#pragma unroll
+          for (int k = 0; k < 4; ++k) out[k] += cold[jj][k];
+        } else if (!args.sc.beta_zero) {
+          float bc[4];
+          left_scale(args.sc.beta, args.sc.beta_real, cold[jj], bc);
+#pragma unroll
+          for (int k = 0; k < 4; ++k) out[k] += bc[k];
+        }
+        stq(args.C + 4 * (row + col * args.ldc), out);
+      }
+    };
+    auto ld_tmem16 = [&](int n0, float (&d)[4][16]) {
+#pragma unroll
+      for (int c = 0; c < 4; ++c) tmem_ld16(tbase + uint32_t(c * kTcBN + n0), d[c]);
+      tmem_ld_wait();
+    };
+    auto release = [&](int c) {  // component c of TMEM may be overwritten by the next chunk
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive_cluster(&acc_empty[c], 0);
+    };
+    for (int64_t j = 0; j < nchunks; ++j) {
+      mbar_wait_guarded(acc_full, uint32_t(j & 1));
+      tc_fence_after();
+      if (j + 1 < nchunks && slotp) {
+        // component by component: TMEM -> registers, release the component (the
+        // next chunk's MMAs into it may start), then slot (+)= values with
+        // round-to-nearest FP32 adds
+#pragma unroll 1
+        for (int c = 0; c < 4; ++c) {
+          float v[kTcBN];
+#pragma unroll
+          for (int n0 = 0; n0 < kTcBN; n0 += 16) {
+            float (&d)[16] = *reinterpret_cast<float (*)[16]>(&v[n0]);
+            tmem_ld16(tbase + uint32_t(c * kTcBN + n0), d);
+          }
+          tmem_ld_wait();
+          release(c);
+          float *sp = slotp + int64_t(c) * kTcBN * kTcBM;
+          if (j == 0) {
+#pragma unroll
+            for (int n = 0; n < kTcBN; ++n) __stcg(sp + int64_t(n) * kTcBM, v[n]);
+          } else {
+#pragma unroll
+            for (int n0 = 0; n0 < kTcBN; n0 += 32) {  // 32 loads in flight before any store
+              float o[32];
+#pragma unroll
+              for (int n = 0; n < 32; ++n) o[n] = __ldcg(sp + int64_t(n0 + n) * kTcBM);
+#pragma unroll
+              for (int n = 0; n < 32; ++n) __stcg(sp + int64_t(n0 + n) * kTcBM, o[n] + v[n0 + n]);
+            }
+          }
+        }
+        continue;
+      }
+      // fold into the target straight from TMEM: the last chunk (plus the running
+      // sum of the earlier ones from the slot), or every chunk without a slot
+      const bool from_slot = slotp && nchunks > 1;
+      for (int n0 = 0; n0 < kTcBN; n0 += 16) {
+        float d[4][16];
+        ld_tmem16(n0, d);
+        if (from_slot) {
+          float o[4][16];
+#pragma unroll
+          for (int c = 0; c < 4; ++c)
+#pragma unroll
+            for (int jj = 0; jj < 16; ++jj) o[c][jj] = __ldcg(slotp + (int64_t(c) * kTcBN + n0 + jj) * kTcBM);
+#pragma unroll
+          for (int c = 0; c < 4; ++c)
+#pragma unroll
+            for (int jj = 0; jj < 16; ++jj) d[c][jj] += o[c][jj];
+        }
+        fold16(n0, d, from_slot || j == 0);
+      }
+      if (j + 1 < nchunks)
+        for (int c = 0; c < 4; ++c) release(c);
     }
   }
   tc_fence_before();

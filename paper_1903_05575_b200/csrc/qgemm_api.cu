@@ -82,7 +82,7 @@ int panel_loop(const PackSpec<T> &pa, const PackSpec<T> &pb, int64_t M, int64_t 
   const size_t min_ws = workspace_for<T>(M, N, K, 1);
   if (workspace == nullptr || (reinterpret_cast<uintptr_t>(workspace) & 255u)) return -14;
   if (workspace_bytes < min_ws) return -15;
-  int64_t KTp = std::min<int64_t>(KT_total, max_panel_kt<T>());
+  int64_t KTp = KT_total;
   while (KTp > 1 && workspace_for<T>(M, N, K, KTp) > workspace_bytes) {
     // largest panel that fits; start from a proportional estimate
     const size_t res = sk_reserve<T>(M, N, KT_total);
@@ -166,7 +166,7 @@ size_t ws_bytes(char transA, char transB, int64_t M, int64_t N, int64_t K, bool 
   if (use_small<T>(M, N, K)) return 0;  // the small kernel needs no workspace
   if (direct_feed<T>(op_code(transA), op_code(transB), M, N, K))
     return sk_reserve<T>(M, N, cdiv(K, Geo<T>::kq));  // stream-K scratch only
-  return workspace_for<T>(M, N, K, minimum ? 1 : std::min<int64_t>(cdiv(K, Geo<T>::kq), max_panel_kt<T>()));
+  return workspace_for<T>(M, N, K, minimum ? 1 : cdiv(K, Geo<T>::kq));
 }
 
 #include "qg_host_path.cuh"

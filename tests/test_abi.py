@@ -127,6 +127,11 @@ def test_qherk_invalid_arguments(lib, kw, code):
     assert lib.qgemm_last_launch_count() == 0
 
 
+# FP32 pair kernel: one raw 4 x 128 x 128 FP32 slot per SM for the accumulation
+# chunks (qg_tc32_2cta.cuh), 148 SMs assumed without a device
+F32_SLOTS = 148 * 4 * 128 * 128 * 4
+
+
 def test_workspace_sizes(lib):
     old = lib.qgemm_set_path_policy(1)  # the packed path's sizes
     f64 = lib.qgemm_workspace_bytes(b"N", b"H", 8192, 8192, 8192, 0)
@@ -135,7 +140,9 @@ def test_workspace_sizes(lib):
     # mainloop: 256 partial slots of 128 KiB + 512 arrival counters
     sk = 256 * 131072 + 2048
     assert f64 == 2 * 8192 * 8192 * 32 + sk
-    assert f32 == 2 * 8192 * 8192 * 32  # tcgen05 3xTF32 path: tf32 hi + lo planes
+    # tcgen05 3xTF32 path: tf32 hi + lo planes + one 256 KiB accumulation-chunk slot
+    # per SM (148 assumed without a device)
+    assert f32 == 2 * 8192 * 8192 * 32 + F32_SLOTS
     # one K-tile: 2 row tiles of A + 2 of B, 32 KiB per (64 x 16)-quaternion chunk,
     # + partial slots for the largest grid over the whole K (4 tiles x 63 k-tiles
     # / 2 = 126 CTAs) + counters
@@ -164,7 +171,7 @@ def test_direct_path_workspace_is_stream_k_scratch(lib):
         lib.qgemm_set_path_policy(pol)
         assert lib.qgemm_workspace_bytes(b"N", b"H", 8192, 8192, 8192, 0) == sk
         assert lib.qgemm_workspace_min_bytes(b"N", b"H", 8192, 8192, 8192, 0) == sk
-        assert lib.qgemm_workspace_bytes(b"N", b"H", 8192, 8192, 8192, 1) == 2 * 8192 * 8192 * 32
+        assert lib.qgemm_workspace_bytes(b"N", b"H", 8192, 8192, 8192, 1) == 2 * 8192 * 8192 * 32 + F32_SLOTS
         assert lib.qherk_workspace_bytes(b"L", b"N", 32768, 256) == sk
     lib.qgemm_set_path_policy(1)  # packed
     assert lib.qherk_workspace_bytes(b"L", b"N", 32768, 256) > sk
@@ -243,7 +250,7 @@ def test_host_workspace_f32_covers_every_panel_split(lib, N):
     ktc = kc // 8                                # FP32 k-tiles per chunk (8 k per tile)
     packed = 2 * (2 * (M // 256)) * ktc * 32768 + 2 * (N // 128) * ktc * 32768
     part = 32 * 2 * 2 * 65536 * 4                # pairs x S x 2 CTAs x 4x128x128 floats
-    want = 2 * M * N * qb + stage + packed + part
+    want = 2 * M * N * qb + stage + packed + F32_SLOTS + part
     assert lib.qgemm_host_workspace_bytes(b"N", b"H", M, N, K, 1) == want
 
 

@@ -488,15 +488,15 @@ def test_metamorphic_conjugate_transpose_identity(n):
     assert float((C2 - conjT).abs().max()) <= tol
 
 
-def test_f32_long_k_error_bounded_by_k_panels():
-    """FP32 on the tensor cores accumulates with truncating FP32 adds, so one
-    launch's error grows like K^1.5 (tools/f32_accuracy.py) while the north-star
-    tolerance grows like sqrt(K); the library therefore cuts K into panels of
-    <= 8192 whose results are added into C with round-to-nearest (beta = 1 after
-    the first).  M = N = 2048, K = 32768 (4 panels, no split-K: 128 tile pairs):
-    max error / tol must stay at the single-panel level (~0.09 at K = 8192), far
-    below the ~0.35 one 32768-deep accumulation gives.  Checked on 2 full rows and
-    2 full columns against the oracle on the FP64 inputs (reading R11)."""
+def test_f32_long_k_error_bounded_by_accumulation_chunks():
+    """FP32 on the tensor cores: the TMEM accumulator adds truncate, so one
+    accumulation chain's error grows like K^1.5 (tools/f32_accuracy.py) while
+    the north-star tolerance grows like sqrt(K); the pair kernel therefore
+    accumulates in chunks of 256 k and adds the chunks with round-to-nearest FP32
+    (qg_tc32_2cta.cuh), which keeps the error a constant fraction of the
+    tolerance (~0.2 for uniform data).  M = N = 2048, K = 32768 (128 tile pairs,
+    no split-K; one 32768-deep chain gave ~7 x tol): max error / tol <= 0.5 on 2
+    full rows and 2 full columns against the oracle on the FP64 inputs (R11)."""
     from synth.gpu_gen import counter_matrix, host_cols, host_rows_N
     n, K = 2048, 32768
     A = counter_matrix(0, 1, n, K, "cuda")             # stored n x K (op N)
@@ -504,7 +504,6 @@ def test_f32_long_k_error_bounded_by_k_panels():
     C = torch.zeros((n, n, 4), dtype=torch.float32, device="cuda")
     qg.qgemm_f32("N", "N", 1.0, A.float(), B.float(), 0.0, C)
     torch.cuda.synchronize()
-    assert qg.last_launch_count() >= 8                 # 4 panels x (pack + mainloop)
     rows, cols = np.array([1, n - 3]), np.array([0, n - 1])
     A_S = host_rows_N(0, 1, n, rows, K)                # (K, 2, 4)
     B_C = host_cols(0, 2, K, cols, K)                  # (2, K, 4)
@@ -517,4 +516,4 @@ def test_f32_long_k_error_bounded_by_k_panels():
     got = C.double().cpu().numpy()
     err = max(float(np.abs(got[:, rows, :] - ref_r).max()), float(np.abs(got[cols] - ref_c).max()))
     tol = 1e-4 * K ** 0.5 * float(np.abs(A_h).max()) * float(np.abs(B_h).max())
-    assert err <= 0.15 * tol, (err, tol)
+    assert err <= 0.5 * tol, (err, tol)
