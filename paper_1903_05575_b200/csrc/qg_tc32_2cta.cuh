@@ -45,7 +45,7 @@ struct alignas(64) Tc2Args {
   int S;             // K splits per tile pair (1: the epilogue updates C)
   float *part;       // S > 1: raw accumulators, kTc2PartFloats per CTA, summed by tc2_reduce_kernel
   int kc;            // k-tiles per TMEM accumulation chunk (promotion, see below)
-  float *tmp;        // chunk promotion: one kTc2PartFloats running-sum slot per SM id (%smid) ...
+  float *tmp;        // chunk promotion: one kTc2PartFloats slot per SM id (%smid) ...
   int nslots;        // ... for SM ids < nslots
 };
 // One CTA's raw partial: 4 components x 128 columns x 128 rows, rows fastest.
@@ -60,11 +60,12 @@ constexpr int64_t kTc2PartFloats = 4 * int64_t(kTcBN) * kTcBM;
 // fraction of the tolerance, proportional to kc): after every chunk but the last
 // the epilogue warps read TMEM component by component, release each component
 // to the MMA issuer at once (it waits per component before the next chunk's
-// first MMA into it, so the next chunk overlaps the drain), and add the values
-// into their SM's running-sum slot with round-to-nearest FP32.  The last chunk
-// adds the slot and folds into the target: C <- alpha sum + beta C, or, for a
-// split-K unit, the raw partial.  Each thread only touches its own TMEM lane
-// (row) of the slot, so the slot needs no synchronisation beyond program order;
+// first MMA into it, so the next chunk overlaps the drain) and store the values
+// into their SM's slot; then, while the next chunk runs, fold the slot into the
+// target with round-to-nearest FP32: C <- alpha chunk + (first ? beta C : C),
+// or, for a split-K unit, the raw partial (+)= chunk.  The last chunk folds
+// straight from TMEM.  Each thread only touches its own TMEM lane (row) of the
+// slot, so the slot needs no synchronisation beyond program order;
 // one CTA per SM (shared memory) makes the %smid-indexed slot private to the
 // running CTA (the host sizes the slots by the SM count; a CTA on an SM id past
 // it -- ids need not be contiguous -- folds every chunk into the target
@@ -144,6 +145,51 @@ __device__ __forceinline__ void tc2_commit_both(uint64_t *bar) {
           smem_u32(bar)),
       "h"((unsigned short)3)
       : "memory");
+}
+
+// Fold W columns (n0..) of one thread's row into the target: the split-K
+// partial (raw sums, coalesced over the warp's rows) or C (alpha; beta on the
+// first contribution, else + C).
+template <int W>
+__device__ __forceinline__ void tc2_fold(const Tc2Args &args, float *part, int64_t row, int64_t pn, int lr, int n0,
+                                         const float (&d)[4][W], bool first_chunk) {
+  if (part) {
+#pragma unroll
+    for (int c = 0; c < 4; ++c)
+#pragma unroll
+      for (int jj = 0; jj < W; ++jj) {
+        float *pp = part + (int64_t(c) * kTcBN + n0 + jj) * kTcBM + lr;
+        __stcg(pp, first_chunk ? d[c][jj] : __ldcg(pp) + d[c][jj]);
+      }
+    return;
+  }
+  if (row >= args.M) return;
+  float cold[W][4];
+  if (!args.sc.beta_zero || !first_chunk) {  // (beta = 0: C is never read, R3)
+#pragma unroll
+    for (int jj = 0; jj < W; ++jj) {
+      const int64_t col = pn * kTcBN + n0 + jj;
+      if (col < args.N) ldq_c(args.C + 4 * (row + col * args.ldc), cold[jj]);
+    }
+  }
+#pragma unroll
+  for (int jj = 0; jj < W; ++jj) {
+    const int64_t col = pn * kTcBN + n0 + jj;
+    if (col >= args.N) continue;
+    const float acc[4] = {d[0][jj], d[1][jj], d[2][jj], d[3][jj]};
+    float out[4];
+    left_scale(args.sc.alpha, args.sc.alpha_real, acc, out);
+    if (!first_chunk) {
+#pragma unroll
+      for (int k = 0; k < 4; ++k) out[k] += cold[jj][k];
+    } else if (!args.sc.beta_zero) {
+      float bc[4];
+      left_scale(args.sc.beta, args.sc.beta_real, cold[jj], bc);
+#pragma unroll
+      for (int k = 0; k < 4; ++k) out[k] += bc[k];
+    }
+    stq(args.C + 4 * (row + col * args.ldc), out);
+  }
 }
 
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kTcThreads, 1)
@@ -250,47 +296,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kTcThreads, 1)
     // the slots) every chunk folds into the target straight from TMEM
     const uint32_t sm = smid();
     float *slotp = sm < uint32_t(args.nslots) ? args.tmp + int64_t(sm) * kTc2PartFloats + q * 32 + lane : nullptr;
-    // Fold 16 columns of this thread's row into the target: split-K partial (raw)
-    // or C (alpha; beta on the first contribution, else + C).
-    auto fold16 = [&](int n0, const float (&d)[4][16], bool first_chunk) {
-      if (part) {  // split K: raw sums (coalesced over the 32 rows of the warp)
-#pragma unroll
-        for (int c = 0; c < 4; ++c)
-#pragma unroll
-          for (int jj = 0; jj < 16; ++jj) {
-            float *pp = part + (int64_t(c) * kTcBN + n0 + jj) * kTcBM + q * 32 + lane;
-            __stcg(pp, first_chunk ? d[c][jj] : __ldcg(pp) + d[c][jj]);
-          }
-        return;
-      }
-      if (row >= args.M) return;
-      float cold[16][4];
-      if (!args.sc.beta_zero || !first_chunk) {  // (beta = 0: C is never read, R3)
-#pragma unroll
-        for (int jj = 0; jj < 16; ++jj) {
-          const int64_t col = pn * kTcBN + n0 + jj;
-          if (col < args.N) ldq_c(args.C + 4 * (row + col * args.ldc), cold[jj]);
-        }
-      }
-#pragma unroll
-      for (int jj = 0; jj < 16; ++jj) {
-        const int64_t col = pn * kTcBN + n0 + jj;
-        if (col >= args.N) continue;
-        const float acc[4] = {d[0][jj], d[1][jj], d[2][jj], d[3][jj]};
-        float out[4];
-        left_scale(args.sc.alpha, args.sc.alpha_real, acc, out);
-        if (!first_chunk) {
-#pragma unroll
-          for (int k = 0; k < 4; ++k) out[k] += cold[jj][k];
-        } else if (!args.sc.beta_zero) {
-          float bc[4];
-          left_scale(args.sc.beta, args.sc.beta_real, cold[jj], bc);
-#pragma unroll
-          for (int k = 0; k < 4; ++k) out[k] += bc[k];
-        }
-        stq(args.C + 4 * (row + col * args.ldc), out);
-      }
-    };
     auto ld_tmem16 = [&](int n0, float (&d)[4][16]) {
 #pragma unroll
       for (int c = 0; c < 4; ++c) tmem_ld16(tbase + uint32_t(c * kTcBN + n0), d[c]);
@@ -306,8 +311,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kTcThreads, 1)
       tc_fence_after();
       if (j + 1 < nchunks && slotp) {
         // component by component: TMEM -> registers, release the component (the
-        // next chunk's MMAs into it may start), then slot (+)= values with
-        // round-to-nearest FP32 adds
+        // next chunk's MMAs into it may start), registers -> slot (plain stores);
+        // then fold the slot into the target while the next chunk runs
 #pragma unroll 1
         for (int c = 0; c < 4; ++c) {
           float v[kTcBN];
@@ -319,40 +324,24 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kTcThreads, 1)
           tmem_ld_wait();
           release(c);
           float *sp = slotp + int64_t(c) * kTcBN * kTcBM;
-          if (j == 0) {
 #pragma unroll
-            for (int n = 0; n < kTcBN; ++n) __stcg(sp + int64_t(n) * kTcBM, v[n]);
-          } else {
+          for (int n = 0; n < kTcBN; ++n) __stcg(sp + int64_t(n) * kTcBM, v[n]);
+        }
+        for (int n0 = 0; n0 < kTcBN; n0 += 8) {
+          float d[4][8];
 #pragma unroll
-            for (int n0 = 0; n0 < kTcBN; n0 += 32) {  // 32 loads in flight before any store
-              float o[32];
+          for (int c = 0; c < 4; ++c)
 #pragma unroll
-              for (int n = 0; n < 32; ++n) o[n] = __ldcg(sp + int64_t(n0 + n) * kTcBM);
-#pragma unroll
-              for (int n = 0; n < 32; ++n) __stcg(sp + int64_t(n0 + n) * kTcBM, o[n] + v[n0 + n]);
-            }
-          }
+            for (int jj = 0; jj < 8; ++jj) d[c][jj] = __ldcg(slotp + (int64_t(c) * kTcBN + n0 + jj) * kTcBM);
+          tc2_fold<8>(args, part, row, pn, q * 32 + lane, n0, d, j == 0);
         }
         continue;
       }
-      // fold into the target straight from TMEM: the last chunk (plus the running
-      // sum of the earlier ones from the slot), or every chunk without a slot
-      const bool from_slot = slotp && nchunks > 1;
+      // the last chunk (or any chunk without a slot) folds straight from TMEM
       for (int n0 = 0; n0 < kTcBN; n0 += 16) {
         float d[4][16];
         ld_tmem16(n0, d);
-        if (from_slot) {
-          float o[4][16];
-#pragma unroll
-          for (int c = 0; c < 4; ++c)
-#pragma unroll
-            for (int jj = 0; jj < 16; ++jj) o[c][jj] = __ldcg(slotp + (int64_t(c) * kTcBN + n0 + jj) * kTcBM);
-#pragma unroll
-          for (int c = 0; c < 4; ++c)
-#pragma unroll
-            for (int jj = 0; jj < 16; ++jj) d[c][jj] += o[c][jj];
-        }
-        fold16(n0, d, from_slot || j == 0);
+        tc2_fold<16>(args, part, row, pn, q * 32 + lane, n0, d, j == 0);
       }
       if (j + 1 < nchunks)
         for (int c = 0; c < 4; ++c) release(c);
