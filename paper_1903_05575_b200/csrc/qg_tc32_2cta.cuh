@@ -154,13 +154,17 @@ template <int W>
 __device__ __forceinline__ void tc2_fold(const Tc2Args &args, float *part, int64_t row, int64_t pn, int lr, int n0,
                                          const float (&d)[4][W], bool first_chunk) {
   if (part) {
+    float old[4][W];
 #pragma unroll
     for (int c = 0; c < 4; ++c)
 #pragma unroll
-      for (int jj = 0; jj < W; ++jj) {
-        float *pp = part + (int64_t(c) * kTcBN + n0 + jj) * kTcBM + lr;
-        __stcg(pp, first_chunk ? d[c][jj] : __ldcg(pp) + d[c][jj]);
-      }
+      for (int jj = 0; jj < W; ++jj)  // every load before any store (they may alias as far as the compiler knows)
+        old[c][jj] = first_chunk ? 0.f : __ldcg(part + (int64_t(c) * kTcBN + n0 + jj) * kTcBM + lr);
+#pragma unroll
+    for (int c = 0; c < 4; ++c)
+#pragma unroll
+      for (int jj = 0; jj < W; ++jj)
+        __stcg(part + (int64_t(c) * kTcBN + n0 + jj) * kTcBM + lr, first_chunk ? d[c][jj] : old[c][jj] + d[c][jj]);
     return;
   }
   if (row >= args.M) return;

@@ -20,8 +20,10 @@ from synth import make_problem  # noqa: E402
 
 def main():
     n = int(os.environ.get("F32ACC_N", "512"))
-    for K in (64, 256, 1024, 4096, 8192):
-        pr = make_problem(n, n, K, "N", "H", 1, 0, seed=1, dist="normal")
+    dist = os.environ.get("F32ACC_DIST", "normal")     # normal | uniform | int2 (entries in {-2..2})
+    Ks = [int(k) for k in os.environ.get("F32ACC_K", "64,256,1024,4096,8192").split(",")]
+    for K in Ks:
+        pr = make_problem(n, n, K, "N", "H", 1, 0, seed=1, dist=dist)
         A = torch.from_numpy(pr.A).cuda().float()
         B = torch.from_numpy(pr.B).cuda().float()
         C = torch.zeros((n, n, 4), dtype=torch.float32, device="cuda")
@@ -33,7 +35,7 @@ def main():
         oracle.qgemm("N", "H", n, n, K, 1, A.double().cpu().numpy(), B.double().cpu().numpy(), 0, ref32)
         e = got - ref
         tol = 1e-4 * K ** 0.5 * np.abs(pr.A).max() * np.abs(pr.B).max()
-        print(json.dumps({"K": K, "M=N": n, "max_err": float(np.abs(e).max()), "std_err": float(e.std()),
+        print(json.dumps({"K": K, "M=N": n, "dist": dist, "max_err": float(np.abs(e).max()), "std_err": float(e.std()),
                           "mean_err": float(e.mean()), "tol": tol, "max_over_tol": float(np.abs(e).max() / tol),
                           "input_rounding_max_err": float(np.abs(ref32 - ref).max()),
                           "kernel_max_err_vs_rounded_inputs": float(np.abs(got - ref32).max()),
