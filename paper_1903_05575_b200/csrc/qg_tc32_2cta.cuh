@@ -204,8 +204,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kTcThreads, 1)
   float *sB = sA + kTc2Stages * kTc2AFloats;
   uint64_t *full = reinterpret_cast<uint64_t *>(sB + kTc2Stages * kTc2BFloats);  // leader's counts both CTAs
   uint64_t *empty = full + kTc2Stages;
-  uint64_t *acc_full = empty + kTc2Stages;
-  uint64_t *acc_empty = acc_full + 1;  // [4] leader: component c of TMEM drained by both CTAs (chunks)
+  uint64_t *acc_full = empty + kTc2Stages;  // [4] component c of a chunk complete (both CTAs, multicast)
+  uint64_t *acc_empty = acc_full + 4;       // [4] leader: component c of TMEM drained by both CTAs
   uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(acc_empty + 4);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -225,7 +225,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kTcThreads, 1)
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], 1);
     }
-    mbar_init(acc_full, 1);
+    for (int c = 0; c < 4; ++c) mbar_init(&acc_full[c], 1);
     for (int c = 0; c < 4; ++c) mbar_init(&acc_empty[c], 8);  // 4 epilogue warps x 2 CTAs
     fence_mbar_init();
   }
@@ -258,6 +258,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kTcThreads, 1)
     uint32_t chunk = 0;
     for (int64_t kt = k0; kt < k1; ++kt) {
       const bool fresh = (kt - k0) % kc == 0;  // first k-tile of an accumulation chunk
+      const bool ends = (kt + 1 - k0) % kc == 0 || kt + 1 == k1;  // last k-tile of a chunk
       mbar_wait_guarded(&full[slot], phase);
       tc_fence_after();
       const uint32_t a0 = smem_u32(sA + slot * kTc2AFloats);
@@ -281,13 +282,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kTcThreads, 1)
           tc2_mma(d, ahi, blo, id, 1u);
           tc2_mma(d, alo, bhi, id, 1u);
         }
+        // component c of this chunk complete once these MMAs are: the epilogue can
+        // drain it while the pipe still runs the other components
+        if (ends) tc2_commit_both(&acc_full[c]);
       }
       tc2_commit_both(&empty[slot]);  // both CTAs may refill this stage
       if (++slot == kTc2Stages) { slot = 0; phase ^= 1u; }
-      if ((kt + 1 - k0) % kc == 0 || kt + 1 == k1) {
-        tc2_commit_both(acc_full);  // this chunk's accumulators complete, in both CTAs' TMEM
-        ++chunk;
-      }
+      if (ends) ++chunk;
     }
   } else if (warp >= 4) {
     // ---------------- epilogue (both CTAs): TMEM -> registers -> C ----------------
@@ -311,14 +312,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kTcThreads, 1)
       if (lane == 0) mbar_arrive_cluster(&acc_empty[c], 0);
     };
     for (int64_t j = 0; j < nchunks; ++j) {
-      mbar_wait_guarded(acc_full, uint32_t(j & 1));
-      tc_fence_after();
       if (j + 1 < nchunks && slotp) {
         // component by component: TMEM -> registers, release the component (the
         // next chunk's MMAs into it may start), registers -> slot (plain stores);
         // then fold the slot into the target while the next chunk runs
 #pragma unroll 1
         for (int c = 0; c < 4; ++c) {
+          mbar_wait_guarded(&acc_full[c], uint32_t(j & 1));
+          tc_fence_after();
           float v[kTcBN];
 #pragma unroll
           for (int n0 = 0; n0 < kTcBN; n0 += 16) {
@@ -342,6 +343,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kTcThreads, 1)
         continue;
       }
       // the last chunk (or any chunk without a slot) folds straight from TMEM
+      for (int c = 0; c < 4; ++c) mbar_wait_guarded(&acc_full[c], uint32_t(j & 1));
+      tc_fence_after();
       for (int n0 = 0; n0 < kTcBN; n0 += 16) {
         float d[4][16];
         ld_tmem16(n0, d);
