@@ -254,11 +254,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kTcThreads, 1)
     // ---------------- MMA issuer (leader only) ----------------
     int slot = 0;
     uint32_t phase = 0;
-    const int64_t kc = args.kc;
+    const int kc = args.kc;
     uint32_t chunk = 0;
+    int kk = 0;  // k-tile index inside the current accumulation chunk (no divisions in this loop)
     for (int64_t kt = k0; kt < k1; ++kt) {
-      const bool fresh = (kt - k0) % kc == 0;  // first k-tile of an accumulation chunk
-      const bool ends = (kt + 1 - k0) % kc == 0 || kt + 1 == k1;  // last k-tile of a chunk
+      const bool fresh = kk == 0;                         // first k-tile of an accumulation chunk
+      const bool ends = kk == kc - 1 || kt + 1 == k1;     // last k-tile of a chunk
+      if (++kk == kc) kk = 0;
       mbar_wait_guarded(&full[slot], phase);
       tc_fence_after();
       const uint32_t a0 = smem_u32(sA + slot * kTc2AFloats);
