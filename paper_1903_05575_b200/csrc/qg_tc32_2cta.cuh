@@ -147,6 +147,51 @@ __device__ __forceinline__ void tc2_commit_both(uint64_t *bar) {
       : "memory");
 }
 
+// The 48 MMAs of one k-tile (4 output components x 4 products x 3xTF32), with
+// the chunk bookkeeping: before the first MMA into component c of a new chunk,
+// wait until both CTAs' epilogue warps have read that component of the previous
+// chunk; after the last k-tile's MMAs into c, commit "component c complete".
+// (Issued from an elect.sync branch of a whole warp: run by a lane-0-only branch
+// next to the chunk epilogue's register arrays, ptxas moved the descriptors out
+// of uniform registers -- an R2UR per operand per MMA -- and the single issuing
+// thread fell behind the pipe: c3 FP32 67 vs 61 ms with chunks off.)
+__device__ __forceinline__ bool elect_one() {
+  uint32_t pred;
+  asm volatile("{\n.reg .pred p;\nelect.sync _|p, 0xffffffff;\nselp.u32 %0, 1, 0, p;\n}\n" : "=r"(pred));
+  return pred != 0;
+}
+__device__ __forceinline__ void tc2_issue_ktile(uint32_t a0, uint32_t b0, uint32_t tmem, bool fresh, bool wait_empty,
+                                             uint32_t empty_parity, uint64_t *acc_empty, bool ends,
+                                             uint64_t *acc_full) {
+  // descriptors of the stage's first A / B plane; the others differ only in the
+  // start-address field (address >> 4, 14 bits: every smem address fits), so
+  // each is the base plus a compile-time constant
+  const uint64_t da = tc_sdesc(a0), db = tc_sdesc(b0);
+#pragma unroll
+  for (int c = 0; c < 4; ++c) {
+    const uint32_t d = tmem + uint32_t(c * kTcBN);
+    if (wait_empty) {  // both CTAs' epilogue warps have read component c of the previous chunk
+      mbar_wait_cluster(&acc_empty[c], empty_parity);
+      tc_fence_after();
+    }
+#pragma unroll
+    for (int p = 0; p < 4; ++p) {
+      const int s = p ^ c;
+      const uint32_t id = tc2_idesc(hneg(p, s));
+      const uint64_t ahi = da + uint64_t(((p * 2 + 0) * kTcPlaneFloats * 4) >> 4);
+      const uint64_t alo = da + uint64_t(((p * 2 + 1) * kTcPlaneFloats * 4) >> 4);
+      const uint64_t bhi = db + uint64_t(((s * 2 + 0) * (kTcPlaneFloats / 2) * 4) >> 4);
+      const uint64_t blo = db + uint64_t(((s * 2 + 1) * (kTcPlaneFloats / 2) * 4) >> 4);
+      tc2_mma(d, ahi, bhi, id, (!fresh || p > 0) ? 1u : 0u);
+      tc2_mma(d, ahi, blo, id, 1u);
+      tc2_mma(d, alo, bhi, id, 1u);
+    }
+    // component c of this chunk complete once these MMAs are: the epilogue can
+    // drain it while the pipe still runs the other components
+    if (ends) tc2_commit_both(&acc_full[c]);
+  }
+}
+
 // Fold W columns (n0..) of one thread's row into the target: the split-K
 // partial (raw sums, coalesced over the warp's rows) or C (alpha; beta on the
 // first contribution, else + C).
@@ -250,8 +295,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kTcThreads, 1)
       tma2_load_2d(sB + slot * kTc2BFloats, &args.tmB, 0, int((pn * KT + kt) * 32 + rank * 16), &full[slot]);
       if (++slot == kTc2Stages) { slot = 0; phase ^= 1u; }
     }
-  } else if (warp == 1 && lane == 0 && rank == 0) {
+  } else if (warp == 1 && rank == 0) {
     // ---------------- MMA issuer (leader only) ----------------
+    // The whole warp walks the loop (its control values are warp-uniform, so
+    // ptxas keeps the descriptors in uniform registers); one elected lane issues.
     int slot = 0;
     uint32_t phase = 0;
     const int kc = args.kc;
@@ -263,32 +310,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kTcThreads, 1)
       if (++kk == kc) kk = 0;
       mbar_wait_guarded(&full[slot], phase);
       tc_fence_after();
-      const uint32_t a0 = smem_u32(sA + slot * kTc2AFloats);
-      const uint32_t b0 = smem_u32(sB + slot * kTc2BFloats);
-#pragma unroll
-      for (int c = 0; c < 4; ++c) {
-        const uint32_t d = tmem + uint32_t(c * kTcBN);
-        if (fresh && kt > k0) {  // both CTAs' epilogue warps have read component c of the previous chunk
-          mbar_wait_cluster(&acc_empty[c], (chunk - 1) & 1u);
-          tc_fence_after();
-        }
-#pragma unroll
-        for (int p = 0; p < 4; ++p) {
-          const int s = p ^ c;
-          const uint32_t id = tc2_idesc(hneg(p, s));
-          const uint64_t ahi = tc_sdesc(a0 + (p * 2 + 0) * kTcPlaneFloats * 4);
-          const uint64_t alo = tc_sdesc(a0 + (p * 2 + 1) * kTcPlaneFloats * 4);
-          const uint64_t bhi = tc_sdesc(b0 + (s * 2 + 0) * (kTcPlaneFloats / 2) * 4);
-          const uint64_t blo = tc_sdesc(b0 + (s * 2 + 1) * (kTcPlaneFloats / 2) * 4);
-          tc2_mma(d, ahi, bhi, id, (!fresh || p > 0) ? 1u : 0u);
-          tc2_mma(d, ahi, blo, id, 1u);
-          tc2_mma(d, alo, bhi, id, 1u);
-        }
-        // component c of this chunk complete once these MMAs are: the epilogue can
-        // drain it while the pipe still runs the other components
-        if (ends) tc2_commit_both(&acc_full[c]);
-      }
-      tc2_commit_both(&empty[slot]);  // both CTAs may refill this stage
+      if (elect_one())
+        tc2_issue_ktile(smem_u32(sA + slot * kTc2AFloats), smem_u32(sB + slot * kTc2BFloats), tmem, fresh,
+                        fresh && kt > k0, (chunk - 1) & 1u, acc_empty, ends, acc_full);
+      __syncwarp();
+      if (lane == 0) tc2_commit_both(&empty[slot]);  // both CTAs may refill this stage
       if (++slot == kTc2Stages) { slot = 0; phase ^= 1u; }
       if (ends) ++chunk;
     }
