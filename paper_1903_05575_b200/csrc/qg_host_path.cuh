@@ -70,7 +70,7 @@ HostPlan<T> host_plan(int oa, int ob, int64_t M, int64_t N, int64_t K) {
   HostPlan<T> h;
   // FP64: each chunk's mainloop reads the staged operands in place (TMA-fed,
   // no pack launch, no packed buffers) where the device path would
-  h.direct = sizeof(T) == 8 && K > 0 && direct_feed<T>(oa, ob, M, N, K) != 0;
+  h.direct = K > 0 && direct_feed<T>(oa, ob, M, N, K) != 0;
   constexpr size_t qb = 4 * sizeof(T);
   const int64_t kq = Geo<T>::kq, rows = 128;  // panel width: multiple of both tile sizes (64, 128)
   h.small = use_small<T>(M, N, K);
@@ -310,10 +310,13 @@ int qgemm_host_impl(char transA, char transB, int64_t M, int64_t N, int64_t K, c
     };
     // one mainloop over columns [n0, n0 + nj) of this chunk into Cdj
     auto mainloop = [&](int64_t n0, int64_t nj, T *Cdj, const qg::Scalars<T> &s_) -> int {
-      if constexpr (sizeof(T) == 8) {
-        if (h.direct)
+      if (h.direct) {
+        if constexpr (sizeof(T) == 8)
           return launch_mainloop_direct(qg::kFeedTma, sa, lda_s, a_rc, a_cj, sb + 4 * (b_rc ? n0 : n0 * ldb_s),
                                         ldb_s, b_rc, b_cj, Cdj, M, M, nj, kc, s_, sk, S);
+        else
+          return launch_mainloop_direct_f32(sa, lda_s, a_rc, a_cj, sb + 4 * (b_rc ? n0 : n0 * ldb_s), ldb_s, b_rc,
+                                            b_cj, Cdj, M, M, nj, kc, s_, sk, S);
       }
       const T *pbj = pb + size_t(n0 / Geo<T>::rows) * size_t(ktn) * (Geo<T>::chunk / sizeof(T));
       return launch_mainloop(pa, pbj, Cdj, M, M, nj, ktn, s_, sk, S);

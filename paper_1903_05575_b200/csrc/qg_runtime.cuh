@@ -571,21 +571,90 @@ int encode_packed_2d(CUtensorMap *tm, const float *base, int64_t chunks, int box
   return r == CUDA_SUCCESS ? 0 : int(cudaErrorInvalidValue);
 }
 
-int launch_mainloop(const float *Ap, const float *Bp, float *C, int64_t ldc, int64_t M, int64_t N, int64_t KT,
-                    const qg::Scalars<float> &sc, void *sk_scratch, cudaStream_t st,
-                    int /*tri: FP64 only*/ = 0) {
+int tc32_set_attributes() {
   static std::atomic<bool> attr_set[kMaxDev];
   int dev = 0;
   if (cudaGetDevice(&dev) != cudaSuccess) return int(cudaErrorInvalidDevice);
-  if (dev >= kMaxDev || !attr_set[dev].load(std::memory_order_acquire)) {
-    cudaError_t e = cudaFuncSetAttribute(qg::qgemm_tc32_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         int(qg::kTcSmemBytes));
-    if (e == cudaSuccess)
-      e = cudaFuncSetAttribute(qg::qgemm_tc32_2cta_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                               int(qg::kTc2SmemBytes));
+  if (dev < kMaxDev && attr_set[dev].load(std::memory_order_acquire)) return 0;
+  cudaError_t e = cudaFuncSetAttribute(qg::qgemm_tc32_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       int(qg::kTcSmemBytes));
+  if (e == cudaSuccess)
+    e = cudaFuncSetAttribute(qg::qgemm_tc32_2cta_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             int(qg::kTc2SmemBytes));
+  if (e == cudaSuccess)
+    e = cudaFuncSetAttribute(qg::qgemm_tc32_2cta_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             int(qg::kTc2DSmemBytes));
+  if (e != cudaSuccess) return int(e);
+  if (dev < kMaxDev) attr_set[dev].store(true, std::memory_order_release);
+  return 0;
+}
+
+// Pair kernel launch (+ the split-K reduce) for a filled-in Tc2Args.
+template <bool kDirect>
+int launch_tc2(qg::Tc2Args &t, int64_t M, int64_t N, int64_t KT, void *sk_scratch, cudaStream_t st) {
+  // sk_scratch = [per-SM chunk slots][split-K partials] (sk_reserve<float>):
+  // fewer tile pairs than a wave -> split K, then one reduce + epilogue launch
+  t.kc = QG_TC2_CHUNK_KT;
+  t.tmp = static_cast<float *>(sk_scratch);
+  t.nslots = num_sms();
+  t.S = int(tc2_splits(M, N, KT));
+  t.part = reinterpret_cast<float *>(static_cast<char *>(sk_scratch) + tc2_slot_bytes());
+  const int64_t grid = 2 * t.MT2 * t.NT * t.S;
+  if (grid > INT32_MAX) return int(cudaErrorInvalidConfiguration);
+  { int ti = tstart(kMain, st);
+  qg::qgemm_tc32_2cta_kernel<kDirect><<<unsigned(grid), qg::kTcThreads,
+                                       kDirect ? qg::kTc2DSmemBytes : qg::kTc2SmemBytes, st>>>(t);
+  tstop(ti, st); }
+  ++g_last_launches;
+  if (t.S > 1) {
+    cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return int(e);
-    if (dev < kMaxDev) attr_set[dev].store(true, std::memory_order_release);
+    { int ti = tstart(kMain, st);
+    qg::tc2_reduce_kernel<<<dim3(unsigned(2 * t.MT2 * t.NT), qg::kTcBN / 16), qg::kTcBM, 0, st>>>(t);
+    tstop(ti, st); }
+    ++g_last_launches;
   }
+  return int(cudaGetLastError());
+}
+
+// Raw interleaved FP32 operand view for the direct pair kernel: rows
+// contiguous -> {4 R floats, K}, box 32 rows x 8 k (no swizzle); k contiguous
+// -> {4 K floats, R}, box 8 k x box_rows rows, 128-byte swizzle (conflict-free
+// converter reads; qg_tc32_2cta.cuh tc2_convert).
+int encode_raw_f32(CUtensorMap *tm, const float *X, int64_t ldx, int rc, int64_t R, int64_t K, int box_rows) {
+  EncodeTiledFn fn = encode_tiled();
+  if (!fn) return int(cudaErrorNotSupported);
+  const cuuint64_t dims[2] = {cuuint64_t(4 * (rc ? R : K)), cuuint64_t(rc ? K : R)};
+  const cuuint64_t strides[1] = {cuuint64_t(16) * cuuint64_t(ldx)};
+  const cuuint32_t box[2] = {rc ? 128u : 32u, rc ? cuuint32_t(qg::kTcBK) : cuuint32_t(box_rows)};
+  const cuuint32_t estr[2] = {1, 1};
+  const CUresult r = fn(tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float *>(X), dims, strides, box, estr,
+                        CU_TENSOR_MAP_INTERLEAVE_NONE, rc ? CU_TENSOR_MAP_SWIZZLE_NONE : CU_TENSOR_MAP_SWIZZLE_128B,
+                        CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS ? 0 : int(cudaErrorInvalidValue);
+}
+
+// FP32 direct path: op(A) / op(B) read in place (rc / cj as PackSpec), no pack
+// launch; K is one launch (the accumulation chunks bound the error, §6).
+int launch_mainloop_direct_f32(const float *A, int64_t lda, int a_rc, int a_cj, const float *B, int64_t ldb,
+                               int b_rc, int b_cj, float *C, int64_t ldc, int64_t M, int64_t N, int64_t K,
+                               const qg::Scalars<float> &sc, void *sk_scratch, cudaStream_t st) {
+  if (int e = tc32_set_attributes()) return e;
+  qg::Tc2Args t{};
+  t.C = C; t.ldc = ldc; t.M = M; t.N = N; t.sc = sc;
+  t.KT = cdiv(K, qg::kTcBK);
+  t.MT2 = cdiv(M, 2 * qg::kTcBM); t.NT = cdiv(N, qg::kTcBN);
+  t.a_rc = a_rc; t.a_cj = a_cj; t.b_rc = b_rc; t.b_cj = b_cj;
+  int rc = encode_raw_f32(&t.tmA, A, lda, a_rc, M, K, qg::kTcBM);
+  if (!rc) rc = encode_raw_f32(&t.tmB, B, ldb, b_rc, N, K, qg::kTcBN / 2);
+  if (rc) return rc;
+  return launch_tc2<true>(t, M, N, t.KT, sk_scratch, st);
+}
+
+int launch_mainloop(const float *Ap, const float *Bp, float *C, int64_t ldc, int64_t M, int64_t N, int64_t KT,
+                    const qg::Scalars<float> &sc, void *sk_scratch, cudaStream_t st,
+                    int /*tri: FP64 only*/ = 0) {
+  if (int e = tc32_set_attributes()) return e;
   if (QG_TC32_2CTA) {
     qg::Tc2Args t{};
     t.C = C; t.ldc = ldc; t.M = M; t.N = N; t.KT = KT; t.sc = sc;
@@ -593,28 +662,7 @@ int launch_mainloop(const float *Ap, const float *Bp, float *C, int64_t ldc, int
     int rc = encode_packed_2d(&t.tmA, Ap, 2 * t.MT2 * KT, 32);
     if (!rc) rc = encode_packed_2d(&t.tmB, Bp, t.NT * KT, 16);
     if (rc) return rc;
-    // sk_scratch = [per-SM chunk slots][split-K partials] (sk_reserve<float>):
-    // fewer tile pairs than a wave -> split K, then one reduce + epilogue launch
-    t.kc = QG_TC2_CHUNK_KT;
-    t.tmp = static_cast<float *>(sk_scratch);
-    t.nslots = num_sms();
-    t.S = int(tc2_splits(M, N, KT));
-    t.part = reinterpret_cast<float *>(static_cast<char *>(sk_scratch) + tc2_slot_bytes());
-    const int64_t grid = 2 * t.MT2 * t.NT * t.S;
-    if (grid > INT32_MAX) return int(cudaErrorInvalidConfiguration);
-    { int ti = tstart(kMain, st);
-    qg::qgemm_tc32_2cta_kernel<<<unsigned(grid), qg::kTcThreads, qg::kTc2SmemBytes, st>>>(t);
-    tstop(ti, st); }
-    ++g_last_launches;
-    if (t.S > 1) {
-      cudaError_t e = cudaGetLastError();
-      if (e != cudaSuccess) return int(e);
-      { int ti = tstart(kMain, st);
-      qg::tc2_reduce_kernel<<<dim3(unsigned(2 * t.MT2 * t.NT), qg::kTcBN / 16), qg::kTcBM, 0, st>>>(t);
-      tstop(ti, st); }
-      ++g_last_launches;
-    }
-    return int(cudaGetLastError());
+    return launch_tc2<false>(t, M, N, KT, sk_scratch, st);
   }
   qg::Tc32Args t;
   t.Ap = Ap; t.Bp = Bp; t.C = C; t.ldc = ldc; t.M = M; t.N = N;
@@ -638,8 +686,10 @@ int launch_mainloop(const float *Ap, const float *Bp, float *C, int64_t ldc, int
 // conflicts on a rows-contiguous op(A)) only up to 2^37 quaternion MACs.
 template <typename T>
 int direct_feed(int opA, int opB, int64_t M, int64_t N, int64_t K) {
-  if (sizeof(T) != 8) return 0;
   const int pol = g_path_policy.load(std::memory_order_relaxed);
+  // FP32 (tcgen05 pair kernel): raw tiles by TMA + the hi/lo split in shared
+  // memory for every shape and op pair; the pack launch only under policy 1
+  if (sizeof(T) != 8) return (pol == 0 || pol == 3 || pol == 4) ? 1 : 0;
   if (pol == 3 || pol == 4) return qg::kFeedTma;
   if (pol != 0) return 0;
   if (opA != 0) return qg::kFeedTma;

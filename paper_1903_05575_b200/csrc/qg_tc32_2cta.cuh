@@ -35,6 +35,16 @@ constexpr int kTc2AFloats = kTcChunkFloats;
 constexpr int kTc2BFloats = kTcChunkFloats / 2;
 constexpr size_t kTc2SmemBytes = size_t(kTc2Stages) * (kTc2ABytes + kTc2BBytes) + 256 + 1024;  // + barriers
 constexpr uint32_t kPeerBitMask = 0xFEFFFFFFu;  // shared::cluster address of the leader's copy
+// Direct feed (no pack launch): raw interleaved FP32 tiles by TMA into a raw
+// ring, split into the tf32 hi/lo planes by two converter warps per CTA.
+constexpr int kTc2DStages = 3;                       // plane stages (the MMA's ring)
+constexpr int kTc2RawStages = 3;                     // raw stages
+constexpr uint32_t kTc2RawABytes = kTcBM * kTcBK * 16;      // 16 KB: 128 rows x 8 k quaternions
+constexpr uint32_t kTc2RawBBytes = kTcBM / 2 * kTcBK * 16;  // 8 KB: 64 columns x 8 k
+constexpr size_t kTc2DSmemBytes =
+    size_t(kTc2DStages) * (kTc2ABytes + kTc2BBytes) + size_t(kTc2RawStages) * (kTc2RawABytes + kTc2RawBBytes) +
+    256 + 1024;
+static_assert(kTc2DSmemBytes <= 232448, "direct FP32 pair kernel exceeds 227 KB of shared memory");
 
 struct alignas(64) Tc2Args {
   CUtensorMap tmA;   // packed A viewed as [rows of 256 floats]; a chunk = 32 rows
@@ -44,6 +54,10 @@ struct alignas(64) Tc2Args {
   Scalars<float> sc;
   int S;             // K splits per tile pair (1: the epilogue updates C)
   float *part;       // S > 1: raw accumulators, kTc2PartFloats per CTA, summed by tc2_reduce_kernel
+  // direct feed: tmA / tmB are 2-D maps of the user's interleaved op(A) / op(B)
+  // (rc: rows contiguous -> {4 R floats, K}, boxes of 32 rows x 8 k; else
+  // {4 K floats, R}, one box of all rows x 8 k, 128-byte swizzle); cj: op H
+  int a_rc, b_rc, a_cj, b_cj;
   int kc;            // k-tiles per TMEM accumulation chunk (promotion, see below)
   float *tmp;        // chunk promotion: one kTc2PartFloats slot per SM id (%smid) ...
   int nslots;        // ... for SM ids < nslots
@@ -155,6 +169,52 @@ __device__ __forceinline__ void tc2_commit_both(uint64_t *bar) {
 // next to the chunk epilogue's register arrays, ptxas moved the descriptors out
 // of uniform registers -- an R2UR per operand per MMA -- and the single issuing
 // thread fell behind the pipe: c3 FP32 67 vs 61 ms with chunks off.)
+// 2-D TMA tile load into this CTA's smem completing on its own barrier.
+__device__ __forceinline__ void tma_load_2d_local(void *dst, const CUtensorMap *tm, int c0, int c1, uint64_t *bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], "
+      "[%4];\n" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(tm)), "r"(c0), "r"(c1), "r"(smem_u32(bar))
+      : "memory");
+}
+
+// Split one raw tile (R rows x 8 k quaternions, as the direct feed's TMA left
+// it) into the 8 tf32 planes [p][hi, lo] of the canonical K-major layout the
+// MMA descriptors expect -- the pack kernel's arithmetic (conj, x_hi =
+// tf32(x), x_lo = tf32(x - x_hi), qg_tc32.cuh), done in shared memory.
+// Thread items: (row r, k quad kq); rows contiguous: raw (r, k, c) at
+// ((r / 32) * 8 + k) * 128 + (r % 32) * 4 + c floats; k contiguous (128-byte
+// swizzled rows of 8 quaternions): r * 32 + ((k ^ (r % 8)) * 4) + c.
+template <int R>
+__device__ __forceinline__ void tc2_convert(const float *raw, float *planes, int rc, int cj, int t, int nt) {
+  constexpr int kPlane = R * kTcBK;  // floats per plane
+  const float sg = cj ? -1.f : 1.f;
+  for (int item = t; item < 2 * R; item += nt) {
+    const int r = item % R, kq = item / R;
+    float4 q[4];
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const int k = 4 * kq + e;
+      const int off = rc ? ((r >> 5) * 8 + k) * 128 + (r & 31) * 4 : r * 32 + ((k ^ (r & 7)) << 2);
+      q[e] = *reinterpret_cast<const float4 *>(raw + off);
+    }
+    const int poff = (r >> 3) * 64 + kq * 32 + (r & 7) * 4;
+#pragma unroll
+    for (int p = 0; p < 4; ++p) {
+      float x[4], hi[4], lo[4];
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const float v = p == 0 ? q[e].x : p == 1 ? q[e].y : p == 2 ? q[e].z : q[e].w;
+        x[e] = p == 0 ? v : sg * v;
+        hi[e] = tf32_rna(x[e]);
+        lo[e] = tf32_rna(x[e] - hi[e]);
+      }
+      *reinterpret_cast<float4 *>(planes + (p * 2 + 0) * kPlane + poff) = make_float4(hi[0], hi[1], hi[2], hi[3]);
+      *reinterpret_cast<float4 *>(planes + (p * 2 + 1) * kPlane + poff) = make_float4(lo[0], lo[1], lo[2], lo[3]);
+    }
+  }
+}
+
 __device__ __forceinline__ bool elect_one() {
   uint32_t pred;
   asm volatile("{\n.reg .pred p;\nelect.sync _|p, 0xffffffff;\nselp.u32 %0, 1, 0, p;\n}\n" : "=r"(pred));
@@ -241,17 +301,26 @@ __device__ __forceinline__ void tc2_fold(const Tc2Args &args, float *part, int64
   }
 }
 
+// kDirect: operands read in place from the user's storage (raw TMA ring +
+// converter warps 2-3); else from the pack kernel's chunks.
+template <bool kDirect>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kTcThreads, 1)
     qgemm_tc32_2cta_kernel(const __grid_constant__ Tc2Args args) {
+  constexpr int P = kDirect ? kTc2DStages : kTc2Stages;  // plane stages
+  constexpr int RS = kTc2RawStages;
   extern __shared__ __align__(128) unsigned char smem_dyn[];
   unsigned char *smem = smem_dyn + ((1024u - (smem_u32(smem_dyn) & 1023u)) & 1023u);
   float *sA = reinterpret_cast<float *>(smem);
-  float *sB = sA + kTc2Stages * kTc2AFloats;
-  uint64_t *full = reinterpret_cast<uint64_t *>(sB + kTc2Stages * kTc2BFloats);  // leader's counts both CTAs
-  uint64_t *empty = full + kTc2Stages;
-  uint64_t *acc_full = empty + kTc2Stages;  // [4] component c of a chunk complete (both CTAs, multicast)
-  uint64_t *acc_empty = acc_full + 4;       // [4] leader: component c of TMEM drained by both CTAs
-  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(acc_empty + 4);
+  float *sB = sA + P * kTc2AFloats;
+  float *rA = sB + P * kTc2BFloats;                                   // direct: raw A tiles
+  float *rB = rA + (kDirect ? RS * kTc2RawABytes / 4 : 0);            // direct: raw B halves
+  uint64_t *full = reinterpret_cast<uint64_t *>(rB + (kDirect ? RS * kTc2RawBBytes / 4 : 0));  // leader's
+  uint64_t *empty = full + P;
+  uint64_t *acc_full = empty + P;     // [4] component c of a chunk complete (both CTAs, multicast)
+  uint64_t *acc_empty = acc_full + 4; // [4] leader: component c of TMEM drained by both CTAs
+  uint64_t *raw_full = acc_empty + 4; // direct [RS]: raw tile landed (TMA bytes)
+  uint64_t *raw_empty = raw_full + RS;  // direct [RS]: converters done with the raw tile
+  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(raw_empty + RS);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t rank = cluster_rank();
@@ -266,10 +335,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kTcThreads, 1)
   const int64_t k0 = ks * KT / args.S, k1 = (ks + 1) * KT / args.S;
 
   if (threadIdx.x == 0) {
-    for (int s = 0; s < kTc2Stages; ++s) {
-      mbar_init(&full[s], 1);
+    for (int s = 0; s < P; ++s) {
+      mbar_init(&full[s], kDirect ? 4 : 1);  // direct: 2 converter warps x 2 CTAs arrive
       mbar_init(&empty[s], 1);
     }
+    if (kDirect)
+      for (int s = 0; s < RS; ++s) {
+        mbar_init(&raw_full[s], 1);
+        mbar_init(&raw_empty[s], 2);
+      }
     for (int c = 0; c < 4; ++c) mbar_init(&acc_full[c], 1);
     for (int c = 0; c < 4; ++c) mbar_init(&acc_empty[c], 8);  // 4 epilogue warps x 2 CTAs
     fence_mbar_init();
@@ -289,11 +363,49 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kTcThreads, 1)
     int slot = 0;
     uint32_t phase = 0;
     for (int64_t kt = k0; kt < k1; ++kt) {
-      if (kt - k0 >= kTc2Stages) mbar_wait_guarded(&empty[slot], phase ^ 1u);
-      if (rank == 0) mbar_arrive_expect_tx(&full[slot], 2 * (kTc2ABytes + kTc2BBytes));
-      tma2_load_2d(sA + slot * kTc2AFloats, &args.tmA, 0, int((mt * KT + kt) * 32), &full[slot]);
-      tma2_load_2d(sB + slot * kTc2BFloats, &args.tmB, 0, int((pn * KT + kt) * 32 + rank * 16), &full[slot]);
-      if (++slot == kTc2Stages) { slot = 0; phase ^= 1u; }
+      if constexpr (kDirect) {
+        // raw interleaved tiles of this CTA's 128 rows of op(A) and 64 columns of op(B)
+        if (kt - k0 >= RS) mbar_wait_guarded(&raw_empty[slot], phase ^ 1u);
+        mbar_arrive_expect_tx(&raw_full[slot], kTc2RawABytes + kTc2RawBBytes);
+        float *ra = rA + slot * (kTc2RawABytes / 4), *rb = rB + slot * (kTc2RawBBytes / 4);
+        const int ka = int(kt * kTcBK), r0 = int(mt * kTcBM), n0 = int(pn * kTcBN + rank * (kTcBN / 2));
+        if (args.a_rc)
+          for (int j = 0; j < kTcBM / 32; ++j)
+            tma_load_2d_local(ra + j * (32 * 4 * kTcBK), &args.tmA, 4 * (r0 + 32 * j), ka, &raw_full[slot]);
+        else
+          tma_load_2d_local(ra, &args.tmA, 4 * ka, r0, &raw_full[slot]);
+        if (args.b_rc)
+          for (int j = 0; j < kTcBN / 64; ++j)
+            tma_load_2d_local(rb + j * (32 * 4 * kTcBK), &args.tmB, 4 * (n0 + 32 * j), ka, &raw_full[slot]);
+        else
+          tma_load_2d_local(rb, &args.tmB, 4 * ka, n0, &raw_full[slot]);
+        if (++slot == RS) { slot = 0; phase ^= 1u; }
+      } else {
+        if (kt - k0 >= P) mbar_wait_guarded(&empty[slot], phase ^ 1u);
+        if (rank == 0) mbar_arrive_expect_tx(&full[slot], 2 * (kTc2ABytes + kTc2BBytes));
+        tma2_load_2d(sA + slot * kTc2AFloats, &args.tmA, 0, int((mt * KT + kt) * 32), &full[slot]);
+        tma2_load_2d(sB + slot * kTc2BFloats, &args.tmB, 0, int((pn * KT + kt) * 32 + rank * 16), &full[slot]);
+        if (++slot == P) { slot = 0; phase ^= 1u; }
+      }
+    }
+  } else if (kDirect && (warp == 2 || warp == 3)) {
+    // ---------------- converters (both CTAs): raw tile -> tf32 hi / lo planes ----------------
+    int rs = 0, ps = 0;
+    uint32_t rph = 0, pph = 0;
+    const int t = threadIdx.x - 64;
+    for (int64_t kt = k0; kt < k1; ++kt) {
+      mbar_wait_guarded(&raw_full[rs], rph);
+      if (kt - k0 >= P) mbar_wait_guarded(&empty[ps], pph ^ 1u);  // the MMAs have read this plane stage
+      tc2_convert<kTcBM>(rA + rs * (kTc2RawABytes / 4), sA + ps * kTc2AFloats, args.a_rc, args.a_cj, t, 64);
+      tc2_convert<kTcBM / 2>(rB + rs * (kTc2RawBBytes / 4), sB + ps * kTc2BFloats, args.b_rc, args.b_cj, t, 64);
+      asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");  // generic writes -> the MMA's reads
+      __syncwarp();
+      if (lane == 0) {
+        mbar_arrive(&raw_empty[rs]);
+        mbar_arrive_cluster(&full[ps], 0);  // the leader's stage barrier (both CTAs' planes ready)
+      }
+      if (++rs == RS) { rs = 0; rph ^= 1u; }
+      if (++ps == P) { ps = 0; pph ^= 1u; }
     }
   } else if (warp == 1 && rank == 0) {
     // ---------------- MMA issuer (leader only) ----------------
@@ -308,14 +420,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kTcThreads, 1)
       const bool fresh = kk == 0;                         // first k-tile of an accumulation chunk
       const bool ends = kk == kc - 1 || kt + 1 == k1;     // last k-tile of a chunk
       if (++kk == kc) kk = 0;
-      mbar_wait_guarded(&full[slot], phase);
+      if (kDirect) mbar_wait_cluster(&full[slot], phase);  // converters of both CTAs (release.cluster)
+      else mbar_wait_guarded(&full[slot], phase);
       tc_fence_after();
       if (elect_one())
         tc2_issue_ktile(smem_u32(sA + slot * kTc2AFloats), smem_u32(sB + slot * kTc2BFloats), tmem, fresh,
                         fresh && kt > k0, (chunk - 1) & 1u, acc_empty, ends, acc_full);
       __syncwarp();
       if (lane == 0) tc2_commit_both(&empty[slot]);  // both CTAs may refill this stage
-      if (++slot == kTc2Stages) { slot = 0; phase ^= 1u; }
+      if (++slot == P) { slot = 0; phase ^= 1u; }
       if (ends) ++chunk;
     }
   } else if (warp >= 4) {

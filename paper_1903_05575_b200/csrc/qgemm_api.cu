@@ -61,13 +61,15 @@ int qgemm_impl(char transA, char transB, int64_t M, int64_t N, int64_t K, const 
   if (use_small<T>(M, N, K))  // one launch, no workspace (NEXT item 4)
     return launch_small<T>(A, lda, pa.row_contig, pa.conj, B, ldb, pb.row_contig, pb.conj, C, ldc, M, N, K,
                            alpha, beta, st);
-  if constexpr (sizeof(T) == 8) {
-    if (const int feed = direct_feed<T>(sh.oa, sh.ob, M, N, K)) {  // one launch; workspace = stream-K scratch
-      if (workspace == nullptr || (reinterpret_cast<uintptr_t>(workspace) & 255u)) return -14;
-      if (workspace_bytes < sk_reserve<T>(M, N, cdiv(K, Geo<T>::kq))) return -15;
+  if (const int feed = direct_feed<T>(sh.oa, sh.ob, M, N, K)) {  // one launch; workspace = scratch only
+    if (workspace == nullptr || (reinterpret_cast<uintptr_t>(workspace) & 255u)) return -14;
+    if (workspace_bytes < sk_reserve<T>(M, N, cdiv(K, Geo<T>::kq))) return -15;
+    if constexpr (sizeof(T) == 8)
       return launch_mainloop_direct(feed, A, lda, pa.row_contig, pa.conj, B, ldb, pb.row_contig, pb.conj, C,
                                     ldc, M, N, K, sc, workspace, st);
-    }
+    else
+      return launch_mainloop_direct_f32(A, lda, pa.row_contig, pa.conj, B, ldb, pb.row_contig, pb.conj, C, ldc, M,
+                                        N, K, sc, workspace, st);
   }
   return panel_loop<T>(pa, pb, M, N, K, sc, C, ldc, workspace, workspace_bytes, st, 0);
 }

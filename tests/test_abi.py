@@ -163,15 +163,15 @@ def test_path_policy_setter(lib):
 
 
 def test_direct_path_workspace_is_stream_k_scratch(lib):
-    """Policy 3 (direct): the pack is fused into the FP64 mainloop, so the
-    workspace is the stream-K scratch only (256 partial slots of 128 KiB + 512
-    arrival counters); FP32 keeps the packed sizes."""
+    """Policy 3 (direct): the pack is fused into the mainloops, so the workspace
+    is the FP64 stream-K scratch only (256 partial slots of 128 KiB + 512
+    arrival counters), resp. the FP32 pair kernel's accumulation-chunk slots."""
     sk = 256 * 131072 + 2048
     for pol in (3,):
         lib.qgemm_set_path_policy(pol)
         assert lib.qgemm_workspace_bytes(b"N", b"H", 8192, 8192, 8192, 0) == sk
         assert lib.qgemm_workspace_min_bytes(b"N", b"H", 8192, 8192, 8192, 0) == sk
-        assert lib.qgemm_workspace_bytes(b"N", b"H", 8192, 8192, 8192, 1) == 2 * 8192 * 8192 * 32 + F32_SLOTS
+        assert lib.qgemm_workspace_bytes(b"N", b"H", 8192, 8192, 8192, 1) == F32_SLOTS
         assert lib.qherk_workspace_bytes(b"L", b"N", 32768, 256) == sk
     lib.qgemm_set_path_policy(1)  # packed
     assert lib.qherk_workspace_bytes(b"L", b"N", 32768, 256) > sk
@@ -235,14 +235,17 @@ def test_host_workspace_c3_plan(lib):
 
 
 @pytest.mark.parametrize("N", [8192, 1024])
-def test_host_workspace_f32_covers_every_panel_split(lib, N):
-    """qgemm_host_f32 (packed FP32 chunks, M = K = 8192): the last chunk runs per
-    column panel and its last panel in 128-column pieces; a 128-wide piece has
-    32 tile pairs (< one wave of 74) and splits K twice, so the plan must reserve
-    its split-K partials (32 pairs x 2 splits x 512 KiB = 32 MiB) even though the
-    full width and the panel width do not split.  (The reserve used to cover only
-    the full and the panel width: an out-of-bounds write of 32 MiB.)"""
-    lib.qgemm_set_path_policy(0)
+@pytest.mark.parametrize("policy", [1, 0], ids=["packed", "direct"])
+def test_host_workspace_f32_covers_every_panel_split(lib, N, policy):
+    """qgemm_host_f32 (M = K = 8192): the last chunk runs per column panel and
+    its last panel in 128-column pieces; a 128-wide piece has 32 tile pairs
+    (< one wave of 74) and splits K twice, so the plan must reserve its split-K
+    partials (32 pairs x 2 splits x 512 KiB = 32 MiB) even though the full width
+    and the panel width do not split.  (The reserve used to cover only the full
+    and the panel width: an out-of-bounds write of 32 MiB.)  Packed chunks
+    (policy 1) also hold 2 packed chunks per operand; the direct chunks (auto)
+    are read in place from the staging slots."""
+    lib.qgemm_set_path_policy(policy)
     M = K = 8192
     qb = 16
     kc = 4096                                    # chunks 256, 1024, 2048, 768, 4096
@@ -250,8 +253,9 @@ def test_host_workspace_f32_covers_every_panel_split(lib, N):
     ktc = kc // 8                                # FP32 k-tiles per chunk (8 k per tile)
     packed = 2 * (2 * (M // 256)) * ktc * 32768 + 2 * (N // 128) * ktc * 32768
     part = 32 * 2 * 2 * 65536 * 4                # pairs x S x 2 CTAs x 4x128x128 floats
-    want = 2 * M * N * qb + stage + packed + F32_SLOTS + part
+    want = 2 * M * N * qb + stage + (packed if policy == 1 else 0) + F32_SLOTS + part
     assert lib.qgemm_host_workspace_bytes(b"N", b"H", M, N, K, 1) == want
+    lib.qgemm_set_path_policy(1)
 
 
 @pytest.mark.parametrize("args,code", [

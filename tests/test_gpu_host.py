@@ -74,10 +74,17 @@ def test_host_ragged_k_direct_chunks(opA, opB):
     assert_parity(pr, run_host(pr), oracle_full(pr), exact=True)
 
 
+@pytest.mark.parametrize("policy", [qg.PATH_AUTO, qg.PATH_PACKED], ids=["auto_direct", "packed"])
 @pytest.mark.parametrize("opA,opB", [("N", "H"), ("T", "N"), ("H", "T")])
-def test_host_f32_chunked(opA, opB):
+def test_host_f32_chunked(opA, opB, policy):
+    """FP32 from host memory: staged K-chunks read in place by the direct pair
+    kernel (auto) or packed per chunk (policy 1)."""
     pr = make_problem(260, 700, 900, opA, opB, QALPHA, QBETA, seed=22, dist="normal")
-    assert_parity(pr, run_host(pr, "f32"), oracle_full(pr), precision="f32")
+    with path_policy(policy):
+        assert_parity(pr, run_host(pr, "f32"), oracle_full(pr), precision="f32")
+    pr = make_problem(260, 700, 900, opA, opB, (2, -1, 0, 3), (1, 0, -2, 1), seed=26, dist="int2")
+    with path_policy(policy):
+        assert_parity(pr, run_host(pr, "f32"), oracle_full(pr), exact=True)
 
 
 def test_host_beta_zero_nan_c_and_single_chunk():

@@ -100,11 +100,14 @@ def test_group4_tma_feed(M, N, K, pad, opA, opB):
 
 @pytest.mark.parametrize("M,N,K", [(300, 260, 700), (512, 512, 64), (1000, 130, 4000), (257, 129, 33)])
 @pytest.mark.parametrize("opA,opB", [("N", "H"), ("T", "N"), ("H", "T")])
-def test_f32_split_k_pair_kernel(M, N, K, opA, opB):
+@pytest.mark.parametrize("policy", [qg.PATH_PACKED, qg.PATH_DIRECT], ids=["packed", "direct"])
+def test_f32_split_k_pair_kernel(M, N, K, opA, opB, policy):
     """FP32 tcgen05 pair kernel with fewer tile pairs than a wave: K split over
     up to 8 clusters per tile pair, raw partials summed by the reduce + epilogue
-    launch.  Tolerance on normal inputs; bitwise on exact-integer inputs."""
-    with path_policy(qg.PATH_PACKED):
+    launch (1000 x 130 x 4000: several accumulation chunks per split).  Packed
+    chunks, and the direct feed (raw tiles by TMA, hi/lo split by the converter
+    warps).  Tolerance on normal inputs; bitwise on exact-integer inputs."""
+    with path_policy(policy):
         pr = make_problem(M, N, K, opA, opB, QALPHA, QBETA, seed=13, dist="normal")
         assert_parity(pr, run_gpu(pr, "f32"), oracle_full(pr), precision="f32")
         pr = make_problem(M, N, K, opA, opB, (1, 0, 0, 0), (-1, 0, 0, 0), seed=14, dist="int2")
