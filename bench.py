@@ -103,6 +103,8 @@ def parse():
     ap.add_argument("--no-configs", action="store_true", help="skip the c1/c2/c4/Fig. 4 lines")
     ap.add_argument("--no-sharded", action="store_true", help="skip the c4/c5 sharded variants")
     ap.add_argument("--no-parity", action="store_true", help="skip the oracle checks")
+    ap.add_argument("--policy", type=int, default=0,
+                    help="library path policy for A/B measurements (qgemm_set_path_policy; 0 = auto)")
     return ap.parse_args()
 
 
@@ -781,6 +783,8 @@ def run_ours(args):
 
     ctx = Ctx(args)
     world, rank, dev = ctx.world, ctx.rank, ctx.dev
+    if args.policy:
+        qg.set_path_policy(args.policy)
     n = args.n
     M_total = n * world
     r0, r1 = rows_for_rank(M_total, world, rank) if world > 1 else (0, n)
