@@ -216,7 +216,9 @@ int qgemm_pack_panel(char trans, int operand, int64_t R, int64_t K, const double
  * path (pack launch + persistent mainloop), 2 = always the one-launch small
  * kernel, 3 = direct (FP64: the persistent mainloop fed by TMA straight from
  * the interleaved storage -- one launch, no pack, workspace = stream-K scratch
- * only; FP32 calls take the packed path), 4 = direct restricted to the
+ * only; FP32: the tcgen05 pair kernel fed with raw tiles by TMA and split into
+ * tf32 hi/lo planes in shared memory -- no pack launch, workspace = the
+ * accumulation-chunk slots and split-K partials), 4 = direct restricted to the
  * 32-byte-swizzle tile feed (3 and auto load both operands as conflict-free
  * 4-quaternion-group tiles when the groups are whole: M, resp. N, a multiple
  * of 4 for op(A) = A, resp. op(B) = B^T / B^H, else K), 5 = as 2 but never the
@@ -225,7 +227,10 @@ int qgemm_pack_panel(char trans, int operand, int64_t R, int64_t K, const double
  * crossover; above it FP64 takes the direct path whenever the group tiles
  * apply (op(A) = A: M % 4 == 0 and N % 4 (op(B) = B^T/B^H) resp. K % 4 == 0),
  * when op(A) is T/H, and otherwise up to M*N*K <= 2^37; else packed; FP32
- * packed (the tcgen05 pair kernel, split over K below one wave).
+ * packed (pack launch + the tcgen05 pair kernel, split over K below one wave:
+ * faster than the direct feed, whose in-SM split saturates shared memory;
+ * DESIGN.md §6).  FP32 on the tensor cores accumulates K in chunks of 256
+ * added with round-to-nearest (the tensor core's own accumulation truncates).
  * Returns the previous policy, or -1 (policy unchanged) for other values.
  * For tests and benchmarks; the result is correct under every policy. */
 int qgemm_set_path_policy(int policy);

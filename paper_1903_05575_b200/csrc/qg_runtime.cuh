@@ -687,9 +687,12 @@ int launch_mainloop(const float *Ap, const float *Bp, float *C, int64_t ldc, int
 template <typename T>
 int direct_feed(int opA, int opB, int64_t M, int64_t N, int64_t K) {
   const int pol = g_path_policy.load(std::memory_order_relaxed);
-  // FP32 (tcgen05 pair kernel): raw tiles by TMA + the hi/lo split in shared
-  // memory for every shape and op pair; the pack launch only under policy 1
-  if (sizeof(T) != 8) return (pol == 0 || pol == 3 || pol == 4) ? 1 : 0;
+  // FP32 (tcgen05 pair kernel): the direct feed (raw tiles by TMA + the hi/lo
+  // split in shared memory) only under policies 3 / 4.  Auto keeps the pack
+  // launch: the in-SM split adds 48 KB of shared-memory traffic per stage to the
+  // MMAs' ~290 KB and the SM's shared-memory port saturates -- c3 FP32 86.6 vs
+  // 75.4 ms (pack + mainloop), tensor pipe 69% vs 92% active (ncu), DESIGN.md §6
+  if (sizeof(T) != 8) return (pol == 3 || pol == 4) ? 1 : 0;
   if (pol == 3 || pol == 4) return qg::kFeedTma;
   if (pol != 0) return 0;
   if (opA != 0) return qg::kFeedTma;

@@ -235,7 +235,7 @@ def test_host_workspace_c3_plan(lib):
 
 
 @pytest.mark.parametrize("N", [8192, 1024])
-@pytest.mark.parametrize("policy", [1, 0], ids=["packed", "direct"])
+@pytest.mark.parametrize("policy", [1, 3], ids=["packed", "direct"])
 def test_host_workspace_f32_covers_every_panel_split(lib, N, policy):
     """qgemm_host_f32 (M = K = 8192): the last chunk runs per column panel and
     its last panel in 128-column pieces; a 128-wide piece has 32 tile pairs
@@ -243,8 +243,8 @@ def test_host_workspace_f32_covers_every_panel_split(lib, N, policy):
     partials (32 pairs x 2 splits x 512 KiB = 32 MiB) even though the full width
     and the panel width do not split.  (The reserve used to cover only the full
     and the panel width: an out-of-bounds write of 32 MiB.)  Packed chunks
-    (policy 1) also hold 2 packed chunks per operand; the direct chunks (auto)
-    are read in place from the staging slots."""
+    (policy 1, and auto for FP32) also hold 2 packed chunks per operand; the
+    direct chunks (policy 3) are read in place from the staging slots."""
     lib.qgemm_set_path_policy(policy)
     M = K = 8192
     qb = 16

@@ -74,11 +74,11 @@ def test_host_ragged_k_direct_chunks(opA, opB):
     assert_parity(pr, run_host(pr), oracle_full(pr), exact=True)
 
 
-@pytest.mark.parametrize("policy", [qg.PATH_AUTO, qg.PATH_PACKED], ids=["auto_direct", "packed"])
+@pytest.mark.parametrize("policy", [qg.PATH_DIRECT, qg.PATH_AUTO], ids=["direct", "auto_packed"])
 @pytest.mark.parametrize("opA,opB", [("N", "H"), ("T", "N"), ("H", "T")])
 def test_host_f32_chunked(opA, opB, policy):
     """FP32 from host memory: staged K-chunks read in place by the direct pair
-    kernel (auto) or packed per chunk (policy 1)."""
+    kernel (policy 3) or packed per chunk (auto)."""
     pr = make_problem(260, 700, 900, opA, opB, QALPHA, QBETA, seed=22, dist="normal")
     with path_policy(policy):
         assert_parity(pr, run_host(pr, "f32"), oracle_full(pr), precision="f32")
