@@ -16,7 +16,11 @@ RAW = ("gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum"
        "sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active",
        "sm__inst_executed_pipe_fp64.avg.pct_of_peak_sustained_active",
        "sm__pipe_tensor_op_dmma_cycles_active.avg.pct_of_peak_sustained_active",
-       "sm__pipe_tc_cycles_active.avg.pct_of_peak_sustained_active")
+       "sm__pipe_tc_cycles_active.avg.pct_of_peak_sustained_active",
+       "sm__inst_executed_pipe_tensor_subpipe_dmma.avg.pct_of_peak_sustained_active",
+       "sm__ops_path_tensor_src_fp64.sum", "sm__ops_path_tensor_src_fp64.sum.pct_of_peak_sustained_elapsed",
+       "sm__ops_path_tensor_src_fp64.sum.per_second",
+       "TPC.TriageCompute.sm__pipe_tensor_cycles_active_realtime.avg.pct_of_peak_sustained_elapsed")
 
 
 def run(args):
