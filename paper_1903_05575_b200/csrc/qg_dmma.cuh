@@ -578,18 +578,6 @@ __global__ void __launch_bounds__(kDmmaThreads, 1) qgemm_dmma_kernel(const __gri
   Unit u;
   [[maybe_unused]] int tr_n = 0;
   QG_TR(1);
-  // Epilogue skew (per-lane epilogues only): the two consumer warps of each SM
-  // sub-partition (w and w + 4) run the same tiles; with warps 4-7 started
-  // about one epilogue later, one of them is in its k-loop, issuing DMMAs,
-  // while the other stores its C tile -- instead of the pipe idling while all
-  // eight store at once.  Nothing re-synchronises the two sets (the per-lane
-  // epilogue has no CTA barrier; the ring lets them drift up to its depth), so
-  // the offset persists across the persistent grid's tiles.  The ring epilogue
-  // synchronises all consumers at every tile and gains nothing.
-#ifndef QG_EPI_SKEW_NS
-#define QG_EPI_SKEW_NS 0
-#endif
-  if (QG_EPI_SKEW_NS > 0 && warp >= 4 && !(kRing && args.c_ring)) __nanosleep(QG_EPI_SKEW_NS);
   while (it.next(args, u)) {
     QG_TR(2);
     double acc[4][2][4][2];
