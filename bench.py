@@ -383,8 +383,19 @@ def measure_other_configs(warmup):
         for _ in range(32):
             qg.qgemm("N", "N", 1.0, A, B, 0.0, C)
     ms32 = _graphed(c1_32, reps=50, warmup=warmup) / 32
+    x = torch.zeros(1, device=dev)
+    floor1 = _graphed(lambda: x.add_(1.0), warmup=warmup)
+
+    def triv32():
+        for _ in range(32):
+            x.add_(1.0)
+    floor32 = _graphed(triv32, reps=50, warmup=warmup) / 32
     out["c1"] = {"workload": "c1: 64^3 N/N alpha=1 beta=0", "us_per_call": ms * 1e3,
                  "us_per_call_back_to_back": ms32 * 1e3,
+                 "trivial_kernel_us": floor1 * 1e3, "trivial_kernel_back_to_back_us": floor32 * 1e3,
+                 "dmma_time_us": 64 * 16 / 1.965e3,  # 64 DMMAs per SM sub-partition at 16 cycles each
+                 "note": "latency-bound: 64 output tiles on 64 SMs; floor = a trivial one-element torch "
+                         "kernel replayed the same way",
                  "tflops": 32.0 * 64 ** 3 / (ms * 1e-3) / 1e12, "launches_per_call": launches,
                  "timing": "CUDA-graph replay: one call per graph, and 32 calls per graph"}
     n, ld = 1024, 1040
