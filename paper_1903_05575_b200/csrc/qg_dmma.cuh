@@ -63,12 +63,6 @@ constexpr int kConsumerRegs = 232;
 #ifndef QG_C_PREFETCH_BULK
 #define QG_C_PREFETCH_BULK 1  // 1: the producer lane bulk-prefetches C tiles; 0: consumer lanes prefetch per quaternion
 #endif
-#ifndef QG_C_ST256
-#define QG_C_ST256 0  // per-lane epilogue: one 256-bit store per quaternion (else two 128-bit)
-#endif
-#ifndef QG_C_LD256
-#define QG_C_LD256 0  // per-lane epilogue: one 256-bit load per quaternion of C
-#endif
 #ifndef QG_C_PREFETCH_KT
 #define QG_C_PREFETCH_KT 2  // k-tiles before the end of a tile at which its C tile is prefetched to L2
 #endif
@@ -131,7 +125,6 @@ struct alignas(64) DmmaArgs {
   CUtensorMap tmC;       // QG_C_RING: C as (component, column, row), box 4 x 64 x 16, 32-byte swizzle
   int c_ring;            // host: C tiles through the ring for this launch (see launch_dmma)
   int c_remote;          // host: C is not in this GPU's memory (multi-GPU epilogue stores): no L2 prefetch of C
-  int c_al32;            // host: C is 32-byte aligned (whole-quaternion 256-bit accesses possible)
   const double *Ap;  // packed path: packed A panel, MT x KT chunks
   const double *Bp;  // packed path: packed B panel, NT x KT chunks
   // TMA feed: op(A) / op(B) read in place as R x K views -- X~(r, k) at
@@ -811,18 +804,7 @@ __global__ void __launch_bounds__(kDmmaThreads, 1) qgemm_dmma_kernel(const __gri
             ok[i2][jj][e] = row < args.M && col < args.N &&
                             (args.tri == 0 || (args.tri == 1 ? row >= col : row <= col));
             cp[i2][jj][e] = args.C + 4 * (row + col * args.ldc);
-            if (!args.sc.beta_zero && ok[i2][jj][e]) {
-#if QG_C_LD256
-              if (args.c_al32) {
-                double *q = cold[i2][jj][e];
-                asm volatile("ld.global.v4.f64 {%0, %1, %2, %3}, [%4];\n"
-                             : "=d"(q[0]), "=d"(q[1]), "=d"(q[2]), "=d"(q[3])
-                             : "l"(cp[i2][jj][e])
-                             : "memory");
-              } else
-#endif
-                ldq_c(cp[i2][jj][e], cold[i2][jj][e]);
-            }
+            if (!args.sc.beta_zero && ok[i2][jj][e]) ldq_c(cp[i2][jj][e], cold[i2][jj][e]);
           }
       QG_TR_DEP(7 + h, cold[0][0][0][0]);  // batch h's first C load has landed
 #pragma unroll
@@ -848,14 +830,6 @@ __global__ void __launch_bounds__(kDmmaThreads, 1) qgemm_dmma_kernel(const __gri
               const int64_t col = nt * kBR + (wn * 2 + jj) * 8 + 2 * (lane & 3) + e;
               if (row == col) out[1] = out[2] = out[3] = 0.0;
             }
-#if QG_C_ST256
-            if (args.c_al32) {  // whole 32-byte sector per store: no partial-sector merge in L2
-              asm volatile("st.global.v4.f64 [%0], {%1, %2, %3, %4};\n" ::"l"(cp[i2][jj][e]), "d"(out[0]),
-                           "d"(out[1]), "d"(out[2]), "d"(out[3])
-                           : "memory");
-              continue;
-            }
-#endif
             stq(cp[i2][jj][e], out);
           }
     }

@@ -474,7 +474,6 @@ int launch_dmma(qg::DmmaArgs &a, DmmaKernel kernel, bool direct, void *sk_scratc
   const bool query = (direct && QG_C_RING) || !a.sc.beta_zero;
   a.c_remote = query ? !c_is_local(a.C) : 0;
   a.c_ring = direct && QG_C_RING && ((QG_RING_TRI && a.tri != 0) || a.KT >= QG_C_RING_MIN_KT) && !a.c_remote;
-  a.c_al32 = (reinterpret_cast<uintptr_t>(a.C) & 31u) == 0;
   if (a.c_ring) {
     const int e = encode_c(&a.tmC, a.C, a.ldc, a.M, a.N);
     if (e) return e;
