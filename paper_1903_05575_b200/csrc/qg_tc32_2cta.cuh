@@ -84,6 +84,9 @@ constexpr int64_t kTc2PartFloats = 4 * int64_t(kTcBN) * kTcBM;
 // running CTA (the host sizes the slots by the SM count; a CTA on an SM id past
 // it -- ids need not be contiguous -- folds every chunk into the target
 // straight from TMEM, holding TMEM during the fold).
+#ifndef QG_TC2_RED
+#define QG_TC2_RED 0  // 1: chunks summed in the slot by L2 reductions, C written once (see the epilogue)
+#endif
 #ifndef QG_TC2_CHUNK_KT
 #define QG_TC2_CHUNK_KT 32  // 256 quaternion k per chunk
 #endif
@@ -470,9 +473,23 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kTcThreads, 1)
           tmem_ld_wait();
           release(c);
           float *sp = slotp + int64_t(c) * kTcBN * kTcBM;
+#if QG_TC2_RED
+          // running sum in the slot: the first chunk stores, later ones add in L2
+          // (red.global.add.f32, round-to-nearest; no round trip, nothing to wait for)
+          if (j == 0) {
+#pragma unroll
+            for (int n = 0; n < kTcBN; ++n) __stcg(sp + int64_t(n) * kTcBM, v[n]);
+          } else {
+#pragma unroll
+            for (int n = 0; n < kTcBN; ++n)
+              asm volatile("red.global.add.f32 [%0], %1;\n" ::"l"(sp + int64_t(n) * kTcBM), "f"(v[n]) : "memory");
+          }
+#else
 #pragma unroll
           for (int n = 0; n < kTcBN; ++n) __stcg(sp + int64_t(n) * kTcBM, v[n]);
+#endif
         }
+#if !QG_TC2_RED
         for (int n0 = 0; n0 < kTcBN; n0 += 8) {
           float d[4][8];
 #pragma unroll
@@ -481,15 +498,29 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kTcThreads, 1)
             for (int jj = 0; jj < 8; ++jj) d[c][jj] = __ldcg(slotp + (int64_t(c) * kTcBN + n0 + jj) * kTcBM);
           tc2_fold<8>(args, part, row, pn, q * 32 + lane, n0, d, j == 0);
         }
+#endif
         continue;
       }
       // the last chunk (or any chunk without a slot) folds straight from TMEM
+      // (QG_TC2_RED: plus the running sum of the earlier chunks from the slot)
       for (int c = 0; c < 4; ++c) mbar_wait_guarded(&acc_full[c], uint32_t(j & 1));
       tc_fence_after();
+      const bool with_slot = QG_TC2_RED && slotp && nchunks > 1;
       for (int n0 = 0; n0 < kTcBN; n0 += 16) {
         float d[4][16];
         ld_tmem16(n0, d);
-        tc2_fold<16>(args, part, row, pn, q * 32 + lane, n0, d, j == 0);
+        if (with_slot) {
+          float o[4][16];
+#pragma unroll
+          for (int c = 0; c < 4; ++c)
+#pragma unroll
+            for (int jj = 0; jj < 16; ++jj) o[c][jj] = __ldcg(slotp + (int64_t(c) * kTcBN + n0 + jj) * kTcBM);
+#pragma unroll
+          for (int c = 0; c < 4; ++c)
+#pragma unroll
+            for (int jj = 0; jj < 16; ++jj) d[c][jj] += o[c][jj];
+        }
+        tc2_fold<16>(args, part, row, pn, q * 32 + lane, n0, d, with_slot || j == 0);
       }
       if (j + 1 < nchunks)
         for (int c = 0; c < 4; ++c) release(c);
