@@ -74,18 +74,23 @@ constexpr int64_t kTc2PartFloats = 4 * int64_t(kTcBN) * kTcBM;
 // fraction of the tolerance, proportional to kc): after every chunk but the last
 // the epilogue warps read TMEM component by component, release each component
 // to the MMA issuer at once (it waits per component before the next chunk's
-// first MMA into it, so the next chunk overlaps the drain) and store the values
-// into their SM's slot; then, while the next chunk runs, fold the slot into the
-// target with round-to-nearest FP32: C <- alpha chunk + (first ? beta C : C),
-// or, for a split-K unit, the raw partial (+)= chunk.  The last chunk folds
-// straight from TMEM.  Each thread only touches its own TMEM lane (row) of the
+// first MMA into it, so the next chunk overlaps the drain) and add the values
+// into their SM's slot with L2 reductions (round-to-nearest FP32; the first
+// chunk stores).  The last chunk adds the slot to its TMEM values and folds
+// into the target: C <- alpha sum + beta C, or, for a split-K unit, the raw
+// partial.  (QG_TC2_RED = 0: every chunk stored to the slot and folded into the
+// target behind the next chunk's MMAs -- four times the L2 traffic.)  Each thread only touches its own TMEM lane (row) of the
 // slot, so the slot needs no synchronisation beyond program order;
 // one CTA per SM (shared memory) makes the %smid-indexed slot private to the
 // running CTA (the host sizes the slots by the SM count; a CTA on an SM id past
 // it -- ids need not be contiguous -- folds every chunk into the target
 // straight from TMEM, holding TMEM during the fold).
 #ifndef QG_TC2_RED
-#define QG_TC2_RED 0  // 1: chunks summed in the slot by L2 reductions, C written once (see the epilogue)
+// 1: chunks summed in the slot by L2 reductions (red.global.add.f32), C written
+// once; 0: each chunk stored to the slot and folded into C behind the next one.
+// c3 FP32 67.7-68.0 vs 71.1-74.5 ms (same box; the clock under the power cap
+// 1605-1620 vs 1466-1485 MHz: a quarter of the L2 traffic), same accuracy.
+#define QG_TC2_RED 1
 #endif
 #ifndef QG_TC2_CHUNK_KT
 #define QG_TC2_CHUNK_KT 32  // 256 quaternion k per chunk
