@@ -143,18 +143,67 @@ int num_sms();
 // than one wave (one pair per 2 SMs) -- as many as fill the wave, at most 8
 // (16 measured 10-19% slower at 320^3-512^3), each split >= 4 k-tiles.  Monotone in ktiles, so a reserve sized for the
 // whole K covers every K-panel launch.
-int64_t tc2_splits(int64_t M, int64_t N, int64_t ktiles) {
-  if (!QG_TC32_2CTA) return 1;
-  const int64_t pairs = cdiv(M, 2 * qg::kTcBM) * cdiv(N, qg::kTcBN);
-  const int64_t wave = std::max<int64_t>(1, num_sms() / 2);
-  if (pairs >= wave) return 1;
-  return std::max<int64_t>(1, std::min<int64_t>({wave / pairs, 8, ktiles / 4}));
+//
+// At one wave or more the whole waves run whole tile pairs (epilogue into C) and
+// only the R pairs of the partial last wave split K, S ways: S minimises the
+// partial wave's cost in units of one whole-pair wave, ceil(R S / wave) / S, over
+// 2 <= S <= 8 with R S <= kTc2SplitMaxWaves waves, and is taken when that cost is
+// <= 0.85 and every split keeps >= kTc2SplitMinKt k-tiles (the partial stores and
+// the reduce launch stay small against it).  2048^3: 128 pairs = 74 + 54, and
+// 54 pairs x 4 splits fill 3 waves of quarter-K units (cost 0.75).  S depends
+// on K only through the k-tile floor, so a reserve for the whole K covers every
+// K-panel / host-chunk launch (tc2_part_bytes).  The environment variable
+// QG_TC2_S (read once) forces S for the sub-wave / remainder case, for A/B
+// measurements (within the same reserve bound).
+struct Tc2Split {
+  int64_t full;  // leading tile pairs of the raster computed whole (epilogue into C)
+  int64_t S;     // splits of each remaining pair (1: none)
+};
+constexpr int64_t kTc2SplitMinKt = 16;    // >= 128 k per split unit above one wave
+constexpr int64_t kTc2SplitMaxWaves = 3;  // remainder split units <= 3 waves
+int tc2_forced_splits() {
+  static const int v = [] {
+    const char *e = std::getenv("QG_TC2_S");
+    return e ? std::atoi(e) : 0;
+  }();
+  return v;
 }
-size_t tc2_part_bytes(int64_t M, int64_t N, int64_t ktiles) {
-  const int64_t S = tc2_splits(M, N, ktiles);
-  if (S <= 1) return 0;
+// Remainder split of R pairs above one wave (K-independent part of the rule).
+int64_t tc2_rem_splits(int64_t R, int64_t wave) {
+  if (R <= 0) return 1;
+  const int64_t smax = std::min<int64_t>(8, kTc2SplitMaxWaves * wave / R);
+  if (const int f = tc2_forced_splits()) return std::max<int64_t>(1, std::min<int64_t>(f, smax));
+  int64_t best = 1;
+  double cbest = 0.85;
+  for (int64_t S = 2; S <= smax; ++S) {
+    const double c = double(cdiv(R * S, wave)) / double(S);
+    if (c < cbest - 1e-9) { cbest = c; best = S; }
+  }
+  return best;
+}
+Tc2Split tc2_split(int64_t M, int64_t N, int64_t ktiles) {
   const int64_t pairs = cdiv(M, 2 * qg::kTcBM) * cdiv(N, qg::kTcBN);
-  return align256(size_t(pairs) * size_t(S) * 2 * size_t(qg::kTc2PartFloats) * sizeof(float));
+  if (!QG_TC32_2CTA) return {pairs, 1};
+  const int64_t wave = std::max<int64_t>(1, num_sms() / 2);
+  if (pairs < wave) {
+    const int f = tc2_forced_splits();
+    int64_t S = f > 0 ? f : std::min<int64_t>({wave / pairs, 8, ktiles / 4});
+    S = std::max<int64_t>(1, std::min<int64_t>({S, wave / pairs, 8, ktiles}));  // within the reserve, >= 1 k-tile each
+    return {S > 1 ? 0 : pairs, S};
+  }
+  const int64_t full = pairs / wave * wave, S = tc2_rem_splits(pairs - full, wave);
+  const int64_t floor_kt = tc2_forced_splits() ? 1 : kTc2SplitMinKt;
+  if (S <= 1 || ktiles < floor_kt * S) return {pairs, 1};
+  return {full, S};
+}
+int64_t tc2_splits(int64_t M, int64_t N, int64_t ktiles) { return tc2_split(M, N, ktiles).S; }
+// Split-K partials: pairs x S of the largest split any launch with <= ktiles
+// k-tiles takes (sub-wave: S is monotone in ktiles; above: S or none).
+size_t tc2_part_bytes(int64_t M, int64_t N, int64_t ktiles) {
+  const Tc2Split sp = tc2_split(M, N, ktiles);
+  if (sp.S <= 1) return 0;
+  const int64_t pairs = cdiv(M, 2 * qg::kTcBM) * cdiv(N, qg::kTcBN);
+  return align256(size_t(pairs - sp.full) * size_t(sp.S) * 2 * size_t(qg::kTc2PartFloats) * sizeof(float));
 }
 
 // FP32 pair kernel, chunk promotion (qg_tc32_2cta.cuh): one raw 4 x 128 x 128
@@ -597,9 +646,12 @@ int launch_tc2(qg::Tc2Args &t, int64_t M, int64_t N, int64_t KT, void *sk_scratc
   t.kc = QG_TC2_CHUNK_KT;
   t.tmp = static_cast<float *>(sk_scratch);
   t.nslots = num_sms();
-  t.S = int(tc2_splits(M, N, KT));
+  const Tc2Split sp = tc2_split(M, N, KT);
+  t.S = int(sp.S);
+  t.full = sp.full;
   t.part = reinterpret_cast<float *>(static_cast<char *>(sk_scratch) + tc2_slot_bytes());
-  const int64_t grid = 2 * t.MT2 * t.NT * t.S;
+  const int64_t rest = t.MT2 * t.NT - t.full;  // pairs split over K
+  const int64_t grid = 2 * (t.full + rest * t.S);
   if (grid > INT32_MAX) return int(cudaErrorInvalidConfiguration);
   { int ti = tstart(kMain, st);
   qg::qgemm_tc32_2cta_kernel<kDirect><<<unsigned(grid), qg::kTcThreads,
@@ -610,7 +662,7 @@ int launch_tc2(qg::Tc2Args &t, int64_t M, int64_t N, int64_t KT, void *sk_scratc
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return int(e);
     { int ti = tstart(kMain, st);
-    qg::tc2_reduce_kernel<<<dim3(unsigned(2 * t.MT2 * t.NT), qg::kTcBN / 16), qg::kTcBM, 0, st>>>(t);
+    qg::tc2_reduce_kernel<<<dim3(unsigned(2 * rest), qg::kTcBN / 16), qg::kTcBM, 0, st>>>(t);
     tstop(ti, st); }
     ++g_last_launches;
   }

@@ -52,8 +52,9 @@ struct alignas(64) Tc2Args {
   float *C;
   int64_t ldc, M, N, MT2, NT, KT;  // MT2 = 256-row tile pairs
   Scalars<float> sc;
-  int S;             // K splits per tile pair (1: the epilogue updates C)
-  float *part;       // S > 1: raw accumulators, kTc2PartFloats per CTA, summed by tc2_reduce_kernel
+  int S;             // K splits of each pair past `full` (1: the epilogue updates C)
+  int64_t full;      // pairs [0, full) of the raster are computed whole, the rest split S ways
+  float *part;       // S > 1: raw accumulators of the split pairs, kTc2PartFloats per CTA, summed by tc2_reduce_kernel
   // direct feed: tmA / tmB are 2-D maps of the user's interleaved op(A) / op(B)
   // (rc: rows contiguous -> {4 R floats, K}, boxes of 32 rows x 8 k; else
   // {4 K floats, R}, one box of all rows x 8 k, 128-byte swizzle); cj: op H
@@ -332,15 +333,18 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kTcThreads, 1)
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t rank = cluster_rank();
-  // tile pair of this cluster (grouped rasterisation as the 1-CTA kernel) and,
-  // with S > 1 splits, its share [k0, k1) of the k-tiles
+  // tile pair of this cluster (grouped rasterisation as the 1-CTA kernel): the
+  // first `full` clusters each take a whole pair; past them, pair full + r / S
+  // and its share [k0, k1) of the k-tiles (split ks = r % S)
   const int64_t cid = int64_t(blockIdx.x) >> 1;
-  const int64_t pid = cid / args.S, ks = cid % args.S;
+  const bool split = cid >= args.full;
+  const int64_t Su = split ? args.S : 1;
+  const int64_t pid = split ? args.full + (cid - args.full) / Su : cid, ks = split ? (cid - args.full) % Su : 0;
   int64_t pm, pn;
   tc2_tile(pid, args.MT2, args.NT, pm, pn);
   const int64_t mt = 2 * pm + rank;  // this CTA's 128-row A tile
   const int64_t KT = args.KT;
-  const int64_t k0 = ks * KT / args.S, k1 = (ks + 1) * KT / args.S;
+  const int64_t k0 = ks * KT / Su, k1 = (ks + 1) * KT / Su;
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < P; ++s) {
@@ -444,7 +448,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kTcThreads, 1)
     const int q = warp - 4;
     const int64_t row = mt * kTcBM + q * 32 + lane;
     const uint32_t tbase = tmem + (uint32_t(q * 32) << 16);
-    float *part = args.S > 1 ? args.part + ((pid * args.S + ks) * 2 + rank) * kTc2PartFloats : nullptr;
+    float *part = Su > 1 ? args.part + (((pid - args.full) * Su + ks) * 2 + rank) * kTc2PartFloats : nullptr;
     const int64_t nchunks = (k1 - k0 + args.kc - 1) / args.kc;
     // this SM's running-sum slot (planar [c][col][row]); without one (SM id past
     // the slots) every chunk folds into the target straight from TMEM
@@ -539,17 +543,18 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kTcThreads, 1)
   }
 }
 
-// Split-K epilogue: C(row, col) <- alpha (x) sum_ks part_ks + beta (x) C, the S
-// partials added in split order (deterministic).  Block = one CTA tile's 128
-// rows (threads) x 16 columns; grid = (2 * pairs, 8).
+// Split-K epilogue of the split pairs (raster positions full..): C(row, col) <-
+// alpha (x) sum_ks part_ks + beta (x) C, the S partials added in split order
+// (deterministic).  Block = one CTA tile's 128 rows (threads) x 16 columns;
+// grid = (2 * split pairs, 8).
 __global__ void __launch_bounds__(kTcBM) tc2_reduce_kernel(const __grid_constant__ Tc2Args args) {
-  const int64_t cta = blockIdx.x, pid = cta >> 1;
+  const int64_t cta = blockIdx.x, sp = cta >> 1, pid = args.full + sp;
   const int rank = int(cta & 1);
   int64_t pm, pn;
   tc2_tile(pid, args.MT2, args.NT, pm, pn);
   const int64_t row = (2 * pm + rank) * kTcBM + threadIdx.x;
   if (row >= args.M) return;
-  const float *p0 = args.part + (pid * args.S * 2 + rank) * kTc2PartFloats + threadIdx.x;
+  const float *p0 = args.part + (sp * args.S * 2 + rank) * kTc2PartFloats + threadIdx.x;
   const int64_t stride = 2 * kTc2PartFloats;  // next split, same rank
   for (int j = 0; j < 16; ++j) {
     const int cl = int(blockIdx.y) * 16 + j;

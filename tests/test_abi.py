@@ -130,6 +130,10 @@ def test_qherk_invalid_arguments(lib, kw, code):
 # FP32 pair kernel: one raw 4 x 128 x 128 FP32 slot per SM for the accumulation
 # chunks (qg_tc32_2cta.cuh), 148 SMs assumed without a device
 F32_SLOTS = 148 * 4 * 128 * 128 * 4
+# c3 FP32: 2048 tile pairs = 27 waves of 74 + 50; the 50 pairs of the partial
+# wave split K 4 ways (200 quarter-K units = 3 waves, cost 0.75 of a whole-pair
+# wave), raw partials 50 x 4 x 2 CTAs x (4 x 128 x 128) floats
+F32_C3_PART = 50 * 4 * 2 * 4 * 128 * 128 * 4
 
 
 def test_workspace_sizes(lib):
@@ -142,7 +146,7 @@ def test_workspace_sizes(lib):
     assert f64 == 2 * 8192 * 8192 * 32 + sk
     # tcgen05 3xTF32 path: tf32 hi + lo planes + one 256 KiB accumulation-chunk slot
     # per SM (148 assumed without a device)
-    assert f32 == 2 * 8192 * 8192 * 32 + F32_SLOTS
+    assert f32 == 2 * 8192 * 8192 * 32 + F32_SLOTS + F32_C3_PART
     # one K-tile: 2 row tiles of A + 2 of B, 32 KiB per (64 x 16)-quaternion chunk,
     # + partial slots for the largest grid over the whole K (4 tiles x 63 k-tiles
     # / 2 = 126 CTAs) + counters
@@ -171,7 +175,7 @@ def test_direct_path_workspace_is_stream_k_scratch(lib):
         lib.qgemm_set_path_policy(pol)
         assert lib.qgemm_workspace_bytes(b"N", b"H", 8192, 8192, 8192, 0) == sk
         assert lib.qgemm_workspace_min_bytes(b"N", b"H", 8192, 8192, 8192, 0) == sk
-        assert lib.qgemm_workspace_bytes(b"N", b"H", 8192, 8192, 8192, 1) == F32_SLOTS
+        assert lib.qgemm_workspace_bytes(b"N", b"H", 8192, 8192, 8192, 1) == F32_SLOTS + F32_C3_PART
         assert lib.qherk_workspace_bytes(b"L", b"N", 32768, 256) == sk
     lib.qgemm_set_path_policy(1)  # packed
     assert lib.qherk_workspace_bytes(b"L", b"N", 32768, 256) > sk
@@ -244,7 +248,11 @@ def test_host_workspace_f32_covers_every_panel_split(lib, N, policy):
     and the panel width do not split.  (The reserve used to cover only the full
     and the panel width: an out-of-bounds write of 32 MiB.)  Packed chunks
     (policy 1, and auto for FP32) also hold 2 packed chunks per operand; the
-    direct chunks (policy 3) are read in place from the staging slots."""
+    direct chunks (policy 3) are read in place from the staging slots.
+    Above one wave only the pairs of the partial last wave split:
+    N = 8192's 512-wide panels have 128 pairs = 74 + 54, split 4 ways (54 x 4
+    units = 3 waves); N = 1024's full width has 256 pairs = 3 x 74 + 34, split 2
+    ways.  Those exceed the 128-wide pieces' 32 x 2 units."""
     lib.qgemm_set_path_policy(policy)
     M = K = 8192
     qb = 16
@@ -252,7 +260,8 @@ def test_host_workspace_f32_covers_every_panel_split(lib, N, policy):
     stage = 2 * M * kc * qb + 2 * N * kc * qb
     ktc = kc // 8                                # FP32 k-tiles per chunk (8 k per tile)
     packed = 2 * (2 * (M // 256)) * ktc * 32768 + 2 * (N // 128) * ktc * 32768
-    part = 32 * 2 * 2 * 65536 * 4                # pairs x S x 2 CTAs x 4x128x128 floats
+    units = {8192: 54 * 4, 1024: 34 * 2}[N]      # split pairs x S, the largest of any launched width
+    part = units * 2 * 65536 * 4                 # x 2 CTAs x 4x128x128 floats
     want = 2 * M * N * qb + stage + (packed if policy == 1 else 0) + F32_SLOTS + part
     assert lib.qgemm_host_workspace_bytes(b"N", b"H", M, N, K, 1) == want
     lib.qgemm_set_path_policy(1)

@@ -114,6 +114,26 @@ def test_f32_split_k_pair_kernel(M, N, K, opA, opB, policy):
         assert_parity(pr, run_gpu(pr, "f32"), oracle_full(pr), exact=True)
 
 
+@pytest.mark.parametrize("M,N,K,S", [(2048, 2048, 1024, 4), (2000, 1900, 777, 3)])
+@pytest.mark.parametrize("opA,opB", [("N", "H"), ("H", "T")])
+def test_f32_remainder_split_above_one_wave(M, N, K, S, opA, opB):
+    """FP32 pair kernel above one wave of 74 tile pairs: the whole waves run whole
+    pairs, the pairs of the partial last wave split K: 2048^2 has
+    128 pairs = 74 + 54 whole + 54 x 4 quarter-K units; 2000 x 1900 has 120 =
+    74 + 46 x 3 (ragged M / N tiles and a K of 98 k-tiles split 32/33/33).  Both
+    feeds; normal inputs within the FP32 tolerance, exact-integer inputs
+    bitwise; the launch count shows the reduce launch ran (split taken)."""
+    prs = [make_problem(M, N, K, opA, opB, QALPHA, QBETA, seed=21, dist="normal"),
+           make_problem(M, N, K, opA, opB, (1, 0, 0, 0), (-1, 0, 0, 0), seed=22, dist="int2")]
+    refs = [oracle_full(pr) for pr in prs]
+    for policy, launches in ((qg.PATH_PACKED, 3), (qg.PATH_DIRECT, 2)):
+        with path_policy(policy):
+            for pr, ref, exact in zip(prs, refs, (False, True)):
+                got = run_gpu(pr, "f32")
+                assert qg.last_launch_count() == launches, (policy, S)
+                assert_parity(pr, got, ref, precision="f32", exact=exact)
+
+
 @pytest.mark.parametrize("M,N,K", [(130, 70, 520), (64, 1, 512), (1, 64, 600), (257, 129, 1000)])
 @pytest.mark.parametrize("opA,opB", OPS)
 @pytest.mark.parametrize("policy", [qg.PATH_PACKED, qg.PATH_DIRECT], ids=["packed", "direct"])
