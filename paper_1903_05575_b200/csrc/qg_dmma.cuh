@@ -60,6 +60,14 @@ constexpr int kConsumerRegs = 232;
 #ifndef QG_C_RING
 #define QG_C_RING 1  // epilogue C tiles through the ring by TMA (see produce_c_stage)
 #endif
+#ifndef QG_C_STORE_WARP
+// 1: a producer-warpgroup warp issues the ring epilogue's TMA stores, waits for
+// the TMA unit to read each box and hands the slot back to the producer, so the
+// consumers go on to the next tile as soon as they have written their
+// quaternions (no CTA-wide barriers, no wait for the store's reads); 0: consumer
+// thread 0 stores behind two consumer barriers and all consumers wait for the reads
+#define QG_C_STORE_WARP 1
+#endif
 #ifndef QG_C_PREFETCH_BULK
 #define QG_C_PREFETCH_BULK 1  // 1: the producer lane bulk-prefetches C tiles; 0: consumer lanes prefetch per quaternion
 #endif
@@ -68,7 +76,8 @@ constexpr int kConsumerRegs = 232;
 #endif
 constexpr int kGroupM = QG_GROUP_M;  // rasterisation: M-tiles per group (L2 reuse of panels)
 // ring + barriers + 1 KB so the ring can start on a 1024-byte boundary
-constexpr size_t kDmmaSmemBytes = size_t(kStages) * 2 * kChunkElems * sizeof(double) + 2 * kStages * 8 + 1024;
+// (barriers: full, empty and, for the ring epilogue's store warp, cdone per slot)
+constexpr size_t kDmmaSmemBytes = size_t(kStages) * 2 * kChunkElems * sizeof(double) + 3 * kStages * 8 + 1024;
 
 // How the ring is fed (kernel template parameter).
 // (a third feed -- all 128 producer threads de-interleaving with 16-byte
@@ -421,6 +430,44 @@ __device__ __forceinline__ bool produce_next_tma(Producer &p, const DmmaArgs &ar
   return true;
 }
 
+__device__ __forceinline__ void mbar_arrive_n(uint64_t *bar, uint32_t n) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(n) : "memory");
+}
+// QG_C_STORE_WARP: the ring epilogue's stores.  This lane walks the CTA's work
+// list like the producer, tracking the ring slot (a unit of k-tiles [kb, ke)
+// occupies ke - kb fills, then two C stages if it runs the ring epilogue); per
+// C stage it waits until all consumer warps have written their quaternions
+// (cdone), TMA-stores the two boxes, waits until the TMA unit has read them and
+// returns the slot to the producer (one arrival counting for every consumer
+// warp).  Its bulk-store groups are completed before the CTA exits.
+__device__ __forceinline__ void c_store_loop(const DmmaArgs &args, const SkSplit &sp, double *sA, double *sB,
+                                             uint64_t *empty, uint64_t *cdone) {
+  WorkIter it = make_iter(args, sp);
+  Unit u;
+  int slot = 0;
+  uint32_t cph = 0;  // parity of each slot's cdone barrier
+  while (it.next(args, u)) {
+    slot = int((int64_t(slot) + (u.ke - u.kb)) % kStages);
+    if (u.kb != 0) continue;  // stream-K contributor: no epilogue here
+    int64_t mt, nt;
+    work_tile(args, u.t, mt, nt);
+    if (!ring_epilogue(args, mt, nt)) continue;
+#pragma unroll 1
+    for (int h = 0; h < 2; ++h) {
+      mbar_wait(&cdone[slot], (cph >> slot) & 1u);
+      cph ^= 1u << slot;
+      const int n0 = int(nt * kBR), r0 = int(mt * kBR) + 16 * h;
+      tma_store_3d(&args.tmC, sA + slot * kChunkElems, 0, n0, r0);
+      tma_store_3d(&args.tmC, sB + slot * kChunkElems, 0, n0, r0 + 32);
+      asm volatile("cp.async.bulk.commit_group;\n" ::: "memory");
+      asm volatile("cp.async.bulk.wait_group.read 0;\n" ::: "memory");
+      mbar_arrive_n(&empty[slot], kConsumerWarps);
+      if (++slot == kStages) slot = 0;
+    }
+  }
+  asm volatile("cp.async.bulk.wait_group 0;\n" ::: "memory");
+}
+
 // Byte offset of the 16-byte pair (components 2pp, 2pp+1) of (r, k) in a TMA tile.
 __device__ __forceinline__ uint32_t tma_tile_off(int rc, int r, int k, int pp) {
   const uint32_t lin = rc ? uint32_t(((k * kBR + r) * 4 + 2 * pp) * 8) : uint32_t(((r * kBK + k) * 4 + 2 * pp) * 8);
@@ -518,6 +565,7 @@ __global__ void __launch_bounds__(kDmmaThreads, 1) qgemm_dmma_kernel(const __gri
   double *sB = sA + kStages * kChunkElems;
   uint64_t *full = reinterpret_cast<uint64_t *>(sB + kStages * kChunkElems);
   uint64_t *empty = full + kStages;
+  uint64_t *cdone = empty + kStages;  // QG_C_STORE_WARP: consumers wrote a C stage (ring epilogue)
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -530,6 +578,7 @@ __global__ void __launch_bounds__(kDmmaThreads, 1) qgemm_dmma_kernel(const __gri
     for (int s = 0; s < kStages; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], kConsumerWarps);
+      mbar_init(&cdone[s], kConsumerWarps);
     }
     fence_mbar_init();
   }
@@ -555,6 +604,8 @@ __global__ void __launch_bounds__(kDmmaThreads, 1) qgemm_dmma_kernel(const __gri
       if (warp == kConsumerWarps && lane == 0)
         while (produce_next_tma<kFeed == kFeedTma128>(prod, args, sA, sB, full, empty)) {
         }
+      if (kRing && QG_C_STORE_WARP && args.c_ring && warp == kConsumerWarps + 1 && lane == 0)
+        c_store_loop(args, sp, sA, sB, empty, cdone);
     } else {
       if (warp == kConsumerWarps && lane == 0)
         while (produce_next(prod, args, sA, sB, full, empty)) {
@@ -765,6 +816,12 @@ __global__ void __launch_bounds__(kDmmaThreads, 1) qgemm_dmma_kernel(const __gri
               *q1 = make_double2(out[2], out[3]);
             }
         asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");  // smem writes -> TMA store
+        if (QG_C_STORE_WARP) {  // the store warp takes it from here (c_store_loop)
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&cdone[slot]);
+          if (++slot == kStages) { slot = 0; phase ^= 1u; }
+          continue;
+        }
         consumer_bar();
         if (tid == 0) {
           const int n0 = int(nt * kBR), r0 = int(mt * kBR) + 16 * h;
@@ -773,6 +830,10 @@ __global__ void __launch_bounds__(kDmmaThreads, 1) qgemm_dmma_kernel(const __gri
           asm volatile("cp.async.bulk.commit_group;\n" ::: "memory");
         }
         if (++slot == kStages) { slot = 0; phase ^= 1u; }
+      }
+      if (QG_C_STORE_WARP) {
+        QG_TR(5);
+        continue;
       }
       // the slots return to the producer once the TMA unit has read them
       if (tid == 0) asm volatile("cp.async.bulk.wait_group.read 0;\n" ::: "memory");
