@@ -350,7 +350,11 @@ int persistent_ctas() {
 #define QG_RING_TRI 1  // QHERK launches take the ring whatever their K (c4 QHERK 125.0 vs 125.8 ms)
 #endif
 #ifndef QG_C_RING_MIN_KT
-#define QG_C_RING_MIN_KT 32
+// ring epilogue for launches of >= this many k-tiles (beta != 0).  32 while the
+// consumers barriered and waited for the TMA store's reads (c4's 16 k-tiles:
+// 248.4 vs 245.5 ms per-lane); with the store warp (QG_C_STORE_WARP) the ring
+// wins at c4 too: 241.8 vs 245.9 ms (profiles/r02w_ab.txt)
+#define QG_C_RING_MIN_KT 1
 #endif
 #ifndef QG_SK_FULL_WAVES
 #define QG_SK_FULL_WAVES 0

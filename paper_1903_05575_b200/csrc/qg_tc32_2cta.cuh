@@ -450,10 +450,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kTcThreads, 1)
     const uint32_t tbase = tmem + (uint32_t(q * 32) << 16);
     float *part = Su > 1 ? args.part + (((pid - args.full) * Su + ks) * 2 + rank) * kTc2PartFloats : nullptr;
     const int64_t nchunks = (k1 - k0 + args.kc - 1) / args.kc;
-    // this SM's running-sum slot (planar [c][col][row]); without one (SM id past
-    // the slots) every chunk folds into the target straight from TMEM
+    // this SM's running-sum slot, [c][col / 4][row][col % 4]: each thread's 4
+    // consecutive columns are one 16-byte vector (one vector reduction; a warp's
+    // 32 rows are 512 contiguous bytes); without a slot (SM id past the slots)
+    // every chunk folds into the target straight from TMEM
     const uint32_t sm = smid();
-    float *slotp = sm < uint32_t(args.nslots) ? args.tmp + int64_t(sm) * kTc2PartFloats + q * 32 + lane : nullptr;
+    float *slotp = sm < uint32_t(args.nslots) ? args.tmp + int64_t(sm) * kTc2PartFloats + 4 * (q * 32 + lane) : nullptr;
+    auto slot_off = [](int c, int n) { return (int64_t(c) * (kTcBN / 4) + (n >> 2)) * (4 * kTcBM) + (n & 3); };
     auto ld_tmem16 = [&](int n0, float (&d)[4][16]) {
 #pragma unroll
       for (int c = 0; c < 4; ++c) tmem_ld16(tbase + uint32_t(c * kTcBN + n0), d[c]);
@@ -481,21 +484,27 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kTcThreads, 1)
           }
           tmem_ld_wait();
           release(c);
-          float *sp = slotp + int64_t(c) * kTcBN * kTcBM;
+          float *sp = slotp + slot_off(c, 0);
 #if QG_TC2_RED
           // running sum in the slot: the first chunk stores, later ones add in L2
-          // (red.global.add.f32, round-to-nearest; no round trip, nothing to wait for)
+          // (red.global.add.v4.f32, round-to-nearest; no round trip, nothing to
+          // wait for; one 16-byte reduction per 4 columns: a quarter of the L2
+          // operations of scalar reductions)
           if (j == 0) {
 #pragma unroll
-            for (int n = 0; n < kTcBN; ++n) __stcg(sp + int64_t(n) * kTcBM, v[n]);
+            for (int n = 0; n < kTcBN; n += 4)
+              __stcg(reinterpret_cast<float4 *>(sp + slot_off(0, n)), make_float4(v[n], v[n + 1], v[n + 2], v[n + 3]));
           } else {
 #pragma unroll
-            for (int n = 0; n < kTcBN; ++n)
-              asm volatile("red.global.add.f32 [%0], %1;\n" ::"l"(sp + int64_t(n) * kTcBM), "f"(v[n]) : "memory");
+            for (int n = 0; n < kTcBN; n += 4)
+              asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};\n" ::"l"(sp + slot_off(0, n)), "f"(v[n]),
+                           "f"(v[n + 1]), "f"(v[n + 2]), "f"(v[n + 3])
+                           : "memory");
           }
 #else
 #pragma unroll
-          for (int n = 0; n < kTcBN; ++n) __stcg(sp + int64_t(n) * kTcBM, v[n]);
+          for (int n = 0; n < kTcBN; n += 4)
+            __stcg(reinterpret_cast<float4 *>(sp + slot_off(0, n)), make_float4(v[n], v[n + 1], v[n + 2], v[n + 3]));
 #endif
         }
 #if !QG_TC2_RED
@@ -504,7 +513,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kTcThreads, 1)
 #pragma unroll
           for (int c = 0; c < 4; ++c)
 #pragma unroll
-            for (int jj = 0; jj < 8; ++jj) d[c][jj] = __ldcg(slotp + (int64_t(c) * kTcBN + n0 + jj) * kTcBM);
+            for (int jj = 0; jj < 8; ++jj) d[c][jj] = __ldcg(slotp + slot_off(c, n0 + jj));
           tc2_fold<8>(args, part, row, pn, q * 32 + lane, n0, d, j == 0);
         }
 #endif
@@ -519,15 +528,20 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kTcThreads, 1)
         float d[4][16];
         ld_tmem16(n0, d);
         if (with_slot) {
-          float o[4][16];
+          float4 o[4][4];
 #pragma unroll
           for (int c = 0; c < 4; ++c)
 #pragma unroll
-            for (int jj = 0; jj < 16; ++jj) o[c][jj] = __ldcg(slotp + (int64_t(c) * kTcBN + n0 + jj) * kTcBM);
+            for (int g = 0; g < 4; ++g) o[c][g] = __ldcg(reinterpret_cast<const float4 *>(slotp + slot_off(c, n0 + 4 * g)));
 #pragma unroll
           for (int c = 0; c < 4; ++c)
 #pragma unroll
-            for (int jj = 0; jj < 16; ++jj) d[c][jj] += o[c][jj];
+            for (int g = 0; g < 4; ++g) {
+              d[c][4 * g] += o[c][g].x;
+              d[c][4 * g + 1] += o[c][g].y;
+              d[c][4 * g + 2] += o[c][g].z;
+              d[c][4 * g + 3] += o[c][g].w;
+            }
         }
         tc2_fold<16>(args, part, row, pn, q * 32 + lane, n0, d, with_slot || j == 0);
       }
