@@ -68,11 +68,6 @@ constexpr int kConsumerRegs = 232;
 // thread 0 stores behind two consumer barriers and all consumers wait for the reads
 #define QG_C_STORE_WARP 1
 #endif
-#ifndef QG_EARLY_RELEASE
-// 1: a consumer warp releases a ring slot once it has loaded the stage's last
-// fragments (before that k4 step's DMMAs); 0: after the stage's last DMMA
-#define QG_EARLY_RELEASE 1
-#endif
 #ifndef QG_C_PREFETCH_BULK
 #define QG_C_PREFETCH_BULK 1  // 1: the producer lane bulk-prefetches C tiles; 0: consumer lanes prefetch per quaternion
 #endif
@@ -706,12 +701,7 @@ __global__ void __launch_bounds__(kDmmaThreads, 1) qgemm_dmma_kernel(const __gri
         for (int jj = 0; jj < 2; ++jj)
 #pragma unroll
           for (int s = 0; s < 4; ++s) bn[jj][s] = -bf[jj][s];
-        if (QG_EARLY_RELEASE && ks == kBK / 4 - 1) {
-          // the stage's last fragments are loaded: hand the slot back before the
-          // last k4 step's 128 DMMAs (~2 us per SM sub-partition at two warps)
-          __syncwarp();
-          if (lane == 0) mbar_arrive(&empty[slot]);
-        }
+
         // 16 DMMA per (m8, n8) tile; p outermost so consecutive DMMAs hit
         // different accumulators.
 #pragma unroll
@@ -727,10 +717,8 @@ __global__ void __launch_bounds__(kDmmaThreads, 1) qgemm_dmma_kernel(const __gri
                 dmma_8x8x4(acc[ii][jj][c], af[ii][p], neg ? bn[jj][s] : bf[jj][s]);
               }
       }
-      if (!QG_EARLY_RELEASE) {
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&empty[slot]);
-      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[slot]);
       if (++slot == kStages) { slot = 0; phase ^= 1u; }
     }
 
