@@ -95,7 +95,8 @@ constexpr int kMaxPersistentCTAs = 256;
 // qgemm_debug_trace): consumer thread 0 of every CTA stamps %globaltimer at
 // phase boundaries; event = (code << 56) | ns.  Codes: 1 consumers start,
 // 2 unit start, 3 unit k-loop done, 4 stream-K fixup done (contributor parked /
-// owner summed), 5 epilogue done, 6 consumers done.
+// owner summed), 5 epilogue done, 6 consumers done, 7/8 per-lane epilogue C
+// batch landed, 9 the unit's first stage landed.
 #ifdef QG_TRACE
 constexpr int kTraceEv = 48;
 __device__ unsigned long long g_trace[256][kTraceEv];
@@ -662,6 +663,7 @@ __global__ void __launch_bounds__(kDmmaThreads, 1) qgemm_dmma_kernel(const __gri
             }
       }
       mbar_wait(&full[slot], phase);
+      if (kt == u.kb) QG_TR(9);  // the unit's first stage has landed
       const double2 *a2 = reinterpret_cast<const double2 *>(sA + slot * kChunkElems);
       const double2 *b2 = reinterpret_cast<const double2 *>(sB + slot * kChunkElems);
       [[maybe_unused]] const unsigned char *a8 = reinterpret_cast<const unsigned char *>(a2);

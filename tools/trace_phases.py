@@ -53,7 +53,7 @@ ctas = [c for c in range(256) if code[c, 0] == 1]
 t0 = min(t[c, 0] for c in ctas)
 t_end = max(t[c][code[c] == 6].max() for c in ctas)
 rows = []
-kl_each, epi_each, gap_each, b0_each, b1_each, tail_each = [], [], [], [], [], []  # per traced unit (the first ~46 events of each CTA)
+kl_each, epi_each, gap_each, b0_each, b1_each, tail_each, first_each = [], [], [], [], [], [], []  # per traced unit (the first ~46 events of each CTA)
 for c in ctas:
     cc, tt = code[c], t[c] - t0
     m = cc > 0
@@ -61,7 +61,13 @@ for c in ctas:
     kloop = fix = epi = 0
     for i in range(len(cc) - 1):
         d = tt[i + 1] - tt[i]
-        if cc[i] == 2 and cc[i + 1] == 3:
+        if cc[i] == 2 and cc[i + 1] == 9:
+            first_each.append(int(d))
+            k = i + 2
+            if k < len(cc) and cc[k] == 3:
+                kloop += tt[k] - tt[i]
+                kl_each.append(int(tt[k] - tt[i]))
+        elif cc[i] == 2 and cc[i + 1] == 3:
             kloop += d
             kl_each.append(int(d))
         elif cc[i] == 3 and cc[i + 1] == 4:
@@ -94,6 +100,9 @@ print(json.dumps({"n": n, "K": K, "ops": a.ops, "policy": a.policy, "beta": a.be
                   if epi_each else None,
                   "kloop_each_ns_p50": float(np.percentile(kl_each, 50)) if kl_each else None,
                   "epilogue_to_next_unit_ns_p50": float(np.percentile(gap_each, 50)) if gap_each else None,
+                  "unit_start_to_first_stage_ns_p50_p90": [float(np.percentile(first_each, 50)),
+                                                           float(np.percentile(first_each, 90))]
+                  if first_each else None,
                   "epi_batch0_wait_p50": float(np.percentile(b0_each, 50)) if b0_each else None,
                   "epi_batch0_work_batch1_wait_p50": float(np.percentile(b1_each, 50)) if b1_each else None,
                   "epi_batch1_work_p50": float(np.percentile(tail_each, 50)) if tail_each else None},
