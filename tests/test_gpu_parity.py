@@ -134,6 +134,23 @@ def test_f32_remainder_split_above_one_wave(M, N, K, S, opA, opB):
                 assert_parity(pr, got, ref, precision="f32", exact=exact)
 
 
+@pytest.mark.parametrize("M,N,K", [(1024, 1024, 16), (1024, 1024, 48), (1000, 1030, 20), (2048, 640, 64)])
+@pytest.mark.parametrize("opA,opB", [("N", "H"), ("T", "N")])
+def test_ring_epilogue_short_k_stream_k(M, N, K, opA, opB):
+    """The ring epilogue at every K (store warp): 1-4 k-tiles per
+    tile, more tiles than one wave, so whole tiles, stream-K owners (ring
+    epilogue after the fixup) and contributors (no C stages) interleave in each
+    CTA's work list and the store warp must track the producer's slot sequence
+    exactly; ragged tiles; beta != 0 (the ring) with quaternion alpha/beta, and
+    beta = 0 (per-lane stores); exact-integer inputs -> bitwise."""
+    with path_policy(qg.PATH_DIRECT):
+        for beta in (QBETA, (0, 0, 0, 0)):
+            pr = make_problem(M, N, K, opA, opB, QALPHA, beta, seed=31, ldc=M + 1)
+            assert_parity(pr, run_gpu(pr), oracle_full(pr))
+        pr = make_problem(M, N, K, opA, opB, (2, -1, 0, 3), (1, 0, -2, 1), seed=32, dist="int8")
+        assert_parity(pr, run_gpu(pr), oracle_full(pr), exact=True)
+
+
 @pytest.mark.parametrize("M,N,K", [(130, 70, 520), (64, 1, 512), (1, 64, 600), (257, 129, 1000)])
 @pytest.mark.parametrize("opA,opB", OPS)
 @pytest.mark.parametrize("policy", [qg.PATH_PACKED, qg.PATH_DIRECT], ids=["packed", "direct"])
