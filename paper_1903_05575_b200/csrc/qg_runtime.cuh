@@ -829,41 +829,23 @@ int small_pdl() {
   return v;
 }
 
-#ifndef QG_TINY_CLUSTER
-#define QG_TINY_CLUSTER 0  // 1: the tile-exact kernel splits each tile's K over a CTA pair when that doubles the SMs in use
-#endif
-// QG_TINY_CLUSTER, overridable at run time with the environment variable
-// QG_TINY_Z=0/1 (read once; for A/B measurements).
-int tiny_cluster() {
-  static const int v = [] {
-    const char *e = std::getenv("QG_TINY_Z");
-    return e ? std::atoi(e) : QG_TINY_CLUSTER;
-  }();
-  return v;
-}
-
 template <typename T>
 using SmallKernel = void (*)(qg::SmallArgs);
-// Tile-exact small kernel for this op pair (qg_small.cuh qgemm_tiny_kernel);
-// Z = 2: the cluster-pair variant.
-template <typename T, int Z>
-SmallKernel<T> tiny_kernel_z(int ops) {
+// Tile-exact small kernel for this op pair (qg_small.cuh qgemm_tiny_kernel).
+template <typename T>
+SmallKernel<T> tiny_kernel(int ops) {
   switch (ops) {
-    case 0: return qg::qgemm_tiny_kernel<T, 0, Z>;
-    case 1: return qg::qgemm_tiny_kernel<T, 1, Z>;
-    case 2: return qg::qgemm_tiny_kernel<T, 2, Z>;
-    case 4: return qg::qgemm_tiny_kernel<T, 4, Z>;
-    case 5: return qg::qgemm_tiny_kernel<T, 5, Z>;
-    case 6: return qg::qgemm_tiny_kernel<T, 6, Z>;
-    case 12: return qg::qgemm_tiny_kernel<T, 12, Z>;
-    case 13: return qg::qgemm_tiny_kernel<T, 13, Z>;
-    case 14: return qg::qgemm_tiny_kernel<T, 14, Z>;
+    case 0: return qg::qgemm_tiny_kernel<T, 0>;
+    case 1: return qg::qgemm_tiny_kernel<T, 1>;
+    case 2: return qg::qgemm_tiny_kernel<T, 2>;
+    case 4: return qg::qgemm_tiny_kernel<T, 4>;
+    case 5: return qg::qgemm_tiny_kernel<T, 5>;
+    case 6: return qg::qgemm_tiny_kernel<T, 6>;
+    case 12: return qg::qgemm_tiny_kernel<T, 12>;
+    case 13: return qg::qgemm_tiny_kernel<T, 13>;
+    case 14: return qg::qgemm_tiny_kernel<T, 14>;
     default: return nullptr;
   }
-}
-template <typename T>
-SmallKernel<T> tiny_kernel(int ops, int Z) {
-  return Z > 1 ? tiny_kernel_z<T, 2>(ops) : tiny_kernel_z<T, 1>(ops);
 }
 
 template <typename T>
@@ -910,7 +892,6 @@ int launch_small(const T *A, int64_t lda, int a_rc, int a_cj, const T *B, int64_
   const int pdl = small_pdl();
   a.pdl_trigger = pdl;
   a.per = cdiv(steps, S);
-  int64_t tz = 1;  // tiny kernel: CTAs per tile (cluster pair)
   if (tiny) {
     // the tile-exact kernel has kTinyWarps warps per CTA (2 per SM sub-partition:
     // two warps' DMMA chains interleave): its own split, by the same rule
@@ -919,27 +900,22 @@ int launch_small(const T *A, int64_t lda, int a_rc, int a_cj, const T *B, int64_
     while (S < WT && cdiv(tm, WT / (2 * S)) * tn <= per_sm * sms && steps >= 2 * QG_SMALL_MIN_STEPS * S) S *= 2;
     a.S = S;
     a.m_blocks = cdiv(tm, WT / S);
-    // one tile per CTA on fewer than half the SMs: a cluster pair per tile
-    // doubles the SMs (and SM sub-partitions) running the DMMA chains, each warp
-    // keeping >= 2 k4 steps
-    tz = (tiny_cluster() && S == WT && a.m_blocks * tn * 2 <= sms && steps >= 4 * S) ? 2 : 1;
-    a.Z = int(tz);
-    a.per = cdiv(steps, S * tz);
+    a.per = cdiv(steps, S);
   }
   cudaError_t e = cudaSuccess;
   { int ti = tstart(kSmall, st);
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(unsigned(blocks * Z));
-  if (tiny) cfg.gridDim = dim3(unsigned(a.m_blocks), unsigned(tn), unsigned(tz));
+  if (tiny) cfg.gridDim = dim3(unsigned(a.m_blocks), unsigned(tn));
   cfg.blockDim = dim3(tiny ? qg::kTinyThreads : qg::kSmallThreads);
   cfg.stream = st;
   cudaLaunchAttribute attr[2];
   int na = 0;
-  if (Z > 1 || tz > 1) {
+  if (Z > 1) {
     attr[na].id = cudaLaunchAttributeClusterDimension;
-    attr[na].val.clusterDim.x = tiny ? 1u : unsigned(Z);
+    attr[na].val.clusterDim.x = unsigned(Z);
     attr[na].val.clusterDim.y = 1;
-    attr[na].val.clusterDim.z = tiny ? unsigned(tz) : 1u;
+    attr[na].val.clusterDim.z = 1;
     ++na;
   }
   if (pdl) {  // programmatic dependent launch (qg_small.cuh griddepcontrol)
@@ -950,7 +926,7 @@ int launch_small(const T *A, int64_t lda, int a_rc, int a_cj, const T *B, int64_
   cfg.attrs = attr;
   cfg.numAttrs = unsigned(na);
   if (tiny)
-    e = cudaLaunchKernelEx(&cfg, tiny_kernel<T>(a_rc | (a_cj << 1) | (b_rc << 2) | (b_cj << 3), int(tz)), a);
+    e = cudaLaunchKernelEx(&cfg, tiny_kernel<T>(a_rc | (a_cj << 1) | (b_rc << 2) | (b_cj << 3)), a);
   else
     e = Z == 1 ? cudaLaunchKernelEx(&cfg, qg::qgemm_small_kernel<T, false>, a)
                : cudaLaunchKernelEx(&cfg, qg::qgemm_small_kernel<T, true>, a);

@@ -335,17 +335,10 @@ __device__ __forceinline__ void tiny_step(double (&acc)[4][2], const double (&qa
 #endif
 constexpr int kTinyWarps = QG_TINY_WARPS;
 constexpr int kTinyThreads = kTinyWarps * 32;
-// kZ = 2 (host: S == kTinyWarps, one tile per CTA): each tile's K is split over
-// a cluster of two CTAs on two SMs (grid z = cluster rank), so every SM
-// sub-partition runs half the DMMA chain; rank 1 adds its CTA-reduced partial
-// into rank 0's shared memory (DSMEM) behind a cluster barrier.
-template <typename T, int kOps, int kZ = 1>
+template <typename T, int kOps>
 __global__ void __launch_bounds__(kTinyThreads, (QG_TINY_DUAL ? 384 : 512) / kTinyThreads) qgemm_tiny_kernel(SmallArgs a) {
   constexpr bool a_rc = kOps & 1, a_cj = (kOps >> 1) & 1, b_rc = (kOps >> 2) & 1, b_cj = (kOps >> 3) & 1;
   __shared__ double red[kTinyWarps][32][8];
-  __shared__ double zred[kZ > 1 ? 32 : 1][8];
-  const uint32_t z = kZ > 1 ? cluster_rank() : 0u;
-  if constexpr (kZ > 1) cluster_arrive_relaxed();  // (waited on before the DSMEM store)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   // grid (m blocks, n tiles); S a power of two (host), so no divisions here
   const int S = a.S, lgS = __ffs(S) - 1;
@@ -357,7 +350,7 @@ __global__ void __launch_bounds__(kTinyThreads, (QG_TINY_DUAL ? 384 : 512) / kTi
   // (the last CTA row may hold tiles past M: no loads, no stores, but they take
   // part in the reduction barrier)
   const bool live = m0 < a.M;
-  const int64_t s0 = live ? min(steps_all, (int64_t(z) * S + part) * a.per) : 0;
+  const int64_t s0 = live ? min(steps_all, int64_t(part) * a.per) : 0;
   const int64_t s1 = live ? min(steps_all, s0 + a.per) : 0;
   const T *A = static_cast<const T *>(a.A);
   const T *B = static_cast<const T *>(a.B);
@@ -425,33 +418,15 @@ __global__ void __launch_bounds__(kTinyThreads, (QG_TINY_DUAL ? 384 : 512) / kTi
       }
     }
     __syncthreads();
-    if (part == 0)
-      for (int w = 1; w < S; ++w)
-#pragma unroll
-        for (int c = 0; c < 4; ++c) {
-          acc[c][0] += red[warp + w][lane][2 * c];
-          acc[c][1] += red[warp + w][lane][2 * c + 1];
-        }
-  }
-  if constexpr (kZ > 1) {  // then across the cluster pair (every thread takes part in its barriers)
-    cluster_wait();        // both CTAs are running: DSMEM is live
-    if (z == 1 && part == 0)
+    if (part != 0) return;
+    for (int w = 1; w < S; ++w)
 #pragma unroll
       for (int c = 0; c < 4; ++c) {
-        st_dsmem(&zred[lane][2 * c], 0, acc[c][0]);
-        st_dsmem(&zred[lane][2 * c + 1], 0, acc[c][1]);
-      }
-    cluster_arrive_release();
-    cluster_wait();
-    if (z != 0) return;
-    if (part == 0)
-#pragma unroll
-      for (int c = 0; c < 4; ++c) {
-        acc[c][0] += zred[lane][2 * c];
-        acc[c][1] += zred[lane][2 * c + 1];
+        acc[c][0] += red[warp + w][lane][2 * c];
+        acc[c][1] += red[warp + w][lane][2 * c + 1];
       }
   }
-  if (part != 0 || !live) return;
+  if (!live) return;
 #pragma unroll
   for (int i = 0; i < 2; ++i) {
     T *cp = cp0 + i * 4 * a.ldc;
