@@ -44,18 +44,9 @@
 namespace qg {
 
 #ifndef QG_DMMA_STAGES
-#define QG_DMMA_STAGES 6  // ring stages of HALF a k-tile (8 k: 16 KB of A + 16 KB of B)
+#define QG_DMMA_STAGES 3
 #endif
-// The ring holds half k-tiles: a 64 x 16 k-tile arrives as two stages of 8 k, so
-// six 32 KB stages (192 KB, as three whole-k-tile stages were) keep every load
-// issued at least a stage ahead across a tile switch -- the two C stages of an
-// epilogue no longer hold the slots the next tile's first k-tile needs (with
-// three whole stages that load could only start once the last k-tile's slot
-// freed: ~1 us per tile at c4, tools/trace_phases.py).
 constexpr int kStages = QG_DMMA_STAGES;
-constexpr int kHalfK = kBK / 2;                   // k per stage
-constexpr int kStageElems = kChunkElems / 2;      // doubles per operand per stage (16 KB)
-constexpr int kSlotElems = 2 * kStageElems;       // one stage = [A half][B half] (32 KB, contiguous)
 constexpr int kConsumerWarps = 8;
 constexpr int kConsumerThreads = kConsumerWarps * 32;
 // 8 consumer warps + a producer warpgroup; setmaxnreg moves registers from the
@@ -69,6 +60,14 @@ constexpr int kConsumerRegs = 232;
 #ifndef QG_C_RING
 #define QG_C_RING 1  // epilogue C tiles through the ring by TMA (see produce_c_stage)
 #endif
+#ifndef QG_C_STORE_WARP
+// 1: a producer-warpgroup warp issues the ring epilogue's TMA stores, waits for
+// the TMA unit to read each box and hands the slot back to the producer, so the
+// consumers go on to the next tile as soon as they have written their
+// quaternions (no CTA-wide barriers, no wait for the store's reads); 0: consumer
+// thread 0 stores behind two consumer barriers and all consumers wait for the reads
+#define QG_C_STORE_WARP 1
+#endif
 #ifndef QG_C_PREFETCH_BULK
 #define QG_C_PREFETCH_BULK 1  // 1: the producer lane bulk-prefetches C tiles; 0: consumer lanes prefetch per quaternion
 #endif
@@ -78,7 +77,7 @@ constexpr int kConsumerRegs = 232;
 constexpr int kGroupM = QG_GROUP_M;  // rasterisation: M-tiles per group (L2 reuse of panels)
 // ring + barriers + 1 KB so the ring can start on a 1024-byte boundary
 // (barriers: full, empty and, for the ring epilogue's store warp, cdone per slot)
-constexpr size_t kDmmaSmemBytes = size_t(kStages) * kSlotElems * sizeof(double) + 3 * kStages * 8 + 1024;
+constexpr size_t kDmmaSmemBytes = size_t(kStages) * 2 * kChunkElems * sizeof(double) + 3 * kStages * 8 + 1024;
 
 // How the ring is fed (kernel template parameter).
 // (a third feed -- all 128 producer threads de-interleaving with 16-byte
@@ -281,7 +280,6 @@ __device__ __forceinline__ void tma_store_3d(const CUtensorMap *tm, const void *
 struct Producer {
   WorkIter it;
   int64_t kt, ke;
-  int kh;          // half of k-tile kt to fill next (0: k 0-7, 1: k 8-15)
   int64_t mt, nt;  // TMA feed: tile coordinates of the current unit
   const double *a_src, *b_src;
   int slot;
@@ -293,26 +291,26 @@ struct Producer {
 };
 
 // ---- C through the ring (QG_C_RING): a unit that runs the epilogue is
-// followed in the ring by four C stages -- stage h = rows 16h..16h+15 of the
-// 64 x 64 tile, one 32 KB TMA box ([row 16][col 64][4 comps], 32-byte swizzle)
-// filling the stage, i.e. the quaternions of the four consumer warps of half
-// wm = h / 2.  Those warps read C from shared memory and write the results back
-// in place; the store warp (c_store_loop) TMA-stores the box (the TMA unit clips
+// followed in the ring by two C stages -- batch h = rows 16h.. and 32 + 16h..
+// of the 64 x 64 tile, one 32 KB TMA box each ([row 16][col 64][4 comps],
+// 32-byte swizzle) into the slot's A and B halves, i.e. the quaternions consumer
+// half wm of batch h owns.  The consumers read C from shared memory, write the
+// results back in place and one thread TMA-stores the boxes (the TMA unit clips
 // the M / N edges): the epilogue's global traffic runs at TMA rates instead of
 // 128-bit per-lane loads and stores with 64 KB in flight per batch.
 // Without a C read (beta = 0, not QHERK) there are no C stages: the plain
 // per-lane store epilogue is faster there.  QHERK's off-diagonal tiles lie
 // wholly inside its triangle; its diagonal tiles never take the ring.
-constexpr uint32_t kCBoxBytes = 16u * 64u * 32u;  // 32 KB = one stage
-constexpr int kCStages = 4;
-__device__ __forceinline__ void produce_c_stage(Producer &p, const DmmaArgs &args, double *ring, uint64_t *full,
-                                                uint64_t *empty) {
-  const int h = kCStages - p.c_left;
+constexpr uint32_t kCBoxBytes = 16u * 64u * 32u;  // 32 KB = one slot half
+__device__ __forceinline__ void produce_c_stage(Producer &p, const DmmaArgs &args, double *sA, double *sB,
+                                                uint64_t *full, uint64_t *empty) {
+  const int h = 2 - p.c_left;
   if (p.fills >= kStages) mbar_wait(&empty[p.slot], p.phase ^ 1u);
   if (p.c_load) {
-    mbar_arrive_expect_tx(&full[p.slot], kCBoxBytes);
+    mbar_arrive_expect_tx(&full[p.slot], 2 * kCBoxBytes);
     const int n0 = int(p.nt * kBR), r0 = int(p.mt * kBR) + 16 * h;
-    tma_load_3d(ring + p.slot * kSlotElems, &args.tmC, 0, n0, r0, &full[p.slot]);
+    tma_load_3d(sA + p.slot * kChunkElems, &args.tmC, 0, n0, r0, &full[p.slot]);
+    tma_load_3d(sB + p.slot * kChunkElems, &args.tmC, 0, n0, r0 + 32, &full[p.slot]);
   } else {  // beta = 0 (QHERK off-diagonal tile): the box is overwritten whole
     mbar_arrive(&full[p.slot]);
   }
@@ -331,7 +329,7 @@ __device__ __forceinline__ bool ring_epilogue(const DmmaArgs &a, int64_t mt, int
 template <bool kRing>
 __device__ __forceinline__ void producer_unit_c(Producer &p, const DmmaArgs &a, const Unit &u) {
   p.c_load = !a.sc.beta_zero;
-  p.c_left = (kRing && u.kb == 0 && ring_epilogue(a, p.mt, p.nt)) ? kCStages : 0;
+  p.c_left = (kRing && u.kb == 0 && ring_epilogue(a, p.mt, p.nt)) ? 2 : 0;
 }
 
 // L2 prefetch of the C tile (mt, nt) by the TMA engine: one bulk prefetch per
@@ -355,12 +353,10 @@ __device__ __forceinline__ void producer_unit_prefetch(Producer &p, const DmmaAr
                     : int64_t(-1);
 }
 
-// Issue the next fill (bulk copies of one half of an A and a B chunk: the
-// chunk layout [ks 4][i 8][pp 2][lane 32][e 2] keeps k4 steps 0-1 and 2-3
-// contiguous); false when done.
-__device__ __forceinline__ bool produce_next(Producer &p, const DmmaArgs &args, double *ring, uint64_t *full,
-                                             uint64_t *empty) {
-  constexpr uint32_t kBytes = kStageElems * sizeof(double);
+// Issue the next fill (bulk copies of one A and one B chunk); false when done.
+__device__ __forceinline__ bool produce_next(Producer &p, const DmmaArgs &args, double *sA, double *sB,
+                                             uint64_t *full, uint64_t *empty) {
+  constexpr uint32_t kBytes = kChunkElems * sizeof(double);
   while (p.kt >= p.ke) {
     Unit u;
     if (!p.it.next(args, u)) return false;
@@ -368,19 +364,16 @@ __device__ __forceinline__ bool produce_next(Producer &p, const DmmaArgs &args, 
     p.a_src = args.Ap + p.mt * args.KT * kChunkElems;
     p.b_src = args.Bp + p.nt * args.KT * kChunkElems;
     p.kt = u.kb;
-    p.kh = 0;
     p.ke = u.ke;
     producer_unit_prefetch<false>(p, args, u);
   }
-  if (p.kt == p.c_pref_kt && p.kh == 0) prefetch_c_tile(args, p.mt, p.nt);
+  if (p.kt == p.c_pref_kt) prefetch_c_tile(args, p.mt, p.nt);
   if (p.fills >= kStages) mbar_wait(&empty[p.slot], p.phase ^ 1u);
   mbar_arrive_expect_tx(&full[p.slot], 2 * kBytes);
-  double *st = ring + p.slot * kSlotElems;
-  const int64_t off = p.kt * kChunkElems + p.kh * kStageElems;
-  bulk_g2s(st, p.a_src + off, kBytes, &full[p.slot]);
-  bulk_g2s(st + kStageElems, p.b_src + off, kBytes, &full[p.slot]);
+  bulk_g2s(sA + p.slot * kChunkElems, p.a_src + p.kt * kChunkElems, kBytes, &full[p.slot]);
+  bulk_g2s(sB + p.slot * kChunkElems, p.b_src + p.kt * kChunkElems, kBytes, &full[p.slot]);
   if (++p.slot == kStages) { p.slot = 0; p.phase ^= 1u; }
-  if (++p.kh == 2) { p.kh = 0; ++p.kt; }
+  ++p.kt;
   ++p.fills;
   return true;
 }
@@ -390,9 +383,8 @@ __device__ __forceinline__ bool produce_next(Producer &p, const DmmaArgs &args, 
 // k, row); out-of-range rows / k are zero-filled by the TMA unit (the padding
 // of Alg. 2).  The tile lands in smem in storage order, 32-byte
 // swizzled (one quaternion = one 32-byte swizzle row; the 128-byte mode would
-// pad every 32-byte row to 128 bytes): element (r, k, c) of a 64-row x 8-k
-// half tile (one ring stage) at
-//   lin = ((k*64 + r)*4 + c)*8   (rows contiguous)   or   ((r*8 + k)*4 + c)*8
+// pad every 32-byte row to 128 bytes): element (r, k, c) of the 64 x 16 tile at
+//   lin = ((k*64 + r)*4 + c)*8   (rows contiguous)   or   ((r*16 + k)*4 + c)*8
 //   swz = lin ^ (((lin >> 7) & 1) << 4)   (16-byte half swapped on odd 128 B)
 // so the de-interleave into DMMA fragments is done by the consumers' addresses
 // (layout verified element by element by tools/microbench/tma_probe.cu).  A
@@ -402,41 +394,39 @@ __device__ __forceinline__ bool produce_next(Producer &p, const DmmaArgs &args, 
 // packing, which auto pays only where the sweep shows it wins.
 
 template <bool kG4>
-__device__ __forceinline__ bool produce_next_tma(Producer &p, const DmmaArgs &args, double *ring, uint64_t *full,
-                                                 uint64_t *empty) {
-  constexpr uint32_t kBytes = kStageElems * sizeof(double);
+__device__ __forceinline__ bool produce_next_tma(Producer &p, const DmmaArgs &args, double *sA, double *sB,
+                                                 uint64_t *full, uint64_t *empty) {
+  constexpr uint32_t kBytes = kChunkElems * sizeof(double);
   while (p.kt >= p.ke && p.c_left == 0) {
     Unit u;
     if (!p.it.next(args, u)) return false;
     work_tile(args, u.t, p.mt, p.nt);
     p.kt = u.kb;
-    p.kh = 0;
     p.ke = u.ke;
     producer_unit_prefetch<QG_C_RING>(p, args, u);
     producer_unit_c<QG_C_RING>(p, args, u);
   }
   if (p.kt >= p.ke) {
-    produce_c_stage(p, args, ring, full, empty);
+    produce_c_stage(p, args, sA, sB, full, empty);
     return true;
   }
-  if (p.kt == p.c_pref_kt && p.kh == 0) prefetch_c_tile(args, p.mt, p.nt);
+  if (p.kt == p.c_pref_kt) prefetch_c_tile(args, p.mt, p.nt);
   if (p.fills >= kStages) mbar_wait(&empty[p.slot], p.phase ^ 1u);
   mbar_arrive_expect_tx(&full[p.slot], 2 * kBytes);
-  double *sa = ring + p.slot * kSlotElems, *sb = sa + kStageElems;
-  const int k0 = int(p.kt * kBK) + kHalfK * p.kh, ra = int(p.mt * kBR), rb = int(p.nt * kBR);
+  const int k0 = int(p.kt * kBK), ra = int(p.mt * kBR), rb = int(p.nt * kBR);
   if constexpr (kG4) {  // group maps (16 doubles, k, row/4) or (16 doubles, k/4, row)
-    if (args.a_rc) tma_load_3d(sa, &args.tmA, 0, k0, ra / 4, &full[p.slot]);
-    else           tma_load_3d(sa, &args.tmA, 0, k0 / 4, ra, &full[p.slot]);
-    if (args.b_rc) tma_load_3d(sb, &args.tmB, 0, k0, rb / 4, &full[p.slot]);
-    else           tma_load_3d(sb, &args.tmB, 0, k0 / 4, rb, &full[p.slot]);
+    if (args.a_rc) tma_load_3d(sA + p.slot * kChunkElems, &args.tmA, 0, k0, ra / 4, &full[p.slot]);
+    else           tma_load_3d(sA + p.slot * kChunkElems, &args.tmA, 0, k0 / 4, ra, &full[p.slot]);
+    if (args.b_rc) tma_load_3d(sB + p.slot * kChunkElems, &args.tmB, 0, k0, rb / 4, &full[p.slot]);
+    else           tma_load_3d(sB + p.slot * kChunkElems, &args.tmB, 0, k0 / 4, rb, &full[p.slot]);
   } else {
-    if (args.a_rc) tma_load_3d(sa, &args.tmA, 0, ra, k0, &full[p.slot]);
-    else           tma_load_3d(sa, &args.tmA, 0, k0, ra, &full[p.slot]);
-    if (args.b_rc) tma_load_3d(sb, &args.tmB, 0, rb, k0, &full[p.slot]);
-    else           tma_load_3d(sb, &args.tmB, 0, k0, rb, &full[p.slot]);
+    if (args.a_rc) tma_load_3d(sA + p.slot * kChunkElems, &args.tmA, 0, ra, k0, &full[p.slot]);
+    else           tma_load_3d(sA + p.slot * kChunkElems, &args.tmA, 0, k0, ra, &full[p.slot]);
+    if (args.b_rc) tma_load_3d(sB + p.slot * kChunkElems, &args.tmB, 0, rb, k0, &full[p.slot]);
+    else           tma_load_3d(sB + p.slot * kChunkElems, &args.tmB, 0, k0, rb, &full[p.slot]);
   }
   if (++p.slot == kStages) { p.slot = 0; p.phase ^= 1u; }
-  if (++p.kh == 2) { p.kh = 0; ++p.kt; }
+  ++p.kt;
   ++p.fills;
   return true;
 }
@@ -444,32 +434,32 @@ __device__ __forceinline__ bool produce_next_tma(Producer &p, const DmmaArgs &ar
 __device__ __forceinline__ void mbar_arrive_n(uint64_t *bar, uint32_t n) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(n) : "memory");
 }
-// The ring epilogue's stores (the "store warp").  This lane walks the CTA's
-// work list like the producer, tracking the ring slot (a unit of k-tiles
-// [kb, ke) occupies 2 (ke - kb) half-k-tile fills, then four C stages if it
-// runs the ring epilogue); per C stage it waits until the four consumer warps
-// owning its rows have written their quaternions (cdone), TMA-stores the box,
-// waits until the TMA unit has read it and returns the slot to the producer
-// (one arrival counting for every consumer warp).  Its bulk-store groups are
-// completed before the CTA exits.
-__device__ __forceinline__ void c_store_loop(const DmmaArgs &args, const SkSplit &sp, double *ring, uint64_t *empty,
-                                             uint64_t *cdone) {
+// QG_C_STORE_WARP: the ring epilogue's stores.  This lane walks the CTA's work
+// list like the producer, tracking the ring slot (a unit of k-tiles [kb, ke)
+// occupies ke - kb fills, then two C stages if it runs the ring epilogue); per
+// C stage it waits until all consumer warps have written their quaternions
+// (cdone), TMA-stores the two boxes, waits until the TMA unit has read them and
+// returns the slot to the producer (one arrival counting for every consumer
+// warp).  Its bulk-store groups are completed before the CTA exits.
+__device__ __forceinline__ void c_store_loop(const DmmaArgs &args, const SkSplit &sp, double *sA, double *sB,
+                                             uint64_t *empty, uint64_t *cdone) {
   WorkIter it = make_iter(args, sp);
   Unit u;
   int slot = 0;
   uint32_t cph = 0;  // parity of each slot's cdone barrier
   while (it.next(args, u)) {
-    slot = int((int64_t(slot) + 2 * (u.ke - u.kb)) % kStages);
+    slot = int((int64_t(slot) + (u.ke - u.kb)) % kStages);
     if (u.kb != 0) continue;  // stream-K contributor: no epilogue here
     int64_t mt, nt;
     work_tile(args, u.t, mt, nt);
     if (!ring_epilogue(args, mt, nt)) continue;
 #pragma unroll 1
-    for (int h = 0; h < kCStages; ++h) {
+    for (int h = 0; h < 2; ++h) {
       mbar_wait(&cdone[slot], (cph >> slot) & 1u);
       cph ^= 1u << slot;
       const int n0 = int(nt * kBR), r0 = int(mt * kBR) + 16 * h;
-      tma_store_3d(&args.tmC, ring + slot * kSlotElems, 0, n0, r0);
+      tma_store_3d(&args.tmC, sA + slot * kChunkElems, 0, n0, r0);
+      tma_store_3d(&args.tmC, sB + slot * kChunkElems, 0, n0, r0 + 32);
       asm volatile("cp.async.bulk.commit_group;\n" ::: "memory");
       asm volatile("cp.async.bulk.wait_group.read 0;\n" ::: "memory");
       mbar_arrive_n(&empty[slot], kConsumerWarps);
@@ -479,14 +469,18 @@ __device__ __forceinline__ void c_store_loop(const DmmaArgs &args, const SkSplit
   asm volatile("cp.async.bulk.wait_group 0;\n" ::: "memory");
 }
 
-// Per-lane part of the fragment offsets in a half tile (one stage, 8 k).  A
-// lane reads rows r0 + 8i (r0 = its first row) at k = 4ks + kl (ks = 0, 1: the
-// stage's two k4 steps).  Rows contiguous: the swizzle bit (address bit 7) is
-// bit 2 of the row, the same for every i, so
+// Byte offset of the 16-byte pair (components 2pp, 2pp+1) of (r, k) in a TMA tile.
+__device__ __forceinline__ uint32_t tma_tile_off(int rc, int r, int k, int pp) {
+  const uint32_t lin = rc ? uint32_t(((k * kBR + r) * 4 + 2 * pp) * 8) : uint32_t(((r * kBK + k) * 4 + 2 * pp) * 8);
+  return lin ^ (((lin >> 7) & 1u) << 4);
+}
+
+// Per-lane part of the fragment offsets in a TMA tile.  A lane reads rows
+// r0 + 8i (r0 = its first row) at k = 4ks + kl.  Rows contiguous: the swizzle
+// bit (address bit 7) is bit 2 of the row, the same for every i, so
 //   off = r0*32 + kl*2048 + ks*8192 + i*256 + ((16 pp) ^ x),   x = 16 * bit2(r0);
-// k contiguous (rows of 8 quaternions): the swizzle bit is bit 2 of k = bit 0
-// of ks, so
-//   off = r0*256 + kl*32 + i*2048 + ks*128 + 16 (pp ^ (ks & 1)).
+// k contiguous: the swizzle bit is bit 2 of k = bit 0 of ks, so
+//   off = r0*512 + kl*32 + i*4096 + ks*128 + 16 (pp ^ (ks & 1)).
 // Everything but `base` / `x` is a compile-time constant of the unrolled loops.
 struct TmaLane {
   uint32_t base, x;
@@ -495,66 +489,60 @@ struct TmaLane {
 __device__ __forceinline__ TmaLane tma_lane(int rc, int r0, int kl) {
   TmaLane t;
   t.rc = rc;
-  t.base = rc ? uint32_t(r0 * 32 + kl * 2048) : uint32_t(r0 * 256 + kl * 32);
+  t.base = rc ? uint32_t(r0 * 32 + kl * 2048) : uint32_t(r0 * 512 + kl * 32);
   t.x = rc ? uint32_t(((r0 >> 2) & 1) << 4) : 0u;
   return t;
 }
 __device__ __forceinline__ uint32_t tma_frag_off(const TmaLane &t, int ks, int i, int pp) {
   return t.rc ? t.base + uint32_t(ks * 8192 + i * 256) + (uint32_t(pp << 4) ^ t.x)
-              : t.base + uint32_t(i * 2048 + ks * 128 + ((pp ^ (ks & 1)) << 4));
+              : t.base + uint32_t(i * 4096 + ks * 128 + ((pp ^ (ks & 1)) << 4));
 }
 
 // ---- kFeedTma128: both operands as tiles of 4-quaternion groups.  The map's
 // inner dimension is 16 doubles = 4 consecutive quaternions along the
 // operand's contiguous index = one 128-byte row of the 128-byte swizzle (no
-// padding); the outer dimensions are the other index and the group index.  A
-// stage holds a half tile (8 k):
-//   rows contiguous: smem [r/4][k][r%4][c]   lin = ((r>>2)*8 + k)*128 + (r&3)*32 + 8c
-//   k contiguous:    smem [r][k/4][k%4][c]   lin = (r*2 + (k>>2))*128 + (k&3)*32 + 8c
+// padding); the outer dimensions are the other index and the group index
+// (layouts checked element by element by tools/microbench/tma_probe_g4.cu):
+//   rows contiguous: smem [r/4][k][r%4][c]   lin = ((r>>2)*16 + k)*128 + (r&3)*32 + 8c
+//   k contiguous:    smem [r][k/4][k%4][c]   lin = (r*4 + (k>>2))*128 + (k&3)*32 + 8c
 //   swz = lin ^ (((lin >> 7) & 7) << 4)      (16-byte chunk ^= 128-byte row & 7)
-// so the 16-byte chunk of (r, k, component pair pp) is
-//   rows contiguous: (2(r&3) + pp) ^ k
-//   k contiguous:    (2(k&3) + pp) ^ (2r + (k>>2)) & 7  =  f(k) ^ (2r & 7) ^ pp,  f(k) = 2(k&3) ^ (k>>2).
 // A quarter-warp's 128-bit loads cover fragment rows rho, rho+1 (rho even) x
-// the 4 k of a k4 step.  The kernel feeds k4 step ks of the stage with the k
-// set P[ks] -- P[0] = {0,3,4,7}, P[1] = {1,2,5,6}, lane kl taking P[ks][kl]; a
-// bijection of the stage's 8 k applied to A and B alike, so the k-sum is
-// unchanged -- because those sets are the ones whose 8 lanes hit 8 distinct
-// bank groups in BOTH layouts: rows contiguous needs S and S ^ 2 disjoint (the
-// two rows differ by 2 in 2(r&3)), k contiguous needs f(S) and f(S) ^ 2
-// disjoint (2r & 7 differs by 2); among the 4-sets of 0..7 exactly four meet
-// both: {0,3,4,7}, {1,2,5,6} (used) and {0,3,5,6}, {1,2,4,7} (checked by brute
-// force over every lane, row block, k4 step and fragment).  (The whole-k-tile layout of the 3-stage ring used kperm(ks, kl) = 8(ks>>1) +
-// 2(ks&1) + {0,1,4,5}[kl]; with 8 k per row group that set collides in the
-// k-contiguous layout.)  Offsets: off = (b[ks] ^ (pp << 4)) + i*2048 with the
-// per-lane
-//   rows contiguous: b = ((rb>>2) + (rho>>2))*1024 + k*128 + ((2(rho&3) ^ k) << 4)
-//   k contiguous:    b = (rb + rho)*256 + (k>>2)*128 + ((2(k&3) ^ ((2rho + (k>>2)) & 7)) << 4)
-// (bits 4-6 of the rest are zero, so the pp XOR never carries).  The host
-// takes this feed when the group extents are whole: M (N) % 4 == 0 for a
-// rows-contiguous op(A) (op(B)), K % 4 == 0 for a k-contiguous one; otherwise
-// kFeedTma.
+// the 4 k of a k4 step.  In the natural k order those 4 k XOR the chunks with
+// {0,1,2,3} (rows contiguous) or sit in one 128-byte row (k contiguous), and
+// the two rows collide.  This kernel therefore feeds k4 step ks with tile k =
+// kperm(ks, kl) = 8(ks>>1) + 2(ks&1) + kk, kk = (kl&1) + 4(kl>>1) in {0,1,4,5}
+// -- a bijection of the tile's 16 k applied to A and B alike, so the k-sum is
+// unchanged -- and the 8 lanes hit 8 distinct bank groups in both layouts
+// (rows contiguous: chunks 2q ^ kk, q = rho & 3 in {0,1} or {2,3}; k
+// contiguous: the 4 k span two 128-byte rows and rho & 1 flips chunk bit 2).
+// (Permuting rows instead needs the permutation in the epilogue: measured
+// slower at c4.)  The host takes this feed when the group extents are whole:
+// M (N) % 4 == 0 for a rows-contiguous op(A) (op(B)), K % 4 == 0 for a
+// k-contiguous one; otherwise kFeedTma.
 struct G4Lane {
-  uint32_t b[2];  // per k4 step of the stage
+  uint32_t base, x;
 };
-__device__ __forceinline__ int g4_k(int ks, int kl) {  // P[ks][kl]
-  return ks == 0 ? ((kl & 1) ? 3 : 0) + 4 * (kl >> 1) : ((kl & 1) ? 2 : 1) + 4 * (kl >> 1);
-}
 // rb: first row of the warp's fragments (a multiple of 8); rho = lane / 4, kl = lane % 4
 __device__ __forceinline__ G4Lane g4_lane(int rc, int rb, int rho, int kl) {
+  const int kk = (kl & 1) + 4 * (kl >> 1);
   G4Lane t;
-#pragma unroll
-  for (int ks = 0; ks < 2; ++ks) {
-    const int k = g4_k(ks, kl);
-    t.b[ks] = rc ? uint32_t(((rb >> 2) + (rho >> 2)) * 1024 + k * 128 + (((2 * (rho & 3)) ^ k) << 4))
-                 : uint32_t((rb + rho) * 256 + (k >> 2) * 128 + (((2 * (k & 3)) ^ ((2 * rho + (k >> 2)) & 7)) << 4));
+  if (rc) {  // chunk = (2q + pp) ^ (k & 7), k & 7 = 2(ks & 1) + kk
+    t.base = uint32_t(((rb >> 2) + (rho >> 2)) * 2048 + kk * 128);
+    t.x = uint32_t(((2 * (rho & 3)) ^ kk) << 4);
+  } else {   // k = 4h + q: h = 2(ks >> 1) + (kl >> 1), q = 2(ks & 1) + (kl & 1);
+             // chunk = (2q + pp) ^ (4(rho & 1) + (h & 3))
+    t.base = uint32_t((rb + rho) * 512 + (kl >> 1) * 128);
+    t.x = uint32_t((2 * (kl & 1) ^ 4 * (rho & 1) ^ (kl >> 1)) << 4);
   }
   return t;
 }
 // Byte offset of the 16-byte pair (components 2pp, 2pp+1) of fragment i
-// (rows rb + 8i + rho) at k = P[ks][kl].
-__device__ __forceinline__ uint32_t g4_frag_off(const G4Lane &t, int ks, int i, int pp) {
-  return (t.b[ks] ^ uint32_t(pp << 4)) + uint32_t(i * 2048);
+// (rows rb + 8i + rho) at k = kperm(ks, kl); rc is a compile-time constant.
+__device__ __forceinline__ uint32_t g4_frag_off(int rc, const G4Lane &t, int ks, int i, int pp) {
+  return rc ? t.base + uint32_t(i * 4096 + (8 * (ks >> 1) + 2 * (ks & 1)) * 128) +
+                  (t.x ^ uint32_t((pp ^ (2 * (ks & 1))) << 4))
+            : t.base + uint32_t(i * 4096 + (ks >> 1) * 256) +
+                  (t.x ^ uint32_t((4 * (ks & 1) ^ 2 * ((ks >> 1) & 1) ^ pp) << 4));
 }
 
 // kFeed: kFeedPacked (conj applied by the pack kernel; CA = CB = false), or a
@@ -574,10 +562,11 @@ __global__ void __launch_bounds__(kDmmaThreads, 1) qgemm_dmma_kernel(const __gri
   // (offset arithmetic on the shared array, not an integer round trip, so the
   // compiler keeps shared-space loads: LDS, not generic LD)
   unsigned char *smem_raw = smem_dyn + ((1024u - (smem_u32(smem_dyn) & 1023u)) & 1023u);
-  double *ring = reinterpret_cast<double *>(smem_raw);  // kStages x [A half][B half]
-  uint64_t *full = reinterpret_cast<uint64_t *>(ring + kStages * kSlotElems);
+  double *sA = reinterpret_cast<double *>(smem_raw);
+  double *sB = sA + kStages * kChunkElems;
+  uint64_t *full = reinterpret_cast<uint64_t *>(sB + kStages * kChunkElems);
   uint64_t *empty = full + kStages;
-  uint64_t *cdone = empty + kStages;  // the owning consumer warps wrote a C stage (ring epilogue)
+  uint64_t *cdone = empty + kStages;  // QG_C_STORE_WARP: consumers wrote a C stage (ring epilogue)
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -602,7 +591,6 @@ __global__ void __launch_bounds__(kDmmaThreads, 1) qgemm_dmma_kernel(const __gri
   Producer prod;
   prod.it = make_iter(args, sp);
   prod.kt = 0;
-  prod.kh = 0;
   prod.ke = 0;
   prod.slot = 0;
   prod.phase = 0;
@@ -615,12 +603,13 @@ __global__ void __launch_bounds__(kDmmaThreads, 1) qgemm_dmma_kernel(const __gri
     asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;\n" ::"n"(kProducerRegs));
     if constexpr (kFeed == kFeedTma || kFeed == kFeedTma128) {
       if (warp == kConsumerWarps && lane == 0)
-        while (produce_next_tma<kFeed == kFeedTma128>(prod, args, ring, full, empty)) {
+        while (produce_next_tma<kFeed == kFeedTma128>(prod, args, sA, sB, full, empty)) {
         }
-      if (kRing && args.c_ring && warp == kConsumerWarps + 1 && lane == 0) c_store_loop(args, sp, ring, empty, cdone);
+      if (kRing && QG_C_STORE_WARP && args.c_ring && warp == kConsumerWarps + 1 && lane == 0)
+        c_store_loop(args, sp, sA, sB, empty, cdone);
     } else {
       if (warp == kConsumerWarps && lane == 0)
-        while (produce_next(prod, args, ring, full, empty)) {
+        while (produce_next(prod, args, sA, sB, full, empty)) {
         }
     }
     return;
@@ -673,69 +662,66 @@ __global__ void __launch_bounds__(kDmmaThreads, 1) qgemm_dmma_kernel(const __gri
                 asm volatile("prefetch.global.L2 [%0];\n" ::"l"(args.C + 4 * (row + col * args.ldc)));
             }
       }
+      mbar_wait(&full[slot], phase);
+      if (kt == u.kb) QG_TR(9);  // the unit's first stage has landed
+      const double2 *a2 = reinterpret_cast<const double2 *>(sA + slot * kChunkElems);
+      const double2 *b2 = reinterpret_cast<const double2 *>(sB + slot * kChunkElems);
+      [[maybe_unused]] const unsigned char *a8 = reinterpret_cast<const unsigned char *>(a2);
+      [[maybe_unused]] const unsigned char *b8 = reinterpret_cast<const unsigned char *>(b2);
 #pragma unroll
-      for (int hk = 0; hk < 2; ++hk) {  // the k-tile's two stages (k 0-7, 8-15)
-        mbar_wait(&full[slot], phase);
-        if (kt == u.kb && hk == 0) QG_TR(9);  // the unit's first stage has landed
-        const double2 *a2 = reinterpret_cast<const double2 *>(ring + slot * kSlotElems);
-        const double2 *b2 = reinterpret_cast<const double2 *>(ring + slot * kSlotElems + kStageElems);
-        [[maybe_unused]] const unsigned char *a8 = reinterpret_cast<const unsigned char *>(a2);
-        [[maybe_unused]] const unsigned char *b8 = reinterpret_cast<const unsigned char *>(b2);
+      for (int ks = 0; ks < kBK / 4; ++ks) {
+        double af[4][4], bf[2][4], bn[2][4];
 #pragma unroll
-        for (int ks = 0; ks < kHalfK / 4; ++ks) {
-          double af[4][4], bf[2][4], bn[2][4];
+        for (int ii = 0; ii < 4; ++ii)
+#pragma unroll
+          for (int pp = 0; pp < 2; ++pp) {
+            double2 v;
+            if constexpr (kFeed == kFeedTma)
+              v = *reinterpret_cast<const double2 *>(a8 + tma_frag_off(ta, ks, ii, pp));
+            else if constexpr (kFeed == kFeedTma128)
+              v = *reinterpret_cast<const double2 *>(a8 + g4_frag_off(kRC & 1, ga, ks, ii, pp));
+            else
+              v = a2[((ks * 8 + wm * 4 + ii) * 2 + pp) * 32 + lane];
+            af[ii][2 * pp] = v.x;
+            af[ii][2 * pp + 1] = v.y;
+          }
+#pragma unroll
+        for (int jj = 0; jj < 2; ++jj)
+#pragma unroll
+          for (int pp = 0; pp < 2; ++pp) {
+            double2 v;
+            if constexpr (kFeed == kFeedTma)
+              v = *reinterpret_cast<const double2 *>(b8 + tma_frag_off(tb, ks, jj, pp));
+            else if constexpr (kFeed == kFeedTma128)
+              v = *reinterpret_cast<const double2 *>(b8 + g4_frag_off((kRC >> 1) & 1, gb, ks, jj, pp));
+            else
+              v = b2[((ks * 8 + wn * 2 + jj) * 2 + pp) * 32 + lane];
+            bf[jj][2 * pp] = v.x;
+            bf[jj][2 * pp + 1] = v.y;
+          }
+#pragma unroll
+        for (int jj = 0; jj < 2; ++jj)
+#pragma unroll
+          for (int s = 0; s < 4; ++s) bn[jj][s] = -bf[jj][s];
+
+        // 16 DMMA per (m8, n8) tile; p outermost so consecutive DMMAs hit
+        // different accumulators.
+#pragma unroll
+        for (int p = 0; p < 4; ++p)
 #pragma unroll
           for (int ii = 0; ii < 4; ++ii)
 #pragma unroll
-            for (int pp = 0; pp < 2; ++pp) {
-              double2 v;
-              if constexpr (kFeed == kFeedTma)
-                v = *reinterpret_cast<const double2 *>(a8 + tma_frag_off(ta, ks, ii, pp));
-              else if constexpr (kFeed == kFeedTma128)
-                v = *reinterpret_cast<const double2 *>(a8 + g4_frag_off(ga, ks, ii, pp));
-              else
-                v = a2[((ks * 8 + wm * 4 + ii) * 2 + pp) * 32 + lane];
-              af[ii][2 * pp] = v.x;
-              af[ii][2 * pp + 1] = v.y;
-            }
+            for (int jj = 0; jj < 2; ++jj)
 #pragma unroll
-          for (int jj = 0; jj < 2; ++jj)
-#pragma unroll
-            for (int pp = 0; pp < 2; ++pp) {
-              double2 v;
-              if constexpr (kFeed == kFeedTma)
-                v = *reinterpret_cast<const double2 *>(b8 + tma_frag_off(tb, ks, jj, pp));
-              else if constexpr (kFeed == kFeedTma128)
-                v = *reinterpret_cast<const double2 *>(b8 + g4_frag_off(gb, ks, jj, pp));
-              else
-                v = b2[((ks * 8 + wn * 2 + jj) * 2 + pp) * 32 + lane];
-              bf[jj][2 * pp] = v.x;
-              bf[jj][2 * pp + 1] = v.y;
-            }
-#pragma unroll
-          for (int jj = 0; jj < 2; ++jj)
-#pragma unroll
-            for (int s = 0; s < 4; ++s) bn[jj][s] = -bf[jj][s];
-
-          // 16 DMMA per (m8, n8) tile; p outermost so consecutive DMMAs hit
-          // different accumulators.
-#pragma unroll
-          for (int p = 0; p < 4; ++p)
-#pragma unroll
-            for (int ii = 0; ii < 4; ++ii)
-#pragma unroll
-              for (int jj = 0; jj < 2; ++jj)
-#pragma unroll
-                for (int c = 0; c < 4; ++c) {
-                  const int s = p ^ c;
-                  const bool neg = hneg(p, s) ^ (CA && p != 0) ^ (CB && s != 0);
-                  dmma_8x8x4(acc[ii][jj][c], af[ii][p], neg ? bn[jj][s] : bf[jj][s]);
-                }
-        }
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&empty[slot]);
-        if (++slot == kStages) { slot = 0; phase ^= 1u; }
+              for (int c = 0; c < 4; ++c) {
+                const int s = p ^ c;
+                const bool neg = hneg(p, s) ^ (CA && p != 0) ^ (CB && s != 0);
+                dmma_8x8x4(acc[ii][jj][c], af[ii][p], neg ? bn[jj][s] : bf[jj][s]);
+              }
       }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[slot]);
+      if (++slot == kStages) { slot = 0; phase ^= 1u; }
     }
 
     QG_TR(3);
@@ -799,46 +785,65 @@ __global__ void __launch_bounds__(kDmmaThreads, 1) qgemm_dmma_kernel(const __gri
     // (beta = 0 outside QHERK: no C read -- the plain store path below is faster;
     // QHERK's diagonal tiles: masked per-lane stores, see ring_epilogue)
     if (kRing && ring_epilogue(args, mt, nt)) {
-      // C tile through the ring (produce_c_stage): stage h holds rows 16h..16h+15,
-      // i.e. fragments ii = 2(h & 1), 2(h & 1) + 1 of the four warps of half
-      // wm = h / 2; they read C, update it in place and hand the box to the
-      // store warp (c_store_loop); the other four warps only step past the slot.
+      // C tile through the ring (produce_c_stage): read, update in place, TMA store.
+      int slots[2];
 #pragma unroll
-      for (int h = 0; h < kCStages; ++h) {
-        if ((h >> 1) == wm) {
-          mbar_wait(&full[slot], phase);
-          unsigned char *box = reinterpret_cast<unsigned char *>(ring + slot * kSlotElems);
+      for (int h = 0; h < 2; ++h) {
+        slots[h] = slot;
+        mbar_wait(&full[slot], phase);
+        unsigned char *box = reinterpret_cast<unsigned char *>((wm ? sB : sA) + slot * kChunkElems);
 #pragma unroll
-          for (int i2 = 0; i2 < 2; ++i2)
+        for (int i2 = 0; i2 < 2; ++i2)
 #pragma unroll
-            for (int jj = 0; jj < 2; ++jj)
+          for (int jj = 0; jj < 2; ++jj)
 #pragma unroll
-              for (int e = 0; e < 2; ++e) {
-                const int ii = 2 * (h & 1) + i2;
-                const int rl = i2 * 8 + (lane >> 2);                    // row in the 16-row box
-                const int cl = (wn * 2 + jj) * 8 + 2 * (lane & 3) + e;  // column in the tile
-                const uint32_t lin = uint32_t(rl * 64 + cl) * 32u;
-                double2 *q0 = reinterpret_cast<double2 *>(box + (lin ^ (((lin >> 7) & 1u) << 4)));
-                double2 *q1 = reinterpret_cast<double2 *>(box + ((lin + 16u) ^ ((((lin + 16u) >> 7) & 1u) << 4)));
-                const double q[4] = {acc[ii][jj][0][e], acc[ii][jj][1][e], acc[ii][jj][2][e], acc[ii][jj][3][e]};
-                double out[4];
-                left_scale(args.sc.alpha, args.sc.alpha_real, q, out);
-                if (!args.sc.beta_zero) {
-                  const double2 c01 = *q0, c23 = *q1;
-                  const double cold[4] = {c01.x, c01.y, c23.x, c23.y};
-                  double bc[4];
-                  left_scale(args.sc.beta, args.sc.beta_real, cold, bc);
+            for (int e = 0; e < 2; ++e) {
+              const int ii = 2 * h + i2;
+              const int rl = i2 * 8 + (lane >> 2);                    // row in the 16-row box
+              const int cl = (wn * 2 + jj) * 8 + 2 * (lane & 3) + e;  // column in the tile
+              const uint32_t lin = uint32_t(rl * 64 + cl) * 32u;
+              double2 *q0 = reinterpret_cast<double2 *>(box + (lin ^ (((lin >> 7) & 1u) << 4)));
+              double2 *q1 = reinterpret_cast<double2 *>(box + ((lin + 16u) ^ ((((lin + 16u) >> 7) & 1u) << 4)));
+              const double q[4] = {acc[ii][jj][0][e], acc[ii][jj][1][e], acc[ii][jj][2][e], acc[ii][jj][3][e]};
+              double out[4];
+              left_scale(args.sc.alpha, args.sc.alpha_real, q, out);
+              if (!args.sc.beta_zero) {
+                const double2 c01 = *q0, c23 = *q1;
+                const double cold[4] = {c01.x, c01.y, c23.x, c23.y};
+                double bc[4];
+                left_scale(args.sc.beta, args.sc.beta_real, cold, bc);
 #pragma unroll
-                  for (int k = 0; k < 4; ++k) out[k] += bc[k];
-                }
-                *q0 = make_double2(out[0], out[1]);
-                *q1 = make_double2(out[2], out[3]);
+                for (int k = 0; k < 4; ++k) out[k] += bc[k];
               }
-          asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");  // smem writes -> TMA store
+              *q0 = make_double2(out[0], out[1]);
+              *q1 = make_double2(out[2], out[3]);
+            }
+        asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");  // smem writes -> TMA store
+        if (QG_C_STORE_WARP) {  // the store warp takes it from here (c_store_loop)
           __syncwarp();
-          if (lane == 0) mbar_arrive_n(&cdone[slot], kConsumerWarps / 4);  // 4 owning warps
+          if (lane == 0) mbar_arrive(&cdone[slot]);
+          if (++slot == kStages) { slot = 0; phase ^= 1u; }
+          continue;
+        }
+        consumer_bar();
+        if (tid == 0) {
+          const int n0 = int(nt * kBR), r0 = int(mt * kBR) + 16 * h;
+          tma_store_3d(&args.tmC, sA + slot * kChunkElems, 0, n0, r0);
+          tma_store_3d(&args.tmC, sB + slot * kChunkElems, 0, n0, r0 + 32);
+          asm volatile("cp.async.bulk.commit_group;\n" ::: "memory");
         }
         if (++slot == kStages) { slot = 0; phase ^= 1u; }
+      }
+      if (QG_C_STORE_WARP) {
+        QG_TR(5);
+        continue;
+      }
+      // the slots return to the producer once the TMA unit has read them
+      if (tid == 0) asm volatile("cp.async.bulk.wait_group.read 0;\n" ::: "memory");
+      consumer_bar();
+      if (lane == 0) {
+        mbar_arrive(&empty[slots[0]]);
+        mbar_arrive(&empty[slots[1]]);
       }
       QG_TR(5);
       continue;
@@ -894,6 +899,7 @@ __global__ void __launch_bounds__(kDmmaThreads, 1) qgemm_dmma_kernel(const __gri
     }
     QG_TR(5);
   }
+  if (kRing && args.c_ring && tid == 0) asm volatile("cp.async.bulk.wait_group 0;\n" ::: "memory");
   // Per-lane C stores may target another GPU's memory (the multi-GPU driver's
   // epilogue stores into root's C over NVLink, dist.qgemm_rowsharded_p2p):
   // make them visible at system scope before this CTA retires, so whatever the

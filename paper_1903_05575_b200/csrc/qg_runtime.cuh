@@ -455,8 +455,7 @@ int encode_view(CUtensorMap *tm, const double *X, int64_t ldx, int rc, int64_t R
   if (!fn) return int(cudaErrorNotSupported);
   const cuuint64_t dims[3] = {4, cuuint64_t(rc ? R : K), cuuint64_t(rc ? K : R)};
   const cuuint64_t strides[2] = {32, cuuint64_t(32) * cuuint64_t(ldx)};
-  // one ring stage = a 64-row x 8-k half tile (qg_dmma.cuh kHalfK)
-  const cuuint32_t box[3] = {4, cuuint32_t(rc ? qg::kBR : qg::kHalfK), cuuint32_t(rc ? qg::kHalfK : qg::kBR)};
+  const cuuint32_t box[3] = {4, cuuint32_t(rc ? qg::kBR : qg::kBK), cuuint32_t(rc ? qg::kBK : qg::kBR)};
   const cuuint32_t estr[3] = {1, 1, 1};
   const CUresult r = fn(tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, const_cast<double *>(X), dims, strides, box, estr,
                         CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_32B,
@@ -465,7 +464,7 @@ int encode_view(CUtensorMap *tm, const double *X, int64_t ldx, int rc, int64_t R
 }
 
 // kFeedTma128 group maps (qg_dmma.cuh): (16 doubles, k, row/4) when rows are
-// contiguous, else (16 doubles, k/4, row); box = one 64-row x 8-k half tile (a ring stage);
+// contiguous, else (16 doubles, k/4, row); box = one 64-row x 16-k tile;
 // 128-byte swizzle.  The inner dimension is 4 quaternions along the
 // contiguous index, so it needs R % 4 == 0, resp. K % 4 == 0 (then no read
 // leaves the operand's extent).
@@ -476,7 +475,7 @@ int encode_view_g4(CUtensorMap *tm, const double *X, int64_t ldx, int rc, int64_
   const cuuint64_t col = cuuint64_t(32) * cuuint64_t(ldx);
   const cuuint64_t dims[3] = {16, cuuint64_t(rc ? K : K / 4), cuuint64_t(rc ? R / 4 : R)};
   const cuuint64_t strides[2] = {rc ? col : 128, rc ? 128 : col};
-  const cuuint32_t box[3] = {16, cuuint32_t(rc ? qg::kHalfK : qg::kHalfK / 4), cuuint32_t(rc ? qg::kBR / 4 : qg::kBR)};
+  const cuuint32_t box[3] = {16, cuuint32_t(rc ? qg::kBK : qg::kBK / 4), cuuint32_t(rc ? qg::kBR / 4 : qg::kBR)};
   const cuuint32_t estr[3] = {1, 1, 1};
   const CUresult r = fn(tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, const_cast<double *>(X), dims, strides, box, estr,
                         CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
