@@ -286,7 +286,6 @@ struct Producer {
   uint32_t phase;
   int64_t fills;
   int64_t c_pref_kt;  // k-tile at which to L2-prefetch the unit's C tile (-1: none)
-  int64_t n_pref_kt;  // TMA feeds: k-tile at which to L2-prefetch the next unit's first k-tile (-1: none)
   int c_left;         // QG_C_RING: C stages still to issue for the current unit
   bool c_load;        // ... and whether they load C (beta != 0)
 };
@@ -346,24 +345,12 @@ __device__ __forceinline__ void prefetch_c_tile(const DmmaArgs &a, int64_t mt, i
     asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;\n" ::"l"(p), "r"(bytes) : "memory");
   }
 }
-#ifndef QG_RING_C_PREFETCH_KT
-#define QG_RING_C_PREFETCH_KT 4  // ring epilogues: L2-prefetch the C tile this many k-tiles before the unit ends (0: off)
-#endif
-#ifndef QG_NEXT_PREFETCH_KT
-#define QG_NEXT_PREFETCH_KT 4  // TMA feeds: L2-prefetch the next unit's first k-tile this many k-tiles ahead (0: off)
-#endif
 template <bool kRing>
 __device__ __forceinline__ void producer_unit_prefetch(Producer &p, const DmmaArgs &a, const Unit &u) {
-  // per-lane epilogues: QG_C_PREFETCH_KT ahead; ring epilogues (C boxes loaded
-  // by TMA right behind the last k-tiles): QG_RING_C_PREFETCH_KT ahead, so the
-  // boxes come from L2 and do not hold up the TMA requests queued behind them
-  const bool ring = kRing && a.c_ring;
-  const int64_t d = ring ? QG_RING_C_PREFETCH_KT : QG_C_PREFETCH_KT;
-  p.c_pref_kt = (!a.c_remote && QG_C_PREFETCH_BULK && d > 0 && u.kb == 0 && !a.sc.beta_zero)
-                    ? (u.ke - d > u.kb ? u.ke - d : u.kb)
+  p.c_pref_kt = (!(kRing && a.c_ring) && !a.c_remote && QG_C_PREFETCH_BULK && QG_C_PREFETCH_KT > 0 && u.kb == 0 &&
+                 !a.sc.beta_zero)
+                    ? (u.ke - QG_C_PREFETCH_KT > u.kb ? u.ke - QG_C_PREFETCH_KT : u.kb)
                     : int64_t(-1);
-  p.n_pref_kt = QG_NEXT_PREFETCH_KT > 0 ? (u.ke - QG_NEXT_PREFETCH_KT > u.kb ? u.ke - QG_NEXT_PREFETCH_KT : u.kb)
-                                        : int64_t(-1);
 }
 
 // Issue the next fill (bulk copies of one A and one B chunk); false when done.
@@ -406,36 +393,6 @@ __device__ __forceinline__ bool produce_next(Producer &p, const DmmaArgs &args, 
 // (4-way conflicts; ncu) or 4 when k is contiguous (2-way) -- the price of not
 // packing, which auto pays only where the sweep shows it wins.
 
-__device__ __forceinline__ void tma_prefetch_3d(const CUtensorMap *tm, int c0, int c1, int c2) {
-  asm volatile("cp.async.bulk.prefetch.tensor.3d.L2.global.tile [%0, {%1, %2, %3}];\n" ::"l"(
-                   reinterpret_cast<uint64_t>(tm)),
-               "r"(c0), "r"(c1), "r"(c2)
-               : "memory");
-}
-// L2 prefetch of the first k-tile of the unit after the current one (the
-// producer's work list peeked with a copy of its iterator): its TMA loads then
-// hit L2 at the tile switch, where they queue behind the epilogue's C boxes.
-template <bool kG4>
-__device__ __forceinline__ void prefetch_next_unit(const Producer &p, const DmmaArgs &args) {
-  WorkIter it = p.it;
-  Unit u;
-  if (!it.next(args, u)) return;
-  int64_t mt, nt;
-  work_tile(args, u.t, mt, nt);
-  const int k0 = int(u.kb * kBK), ra = int(mt * kBR), rb = int(nt * kBR);
-  if constexpr (kG4) {
-    if (args.a_rc) tma_prefetch_3d(&args.tmA, 0, k0, ra / 4);
-    else           tma_prefetch_3d(&args.tmA, 0, k0 / 4, ra);
-    if (args.b_rc) tma_prefetch_3d(&args.tmB, 0, k0, rb / 4);
-    else           tma_prefetch_3d(&args.tmB, 0, k0 / 4, rb);
-  } else {
-    if (args.a_rc) tma_prefetch_3d(&args.tmA, 0, ra, k0);
-    else           tma_prefetch_3d(&args.tmA, 0, k0, ra);
-    if (args.b_rc) tma_prefetch_3d(&args.tmB, 0, rb, k0);
-    else           tma_prefetch_3d(&args.tmB, 0, k0, rb);
-  }
-}
-
 template <bool kG4>
 __device__ __forceinline__ bool produce_next_tma(Producer &p, const DmmaArgs &args, double *sA, double *sB,
                                                  uint64_t *full, uint64_t *empty) {
@@ -454,7 +411,6 @@ __device__ __forceinline__ bool produce_next_tma(Producer &p, const DmmaArgs &ar
     return true;
   }
   if (p.kt == p.c_pref_kt) prefetch_c_tile(args, p.mt, p.nt);
-  if (p.kt == p.n_pref_kt) prefetch_next_unit<kG4>(p, args);
   if (p.fills >= kStages) mbar_wait(&empty[p.slot], p.phase ^ 1u);
   mbar_arrive_expect_tx(&full[p.slot], 2 * kBytes);
   const int k0 = int(p.kt * kBK), ra = int(p.mt * kBR), rb = int(p.nt * kBR);
@@ -640,7 +596,6 @@ __global__ void __launch_bounds__(kDmmaThreads, 1) qgemm_dmma_kernel(const __gri
   prod.phase = 0;
   prod.fills = 0;
   prod.c_pref_kt = -1;
-  prod.n_pref_kt = -1;
   prod.c_left = 0;
   prod.c_load = false;
   prod.mt = prod.nt = 0;
