@@ -9,14 +9,7 @@
 #define QG_HOST_KC_DIV 8
 #endif
 #ifndef QG_HOST_KC0_DIV
-#define QG_HOST_KC0_DIV 16
-#endif
-// Chunks shorter than the second one's (~K/QG_HOST_KC_DIV) grow by QG_HOST_RAMP
-// from the first: every upload stays shorter than the mainloop of the chunk
-// before it (an upload moves K 5-6x faster than the mainloop consumes it at c3)
-// while the first, exposed one is small (c3: 64, 256, 1024, ...).
-#ifndef QG_HOST_RAMP
-#define QG_HOST_RAMP 4
+#define QG_HOST_KC0_DIV 4
 #endif
 #ifndef QG_HOST_PANELS
 #define QG_HOST_PANELS 16
@@ -91,7 +84,7 @@ HostPlan<T> host_plan(int oa, int ob, int64_t M, int64_t N, int64_t K) {
                              std::max<int64_t>(256, std::min<int64_t>(2048, cdiv(cdiv(K, QG_HOST_KC_DIV), kq) * kq)));
     h.Kc0 = std::min<int64_t>(kc1, std::max<int64_t>(kq, cdiv(cdiv(kc1, QG_HOST_KC0_DIV), kq) * kq));
     h.kb.push_back(0);
-    int64_t k = std::min<int64_t>(K, h.Kc0), len = std::min<int64_t>(kc1, h.Kc0 * QG_HOST_RAMP);
+    int64_t k = std::min<int64_t>(K, h.Kc0), len = kc1;
     h.kb.push_back(k);
     h.Kc = h.Kc0;
     while (k < K) {
@@ -99,8 +92,7 @@ HostPlan<T> host_plan(int oa, int ob, int64_t M, int64_t N, int64_t K) {
       h.Kc = std::max(h.Kc, l);
       k += l;
       h.kb.push_back(k);
-      len = len < kc1 ? std::min<int64_t>(kc1, len * QG_HOST_RAMP)
-                      : std::max<int64_t>(kc1, std::min<int64_t>(int64_t(QG_HOST_KC_MAX), len * QG_HOST_GROWTH));
+      len = std::max<int64_t>(kc1, std::min<int64_t>(int64_t(QG_HOST_KC_MAX), len * QG_HOST_GROWTH));
     }
     h.Q = int64_t(h.kb.size()) - 1;
     // the last chunk runs per column panel with each panel's download behind the

@@ -227,7 +227,7 @@ def test_small_path_validates_identically(lib, kw, code):
 def test_host_workspace_c3_plan(lib):
     """qgemm_host at c3 (FP64, auto = direct chunks): caller's C + accumulator C
     (2 x 2 GiB) + 2 staging slots per operand for the largest K-chunk (4096 k:
-    chunks 64, 256, 1024, 2048, 704, 4096 after the longest-last reorder) + the
+    chunks 256, 1024, 2048, 768, 4096 after the longest-last reorder) + the
     stream-K scratch; no packed buffers (the chunks are read in place)."""
     lib.qgemm_set_path_policy(0)
     n = 8192
@@ -256,7 +256,7 @@ def test_host_workspace_f32_covers_every_panel_split(lib, N, policy):
     lib.qgemm_set_path_policy(policy)
     M = K = 8192
     qb = 16
-    kc = 4096                                    # chunks 64, 256, 1024, 2048, 704, 4096
+    kc = 4096                                    # chunks 256, 1024, 2048, 768, 4096
     stage = 2 * M * kc * qb + 2 * N * kc * qb
     ktc = kc // 8                                # FP32 k-tiles per chunk (8 k per tile)
     packed = 2 * (2 * (M // 256)) * ktc * 32768 + 2 * (N // 128) * ktc * 32768
