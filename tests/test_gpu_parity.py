@@ -155,7 +155,8 @@ def test_ring_epilogue_short_k_stream_k(M, N, K, opA, opB):
 @pytest.mark.parametrize("opA,opB", OPS)
 @pytest.mark.parametrize("policy", [qg.PATH_PACKED, qg.PATH_DIRECT], ids=["packed", "direct"])
 def test_ring_epilogue_edges(M, N, K, opA, opB, policy):
-    """K >= 512 (>= 32 k-tiles): the FP64 epilogue reads C through the ring (TMA
+    """K >= 512 (>= 32 k-tiles; since the store warp the ring applies at every K,
+    see test_ring_epilogue_short_k_stream_k): the FP64 epilogue reads C through the ring (TMA
     load, update in shared memory, TMA store clipped at the M / N edges), on
     ragged tiles, degenerate M or N, padded ld (sentinel in C's padding must
     survive), quaternion alpha/beta; exact-integer inputs -> bitwise."""
