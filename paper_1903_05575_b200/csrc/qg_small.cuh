@@ -129,8 +129,8 @@ __device__ __forceinline__ void st_dsmem(const double *p, uint32_t rank, double 
 template <typename T, bool kZ>
 // (<= 128 registers: 4 CTAs per SM -- occupancy, not ILP, sets its speed; measured)
 __global__ void __launch_bounds__(kSmallThreads, 512 / kSmallThreads) qgemm_small_kernel(SmallArgs a) {
-  __shared__ double red[kSmallThreads / 32][32][8];
-  __shared__ double zred[kZ ? kSmallMaxCluster - 1 : 1][32][8];
+  __shared__ double red[kSmallThreads / 32][8][32];  // [warp][component, e][lane]: conflict-free
+  __shared__ double zred[kZ ? kSmallMaxCluster - 1 : 1][8][32];
   const T *A = static_cast<const T *>(a.A);
   const T *B = static_cast<const T *>(a.B);
   T *C = static_cast<T *>(a.C);
@@ -205,8 +205,8 @@ __global__ void __launch_bounds__(kSmallThreads, 512 / kSmallThreads) qgemm_smal
     if (part != 0) {
 #pragma unroll
       for (int c = 0; c < 4; ++c) {
-        red[warp][lane][2 * c] = acc[c][0];
-        red[warp][lane][2 * c + 1] = acc[c][1];
+        red[warp][2 * c][lane] = acc[c][0];
+        red[warp][2 * c + 1][lane] = acc[c][1];
       }
     }
     __syncthreads();
@@ -214,8 +214,8 @@ __global__ void __launch_bounds__(kSmallThreads, 512 / kSmallThreads) qgemm_smal
       for (int w = 1; w < S; ++w)
 #pragma unroll
         for (int c = 0; c < 4; ++c) {
-          acc[c][0] += red[warp + w][lane][2 * c];
-          acc[c][1] += red[warp + w][lane][2 * c + 1];
+          acc[c][0] += red[warp + w][2 * c][lane];
+          acc[c][1] += red[warp + w][2 * c + 1][lane];
         }
   }
   // then across the cluster (every thread takes part in the cluster barriers)
@@ -224,8 +224,8 @@ __global__ void __launch_bounds__(kSmallThreads, 512 / kSmallThreads) qgemm_smal
     if (z > 0 && part == 0)
 #pragma unroll
       for (int c = 0; c < 4; ++c) {
-        st_dsmem(&zred[z - 1][lane][2 * c], 0, acc[c][0]);
-        st_dsmem(&zred[z - 1][lane][2 * c + 1], 0, acc[c][1]);
+        st_dsmem(&zred[z - 1][2 * c][lane], 0, acc[c][0]);
+        st_dsmem(&zred[z - 1][2 * c + 1][lane], 0, acc[c][1]);
       }
     cluster_arrive_release();
     cluster_wait();
@@ -234,8 +234,8 @@ __global__ void __launch_bounds__(kSmallThreads, 512 / kSmallThreads) qgemm_smal
       for (int r = 0; r < Z - 1; ++r)
 #pragma unroll
         for (int c = 0; c < 4; ++c) {
-          acc[c][0] += zred[r][lane][2 * c];
-          acc[c][1] += zred[r][lane][2 * c + 1];
+          acc[c][0] += zred[r][2 * c][lane];
+          acc[c][1] += zred[r][2 * c + 1][lane];
         }
   }
   if (part != 0) return;
@@ -338,7 +338,7 @@ constexpr int kTinyThreads = kTinyWarps * 32;
 template <typename T, int kOps>
 __global__ void __launch_bounds__(kTinyThreads, (QG_TINY_DUAL ? 384 : 512) / kTinyThreads) qgemm_tiny_kernel(SmallArgs a) {
   constexpr bool a_rc = kOps & 1, a_cj = (kOps >> 1) & 1, b_rc = (kOps >> 2) & 1, b_cj = (kOps >> 3) & 1;
-  __shared__ double red[kTinyWarps][32][8];
+  __shared__ double red[kTinyWarps][8][32];  // [warp][component, e][lane]: conflict-free
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   // grid (m blocks, n tiles); S a power of two (host), so no divisions here
   const int S = a.S, lgS = __ffs(S) - 1;
@@ -413,8 +413,8 @@ __global__ void __launch_bounds__(kTinyThreads, (QG_TINY_DUAL ? 384 : 512) / kTi
     if (part != 0) {
 #pragma unroll
       for (int c = 0; c < 4; ++c) {
-        red[warp][lane][2 * c] = acc[c][0];
-        red[warp][lane][2 * c + 1] = acc[c][1];
+        red[warp][2 * c][lane] = acc[c][0];
+        red[warp][2 * c + 1][lane] = acc[c][1];
       }
     }
     __syncthreads();
@@ -422,8 +422,8 @@ __global__ void __launch_bounds__(kTinyThreads, (QG_TINY_DUAL ? 384 : 512) / kTi
     for (int w = 1; w < S; ++w)
 #pragma unroll
       for (int c = 0; c < 4; ++c) {
-        acc[c][0] += red[warp + w][lane][2 * c];
-        acc[c][1] += red[warp + w][lane][2 * c + 1];
+        acc[c][0] += red[warp + w][2 * c][lane];
+        acc[c][1] += red[warp + w][2 * c + 1][lane];
       }
   }
   if (!live) return;
