@@ -135,6 +135,7 @@ struct alignas(64) DmmaArgs {
   CUtensorMap tmC;       // QG_C_RING: C as (component, column, row), box 4 x 64 x 16, 32-byte swizzle
   int c_ring;            // host: C tiles through the ring for this launch (see launch_dmma)
   int c_remote;          // host: C is not in this GPU's memory (multi-GPU epilogue stores): no L2 prefetch of C
+  int c_reduce;          // host: ring epilogue with beta == 1: boxes of alpha (x) acc added into C by TMA reductions
   const double *Ap;  // packed path: packed A panel, MT x KT chunks
   const double *Bp;  // packed path: packed B panel, NT x KT chunks
   // TMA feed: op(A) / op(B) read in place as R x K views -- X~(r, k) at
@@ -276,6 +277,15 @@ __device__ __forceinline__ void tma_store_3d(const CUtensorMap *tm, const void *
                : "memory");
 }
 
+// 3-D TMA reduction from shared memory into global: dst += box, element-wise in
+// the map's type (FP64 here), performed in L2 (bulk-group completion).
+__device__ __forceinline__ void tma_reduce_add_3d(const CUtensorMap *tm, const void *src, int c0, int c1, int c2) {
+  asm volatile("cp.reduce.async.bulk.tensor.3d.global.shared::cta.add.tile.bulk_group [%0, {%1, %2, %3}], [%4];\n" ::"l"(
+                   reinterpret_cast<uint64_t>(tm)),
+               "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(src))
+               : "memory");
+}
+
 // Producer cursor over the CTA's (unit, k-tile) sequence.
 struct Producer {
   WorkIter it;
@@ -328,7 +338,7 @@ __device__ __forceinline__ bool ring_epilogue(const DmmaArgs &a, int64_t mt, int
 }
 template <bool kRing>
 __device__ __forceinline__ void producer_unit_c(Producer &p, const DmmaArgs &a, const Unit &u) {
-  p.c_load = !a.sc.beta_zero;
+  p.c_load = !a.sc.beta_zero && !a.c_reduce;  // (c_reduce: C is read by the TMA reduction, in L2)
   p.c_left = (kRing && u.kb == 0 && ring_epilogue(a, p.mt, p.nt)) ? 2 : 0;
 }
 
@@ -458,8 +468,13 @@ __device__ __forceinline__ void c_store_loop(const DmmaArgs &args, const SkSplit
       mbar_wait(&cdone[slot], (cph >> slot) & 1u);
       cph ^= 1u << slot;
       const int n0 = int(nt * kBR), r0 = int(mt * kBR) + 16 * h;
-      tma_store_3d(&args.tmC, sA + slot * kChunkElems, 0, n0, r0);
-      tma_store_3d(&args.tmC, sB + slot * kChunkElems, 0, n0, r0 + 32);
+      if (args.c_reduce) {  // C += box (beta == 1): the add happens in L2
+        tma_reduce_add_3d(&args.tmC, sA + slot * kChunkElems, 0, n0, r0);
+        tma_reduce_add_3d(&args.tmC, sB + slot * kChunkElems, 0, n0, r0 + 32);
+      } else {
+        tma_store_3d(&args.tmC, sA + slot * kChunkElems, 0, n0, r0);
+        tma_store_3d(&args.tmC, sB + slot * kChunkElems, 0, n0, r0 + 32);
+      }
       asm volatile("cp.async.bulk.commit_group;\n" ::: "memory");
       asm volatile("cp.async.bulk.wait_group.read 0;\n" ::: "memory");
       mbar_arrive_n(&empty[slot], kConsumerWarps);
@@ -807,7 +822,7 @@ __global__ void __launch_bounds__(kDmmaThreads, 1) qgemm_dmma_kernel(const __gri
               const double q[4] = {acc[ii][jj][0][e], acc[ii][jj][1][e], acc[ii][jj][2][e], acc[ii][jj][3][e]};
               double out[4];
               left_scale(args.sc.alpha, args.sc.alpha_real, q, out);
-              if (!args.sc.beta_zero) {
+              if (!args.sc.beta_zero && !args.c_reduce) {
                 const double2 c01 = *q0, c23 = *q1;
                 const double cold[4] = {c01.x, c01.y, c23.x, c23.y};
                 double bc[4];

@@ -356,6 +356,9 @@ int persistent_ctas() {
 // wins at c4 too: 241.8 vs 245.9 ms (profiles/r02w_ab.txt)
 #define QG_C_RING_MIN_KT 1
 #endif
+#ifndef QG_C_REDUCE
+#define QG_C_REDUCE 1
+#endif
 #ifndef QG_SK_FULL_WAVES
 #define QG_SK_FULL_WAVES 0
 #endif
@@ -527,6 +530,10 @@ int launch_dmma(qg::DmmaArgs &a, DmmaKernel kernel, bool direct, void *sk_scratc
   const bool query = (direct && QG_C_RING) || !a.sc.beta_zero;
   a.c_remote = query ? !c_is_local(a.C) : 0;
   a.c_ring = direct && QG_C_RING && ((QG_RING_TRI && a.tri != 0) || a.KT >= QG_C_RING_MIN_KT) && !a.c_remote;
+  // beta == 1 (real): the ring epilogue writes alpha (x) acc and the store warp
+  // adds the boxes into C with TMA reductions, so no C stage is loaded through
+  // the ring and no C value passes through shared memory (QG_C_REDUCE)
+  a.c_reduce = a.c_ring && QG_C_REDUCE && a.sc.beta_real && a.sc.beta[0] == 1.0;
   if (a.c_ring) {
     const int e = encode_c(&a.tmC, a.C, a.ldc, a.M, a.N);
     if (e) return e;

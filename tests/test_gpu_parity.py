@@ -151,6 +151,23 @@ def test_ring_epilogue_short_k_stream_k(M, N, K, opA, opB):
         assert_parity(pr, run_gpu(pr), oracle_full(pr), exact=True)
 
 
+@pytest.mark.parametrize("M,N,K", [(1024, 1024, 48), (300, 260, 700), (130, 70, 520), (1, 64, 600)])
+@pytest.mark.parametrize("opA,opB", [("N", "H"), ("T", "N"), ("H", "H")])
+@pytest.mark.parametrize("alpha", [(1, 0, 0, 0), (0.75, 0, 0, 0), QALPHA], ids=["a1", "areal", "aquat"])
+def test_ring_epilogue_beta_one_tma_reduction(M, N, K, opA, opB, alpha):
+    """beta == 1 (c3, c4, QHERK's configs): the ring epilogue writes alpha (x) acc
+    and the store warp adds each box into C with a TMA reduction,
+    no C read through shared memory; ragged tiles, padded ldc (the sentinel in
+    C's padding must survive the reduction), stream-K owners; real and
+    quaternion alpha; exact-integer inputs -> bitwise."""
+    with path_policy(qg.PATH_DIRECT):
+        pr = make_problem(M, N, K, opA, opB, alpha, (1, 0, 0, 0), seed=41, ldc=M + 3)
+        assert_parity(pr, run_gpu(pr), oracle_full(pr))
+        ia = tuple(int(round(2 * x)) for x in alpha)
+        pr = make_problem(M, N, K, opA, opB, ia, (1, 0, 0, 0), seed=42, dist="int8", ldc=M + 3)
+        assert_parity(pr, run_gpu(pr), oracle_full(pr), exact=True)
+
+
 @pytest.mark.parametrize("M,N,K", [(130, 70, 520), (64, 1, 512), (1, 64, 600), (257, 129, 1000)])
 @pytest.mark.parametrize("opA,opB", OPS)
 @pytest.mark.parametrize("policy", [qg.PATH_PACKED, qg.PATH_DIRECT], ids=["packed", "direct"])
