@@ -57,6 +57,9 @@ constexpr int kConsumerRegs = 232;
 #ifndef QG_GROUP_M
 #define QG_GROUP_M 8
 #endif
+#ifndef QG_RING_BETA0
+#define QG_RING_BETA0 1  // beta == 0 tiles take the ring too (no C stage loads; the store warp TMA-stores the boxes)
+#endif
 #ifndef QG_C_RING
 #define QG_C_RING 1  // epilogue C tiles through the ring by TMA (see produce_c_stage)
 #endif
@@ -308,9 +311,12 @@ struct Producer {
 // results back in place and one thread TMA-stores the boxes (the TMA unit clips
 // the M / N edges): the epilogue's global traffic runs at TMA rates instead of
 // 128-bit per-lane loads and stores with 64 KB in flight per batch.
-// Without a C read (beta = 0, not QHERK) there are no C stages: the plain
-// per-lane store epilogue is faster there.  QHERK's off-diagonal tiles lie
-// wholly inside its triangle; its diagonal tiles never take the ring.
+// Without a C read (beta = 0) the C stages load nothing and the consumers
+// overwrite the boxes whole (QG_RING_BETA0; with the store warp this beats the
+// per-lane stores); with a real beta == 1 they load nothing either
+// and the store warp adds the boxes into C by TMA reductions (QG_C_REDUCE).
+// QHERK's off-diagonal tiles lie wholly inside its triangle; its diagonal tiles
+// never take the ring.
 constexpr uint32_t kCBoxBytes = 16u * 64u * 32u;  // 32 KB = one slot half
 __device__ __forceinline__ void produce_c_stage(Producer &p, const DmmaArgs &args, double *sA, double *sB,
                                                 uint64_t *full, uint64_t *empty) {
@@ -334,7 +340,7 @@ __device__ __forceinline__ void produce_c_stage(Producer &p, const DmmaArgs &arg
 // values loaded earlier, losing a concurrent writer's update; those few tiles
 // (MT of MT(MT+1)/2) take the per-lane masked store epilogue instead.
 __device__ __forceinline__ bool ring_epilogue(const DmmaArgs &a, int64_t mt, int64_t nt) {
-  return a.c_ring && (!a.sc.beta_zero || a.tri != 0) && !(a.tri != 0 && mt == nt);
+  return a.c_ring && (!a.sc.beta_zero || a.tri != 0 || QG_RING_BETA0) && !(a.tri != 0 && mt == nt);
 }
 template <bool kRing>
 __device__ __forceinline__ void producer_unit_c(Producer &p, const DmmaArgs &a, const Unit &u) {

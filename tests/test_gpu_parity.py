@@ -168,6 +168,20 @@ def test_ring_epilogue_beta_one_tma_reduction(M, N, K, opA, opB, alpha):
         assert_parity(pr, run_gpu(pr), oracle_full(pr), exact=True)
 
 
+@pytest.mark.parametrize("M,N,K", [(1024, 1024, 48), (300, 260, 700), (130, 70, 520), (1, 64, 600)])
+@pytest.mark.parametrize("opA,opB", [("N", "N"), ("T", "H")])
+def test_ring_epilogue_beta_zero_nan_c(M, N, K, opA, opB):
+    """beta == 0 (c5's config) through the ring epilogue (QG_RING_BETA0): no C
+    stage is loaded, the store warp TMA-stores alpha (x) acc; a NaN-filled C must
+    not leak into the result (beta = 0 means C is not read), ragged
+    tiles, stream-K owners; exact-integer inputs -> bitwise."""
+    with path_policy(qg.PATH_DIRECT):
+        pr = make_problem(M, N, K, opA, opB, QALPHA, 0, seed=43, c_init="nan")
+        assert_parity(pr, run_gpu(pr), oracle_full(pr))
+        pr = make_problem(M, N, K, opA, opB, (2, -1, 0, 3), 0, seed=44, dist="int8", c_init="nan")
+        assert_parity(pr, run_gpu(pr), oracle_full(pr), exact=True)
+
+
 @pytest.mark.parametrize("M,N,K", [(130, 70, 520), (64, 1, 512), (1, 64, 600), (257, 129, 1000)])
 @pytest.mark.parametrize("opA,opB", OPS)
 @pytest.mark.parametrize("policy", [qg.PATH_PACKED, qg.PATH_DIRECT], ids=["packed", "direct"])

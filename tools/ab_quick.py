@@ -43,6 +43,7 @@ B = torch.randn((n, n, 4), dtype=torch.float64, device="cuda", generator=g)
 C = torch.randn((n, n, 4), dtype=torch.float64, device="cuda", generator=g)
 ws = torch.empty(qg.workspace_bytes("N", "H", n, n, n), dtype=torch.uint8, device="cuda")
 out["c3_ms"] = best_ms(lambda: qg.qgemm("N", "H", 1.0, A, B, 1.0, C, workspace=ws), a.reps)
+out["c3_beta0_NN_ms"] = best_ms(lambda: qg.qgemm("N", "N", 1.0, A, B, 0.0, C, workspace=ws), a.reps)
 del A, B, C, ws
 n, K = 32768, 256
 A = torch.rand((K, n, 4), dtype=torch.float64, device="cuda", generator=g)
@@ -50,6 +51,7 @@ C = torch.rand((n, n, 4), dtype=torch.float64, device="cuda", generator=g)
 ws = torch.empty(qg.workspace_bytes("N", "H", n, n, K), dtype=torch.uint8, device="cuda")
 out["c4_ms"] = best_ms(lambda: qg.qgemm("N", "H", 1.0, A, A, 1.0, C, M=n, N=n, K=K, workspace=ws), a.reps)
 out["c4_herk_ms"] = best_ms(lambda: qg.qherk("L", "N", 1.0, A, 1.0, C, N=n), a.reps)
+out["c4_beta0_ms"] = best_ms(lambda: qg.qgemm("N", "H", 1.0, A, A, 0.0, C, M=n, N=n, K=K, workspace=ws), a.reps)
 del A, C, ws
 n = 1024
 A = torch.randn((n, n, 4), dtype=torch.float64, device="cuda", generator=g)
@@ -58,4 +60,6 @@ C = torch.randn((n, n, 4), dtype=torch.float64, device="cuda", generator=g)
 ws = torch.empty(max(256, qg.workspace_bytes("N", "N", n, n, n)), dtype=torch.uint8, device="cuda")
 out["c2_NN_ms"] = best_ms(lambda: [qg.qgemm("N", "N", 0.75, A, B, -0.5, C, workspace=ws) for _ in range(20)],
                           a.reps) / 20
+out["c2_beta0_NN_ms"] = best_ms(lambda: [qg.qgemm("N", "N", 0.75, A, B, 0.0, C, workspace=ws) for _ in range(20)],
+                                a.reps) / 20
 print(json.dumps(out))
