@@ -1,8 +1,11 @@
 #!/bin/bash
-# final evidence with the TMA-reduction ring epilogue (beta == 1): bench line, smoke,
+# final evidence with the TMA-reduction ring epilogue (beta == 1) and the beta == 0 ring: full -m gpu suite, bench line, smoke,
 # launch list of the bench command, c4 qgemm / QHERK metrics, full ncu of the c3 DMMA kernel
 cd $GRAFT_REPO_ROOT
 mkdir -p gpurun_out
+start=$(date +%s)
+timeout 2400 python -m pytest tests -m gpu -q > gpurun_out/r2zl_tests.log 2>&1
+echo "rc=$? seconds=$(( $(date +%s) - start ))" >> gpurun_out/r2zl_tests.log
 timeout 900 python bench.py > gpurun_out/r2zl_bench.json 2> gpurun_out/r2zl_bench.err; echo "bench rc=$?" >> gpurun_out/r2zl_bench.err
 timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/r2zl_smoke.log 2>&1; echo "smoke rc=$?" >> gpurun_out/r2zl_smoke.log
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file gpurun_out/r2zl_launches.csv \
