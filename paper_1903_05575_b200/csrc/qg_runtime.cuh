@@ -489,7 +489,18 @@ int encode_view_g4(CUtensorMap *tm, const double *X, int64_t ldx, int rc, int64_
 // The ring epilogue moves C with the TMA unit; C in another GPU's memory (the
 // multi-GPU driver stores row blocks straight into root's C over peer memory,
 // dist.qgemm_rowsharded_p2p) keeps the per-lane load / store epilogue.
+// QG_FORCE_REMOTE_C=1 (test hook, read once): treat every C as remote, so the
+// multi-GPU epilogue (per-lane loads / stores, no ring, no L2 prefetch of C) is
+// checked against the oracle on a one-GPU box (tests/test_gpu_parity.py).
+bool force_remote_c() {
+  static const bool v = [] {
+    const char *e = std::getenv("QG_FORCE_REMOTE_C");
+    return e && std::atoi(e) != 0;
+  }();
+  return v;
+}
 bool c_is_local(const void *C) {
+  if (force_remote_c()) return false;
   cudaPointerAttributes at{};
   int dev = 0;
   // a failed query leaves an error behind: clear only that one, never an error

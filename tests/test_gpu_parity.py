@@ -589,3 +589,25 @@ def test_f32_long_k_error_bounded_by_accumulation_chunks():
     err = max(float(np.abs(got[:, rows, :] - ref_r).max()), float(np.abs(got[cols] - ref_c).max()))
     tol = 1e-4 * K ** 0.5 * float(np.abs(A_h).max()) * float(np.abs(B_h).max())
     assert err <= 0.5 * tol, (err, tol)
+
+
+def test_remote_c_epilogue_in_child_process():
+    """The multi-GPU epilogue -- C in another GPU's memory (dist.qgemm_rowsharded_p2p
+    stores row blocks into root's C over peer memory): per-lane loads / stores, no
+    ring, no L2 prefetch of C.  On a one-GPU box every C is local, so the child
+    process sets QG_FORCE_REMOTE_C=1 (read once by the library) and reruns the
+    ring tests (beta = 1, beta = 0 with a NaN C, quaternion beta at short K with
+    stream-K owners) and the exact-integer QHERK tests on that epilogue against
+    the oracle."""
+    import os
+    import subprocess
+    import sys as _sys
+    if os.environ.get("QG_FORCE_REMOTE_C"):
+        pytest.skip("already the child")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, QG_FORCE_REMOTE_C="1")
+    cmd = [_sys.executable, "-m", "pytest", "-q", "-x", "-m", "gpu", "-p", "no:cacheprovider",
+           "tests/test_gpu_parity.py", "tests/test_gpu_qherk.py",
+           "-k", "ring_epilogue or qherk_exact_integer or qherk_multi_band"]
+    res = subprocess.run(cmd, cwd=root, env=env, capture_output=True, text=True, timeout=900)
+    assert res.returncode == 0 and " passed" in res.stdout, res.stdout[-3000:] + res.stderr[-3000:]
