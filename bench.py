@@ -315,7 +315,10 @@ def measure_f32_variant(A, B, C, n, warmup, steps):
     clocks = sampler.stop()
     fl = 32.0 * n ** 3
     main_ms, main_cnt = kt["mainloop"]
-    achieved = fl / (main_ms / max(1, main_cnt) / 1e3) / 1e12 if main_cnt else None
+    # per step, not per launch: a step runs the pair kernel and, when the partial
+    # last wave splits over K (c3: 50 pairs x 4), its reduce kernel -- both timed
+    # as mainloop launches (dividing by the launch count halved the time)
+    achieved = fl / (main_ms / max(1, steps) / 1e3) / 1e12 if main_cnt else None
     del A32, B32, C32
     torch.cuda.empty_cache()
     roof = make_roofline("f32", achieved, main_ms, ms, kt["pack"][0], steps, c3_shape=(n == 8192))
@@ -840,7 +843,9 @@ def run_ours(args):
     value = flops_step * args.steps / (ms / 1e3) / 1e12
     main_ms, main_cnt = kt["mainloop"]
     pack_ms, pack_cnt = kt["pack"]
-    main_avg_s = main_ms / max(1, main_cnt) / 1e3
+    # the mainloop launches of one step (FP64 c3: one DMMA launch; FP32: the
+    # pair kernel + its split-K reduce) against one rank's flops per step
+    main_avg_s = main_ms / max(1, args.steps) / 1e3
     achieved = 32.0 * n * n * n / main_avg_s / 1e12 if main_cnt else None
     roofline = make_roofline(args.precision, achieved, main_ms, ms, pack_ms, args.steps,
                              c3_shape=(n == 8192))
