@@ -660,6 +660,34 @@ int tc32_set_attributes() {
   return 0;
 }
 
+// QG_TC2_L2_PERSIST=1 (environment, read once; off by default because it changes
+// device-wide state): the per-SM running-sum slots of the FP32 pair kernel are
+// launched under a persisting-L2 access-policy window, with the persisting
+// carve-out (cudaLimitPersistingL2CacheSize) raised once to the slots' size.
+bool tc2_l2_persist() {
+  static const bool v = [] {
+    const char *e = std::getenv("QG_TC2_L2_PERSIST");
+    return e && std::atoi(e) != 0;
+  }();
+  return v;
+}
+// Returns the window size to use (0: not available), raising the carve-out once per device.
+size_t tc2_persist_window(size_t want) {
+  static std::atomic<int64_t> got[kMaxDev];
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev >= kMaxDev) return 0;
+  int64_t g = got[dev].load(std::memory_order_acquire);
+  if (g == 0) {
+    int max_persist = 0, max_window = 0;
+    cudaDeviceGetAttribute(&max_persist, cudaDevAttrMaxPersistingL2CacheSize, dev);
+    cudaDeviceGetAttribute(&max_window, cudaDevAttrMaxAccessPolicyWindowSize, dev);
+    const size_t n = std::min({want, size_t(max_persist), size_t(max_window)});
+    g = (n > 0 && cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, n) == cudaSuccess) ? int64_t(n) : -1;
+    got[dev].store(g, std::memory_order_release);
+  }
+  return g > 0 ? size_t(g) : 0;
+}
+
 // Pair kernel launch (+ the split-K reduce) for a filled-in Tc2Args.
 template <bool kDirect>
 int launch_tc2(qg::Tc2Args &t, int64_t M, int64_t N, int64_t KT, void *sk_scratch, cudaStream_t st) {
@@ -675,9 +703,28 @@ int launch_tc2(qg::Tc2Args &t, int64_t M, int64_t N, int64_t KT, void *sk_scratc
   const int64_t rest = t.MT2 * t.NT - t.full;  // pairs split over K
   const int64_t grid = 2 * (t.full + rest * t.S);
   if (grid > INT32_MAX) return int(cudaErrorInvalidConfiguration);
+  const size_t window = tc2_l2_persist() ? tc2_persist_window(tc2_slot_bytes()) : 0;
   { int ti = tstart(kMain, st);
-  qg::qgemm_tc32_2cta_kernel<kDirect><<<unsigned(grid), qg::kTcThreads,
-                                       kDirect ? qg::kTc2DSmemBytes : qg::kTc2SmemBytes, st>>>(t);
+  if (window) {
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeAccessPolicyWindow;
+    at[0].val.accessPolicyWindow.base_ptr = t.tmp;
+    at[0].val.accessPolicyWindow.num_bytes = window;
+    at[0].val.accessPolicyWindow.hitRatio = 1.0f;
+    at[0].val.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
+    at[0].val.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(unsigned(grid));
+    cfg.blockDim = dim3(qg::kTcThreads);
+    cfg.dynamicSmemBytes = kDirect ? qg::kTc2DSmemBytes : qg::kTc2SmemBytes;
+    cfg.stream = st;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    cudaLaunchKernelEx(&cfg, qg::qgemm_tc32_2cta_kernel<kDirect>, t);
+  } else {
+    qg::qgemm_tc32_2cta_kernel<kDirect><<<unsigned(grid), qg::kTcThreads,
+                                         kDirect ? qg::kTc2DSmemBytes : qg::kTc2SmemBytes, st>>>(t);
+  }
   tstop(ti, st); }
   ++g_last_launches;
   if (t.S > 1) {
