@@ -94,7 +94,11 @@ int qgemm(char transA, char transB, int64_t M, int64_t N, int64_t K,
 /* FP32: same contract with float storage.  Arithmetic: 3xTF32 on the tcgen05
  * tensor cores with FP32 accumulation (hi/lo split of both operands), which
  * meets the FP32 tolerance where 1xTF32 does not; the small-
- * problem path below computes in FP64 and rounds once on store. */
+ * problem path below computes in FP64 and rounds once on store.
+ * Environment (read once per process): QG_TC2_L2_PERSIST=1 launches the FP32
+ * mainloop under a persisting-L2 access-policy window over its running-sum
+ * scratch and raises cudaLimitPersistingL2CacheSize on the device once
+ * (device-wide state, hence opt-in); results are identical. */
 int qgemm_f32(char transA, char transB, int64_t M, int64_t N, int64_t K,
               const float alpha[4], const float *A, int64_t lda,
               const float *B, int64_t ldb, const float beta[4],
